@@ -1,0 +1,185 @@
+/*
+ * moeplace_b200.h -- C ABI of the B200-native distributed MoE-layer forward.
+ *
+ * The reference (`moeplace`, arXiv 2508.12851) is a pure-Python placement
+ * library + simulator; it has no FFI.  Its hot path -- the per-layer dispatch
+ * `_EventLoop._dispatch_layer` (reference pkg/src/moeplace/sim.py:441-463) with
+ * the target rule `_choose_target` (sim.py:433-439), the activation counting
+ * `ActivationStats.ingest` (stats.py:82-96), the analytic `comp_time` /
+ * `comm_time` estimators (cost.py:132-149) and the migration slot diff of
+ * `migration_cost` (cost.py:171-191) -- is replaced by the entry points below.
+ * Each entry point names the reference interface it replaces.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Device pointers are `void*` / typed
+ *     pointers into GPU memory; `stream` is a cudaStream_t passed as void*.
+ *   - Every call returns 0 (MP_OK) or a negative MP_E_* code; the message of
+ *     the last failure on the calling thread is available from mp_last_error.
+ *   - bf16 buffers are row-major, 2 bytes per element.
+ *   - The library owns only what mp_layer_create allocates (the NVLink-shared
+ *     window, the expert-weight slot pool and per-layer scratch); caller
+ *     buffers are never freed by the library.
+ *   - One host thread per mp_layer; calls on one layer are not re-entrant
+ *     (the reference event loop is single-threaded).
+ */
+#ifndef MOEPLACE_B200_H
+#define MOEPLACE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MP_ABI_VERSION 1
+
+#define MP_OK 0
+#define MP_E_ARG -1        /* bad argument (null pointer, unknown mode)                  */
+#define MP_E_SHAPE -2      /* shape mismatch      -> moeplace.DimensionMismatch           */
+#define MP_E_CAPACITY -3   /* slot / buffer cap   -> moeplace.InfeasibleError             */
+#define MP_E_UNPLACED -4   /* route w/o holder    -> moeplace.UnplacedExpertError         */
+#define MP_E_CUDA -5       /* CUDA runtime / driver failure -> RuntimeError               */
+#define MP_E_PEER -6       /* IPC / NVLink peer failure or barrier timeout -> RuntimeError */
+
+/* Router score modes (public model definitions; the reference has no router,
+ * SPEC.md:416). */
+#define MP_SCORE_TOPK_SOFTMAX 0 /* Mixtral: top-k logits, softmax over the k            */
+#define MP_SCORE_SOFTMAX_TOPK 1 /* Qwen1.5-MoE / DeepSeek-V2-Lite: softmax over E, top-k */
+
+int mp_abi_version(void);
+/* Copies the last error message of the calling thread (NUL-terminated). */
+int mp_last_error(char* buf, int buf_len);
+
+/* ------------------------------------------------------------------------
+ * Stateless kernels (used by the layer, exported for parity tests).
+ * --------------------------------------------------------------------- */
+
+/* Repack router weights Wg [E_tot, d] bf16 into the kernel layout
+ * [d/4][E_tot][4] fp32 (E_tot = E, or E+1 with the shared-expert gate row). */
+int mp_router_pack(const void* wg_bf16, int E_tot, int d, float* packed, void* stream);
+
+/* K1 -- replaces ActivationStats.ingest (stats.py:82-96) fed by sampled expert
+ * sets (sim.py:181-185): top-k routing of T tokens plus a fused histogram.
+ *   x        [T, d] bf16           packed  from mp_router_pack (E + has_gate rows)
+ *   bias     [E] fp32 or NULL      per-origin routing skew (log p, sim.py:161-164)
+ *   idx      [T, k] int32 out      experts, descending logit, ties -> lower id
+ *   w        [T, k] fp32 out       gate weights
+ *   gate_out [T] fp32 out or NULL  sigmoid shared-expert gate (has_gate = 1)
+ *   hist     [E] uint32 in/out     += tokens routed to each expert (token_count 1)
+ */
+int mp_router_topk_hist(const void* x, const float* packed, const float* bias, int T, int d, int E, int has_gate,
+                        int k, int score_mode, int renorm, int32_t* idx, float* w, float* gate_out, uint32_t* hist,
+                        void* stream);
+
+/* K3 -- replaces comp_time (cost.py:132-136).  Grouped GEMM on tcgen05:
+ *   for g < *n_groups: rows [a_row, a_row+m) of A [a_rows, K] times slot `slot`
+ *   of B (rows slot*N .. slot*N+N of B [b_rows, K]) -> out rows [o_row, o_row+m).
+ *   swiglu = 1: B holds interleaved gate/up blocks of 128 rows, out [*, N/2].
+ *   groups (device) = n x {a_row, m, slot, o_row}; n_groups (device) int32.   */
+int mp_grouped_gemm(const void* a, int64_t a_rows, const void* b, int64_t b_rows, const int32_t* groups,
+                    const int32_t* n_groups, int N, int K, void* out, int out_ld, int swiglu, void* stream);
+
+/* ------------------------------------------------------------------------
+ * The MoE layer: one per (process, GPU); rank r of G ranks = reference server r
+ * with one GPU (ClusterSpec servers, domain.py:73-155).
+ * --------------------------------------------------------------------- */
+typedef struct mp_layer mp_layer;
+
+typedef struct mp_layer_desc {
+  int32_t rank;         /* this GPU = reference server id                      */
+  int32_t world;        /* G: number of GPUs (servers), 1..8                    */
+  int32_t device;       /* CUDA device ordinal                                   */
+  int32_t max_tokens;   /* T capacity per forward on this origin                */
+  int32_t d;            /* hidden width  (ModelSpec.hidden_width)               */
+  int32_t f;            /* expert FFN width                                     */
+  int32_t E;            /* routed experts (ModelSpec.experts_per_layer[l])      */
+  int32_t top_k;        /* ModelSpec.top_k                                      */
+  int32_t score_mode;   /* MP_SCORE_*                                           */
+  int32_t renorm;       /* renormalise top-k weights (softmax_topk mode)        */
+  int32_t n_slots;      /* expert slots on this GPU: floor(GpuSpec.memory / m_e) */
+  int32_t shared_f;     /* shared-expert FFN width, 0 = none                    */
+  int32_t shared_gate;  /* 1: shared output scaled by sigmoid(x . w_sg)          */
+} mp_layer_desc;
+
+/* Device pointers of the layer's buffers (for filling weights and for
+ * parity inspection).  Sizes in elements. */
+typedef struct mp_layer_ptrs {
+  void* w13_pool;    /* [n_slots][2f][d] bf16, gate/up interleaved per 128 rows  */
+  void* w2_pool;     /* [n_slots][d][f] bf16                                     */
+  void* wg;          /* [E + shared_gate][d] bf16 router weights (packed on set)  */
+  float* bias;       /* [E] fp32                                                 */
+  void* w13_shared;  /* [2*shared_f][d] bf16 or NULL                             */
+  void* w2_shared;   /* [d][shared_f] bf16 or NULL                               */
+  int32_t* idx;      /* [max_tokens][k]                                          */
+  float* w;          /* [max_tokens][k]                                          */
+  int32_t* pos_dst;  /* [max_tokens][k] target GPU of each (token, slot)         */
+  int32_t* pos_row;  /* [max_tokens][k] row in the target's receive buffer       */
+  void* recv;        /* [recv_cap][d] bf16 rows received for local experts       */
+  void* h;           /* [recv_cap][f] bf16 SwiGLU activations                    */
+  void* y;           /* [recv_cap][d] bf16 expert outputs                        */
+  uint32_t* hist;    /* [E] cumulative activation histogram (this origin)        */
+  int32_t* counts;   /* [2][G][E] exchanged batch counts C[src][e] (parity halves) */
+  int32_t* groups;   /* [E][4] local GEMM groups                                 */
+  int32_t* n_groups; /* [1]                                                      */
+  float* shared_gate;/* [max_tokens] or NULL                                     */
+  int64_t recv_cap;  /* rows                                                     */
+  int64_t slot_bytes;/* bytes of one expert slot (w13 + w2) = ModelSpec.expert_size */
+} mp_layer_ptrs;
+
+int mp_layer_create(const mp_layer_desc* desc, mp_layer** out);
+int mp_layer_destroy(mp_layer* layer);
+int mp_layer_get_ptrs(mp_layer* layer, mp_layer_ptrs* out);
+
+/* NVLink window setup (G > 1): export this rank's IPC handles (2 x 64 bytes:
+ * exchange window, weight pool), then open all ranks' handles (G x 128 bytes,
+ * ordered by rank; this rank's own entry is ignored). */
+int mp_layer_export_handles(mp_layer* layer, void* handles_out /* 128 bytes */);
+int mp_layer_open_peers(mp_layer* layer, const void* all_handles /* G * 128 bytes */);
+
+/* Route table -- replaces `_choose_target` (sim.py:433-439) evaluated per
+ * invocation: route[s*E + e] = target GPU for origin s and expert e (origin if
+ * it holds e, else the cheapest holder, ties to the lowest id); slot_of[e] =
+ * local slot holding e on this GPU or -1.  Host arrays; validated
+ * (MP_E_UNPLACED when a route points at a GPU without the expert here). */
+int mp_layer_set_routes(mp_layer* layer, const int32_t* route, const int32_t* slot_of, void* stream);
+
+/* Packs layer->wg (+ bias) after the caller filled them. */
+int mp_layer_prepare_router(mp_layer* layer, void* stream);
+
+/* One MoE-layer forward of T tokens originating on this GPU -- replaces
+ * `_dispatch_layer` (sim.py:441-463).  x, out: [T, d] bf16 device.  SPMD: all
+ * G ranks must call it with their own T.  Kernels: router+histogram, count
+ * exchange, layout, permute+dispatch (NVLink stores), shared expert, barrier,
+ * grouped SwiGLU GEMMs (tcgen05), barrier, combine+return (NVLink loads). */
+int mp_layer_forward(mp_layer* layer, const void* x, void* out, int T, void* stream);
+
+/* Number of kernels the last mp_layer_forward launched. */
+int mp_layer_last_launches(mp_layer* layer);
+
+/* Host copy of the last forward's exchanged count table C[src][e] (G*E int32;
+ * synchronises the stream).  C feeds the reference accounting: remote pairs
+ * (sim.py:452-456), remote_volume (cost.py:120-129). */
+int mp_layer_read_counts(mp_layer* layer, int32_t* host_counts, void* stream);
+
+/* Barrier/peer error word (0 = ok); synchronises the stream. */
+int mp_layer_check(mp_layer* layer, void* stream);
+
+/* K6 -- executes the slot diff of migration_cost (cost.py:186-187) adopted by
+ * should_migrate (cost.py:217-248): copy expert slots into local slots, from a
+ * peer GPU's pool over NVLink (src_rank != rank) or locally, on `stream`
+ * (a side stream), then record `done_event` (cudaEvent_t, may be NULL).  The
+ * caller swaps routes (mp_layer_set_routes) only after the event completes,
+ * matching migration_complete (sim.py:520-525). */
+typedef struct mp_copy_op {
+  int32_t src_rank;
+  int32_t src_slot;
+  int32_t dst_slot;
+} mp_copy_op;
+int mp_layer_migrate(mp_layer* layer, const mp_copy_op* ops, int n_ops, void* stream, void* done_event);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOEPLACE_B200_H */

@@ -1,0 +1,550 @@
+// extern "C" boundary (include/moeplace_b200.h) and the MoE layer object.
+//
+// The layer composes the kernels of one distributed MoE-layer forward; it is
+// the B200 counterpart of `_EventLoop._dispatch_layer` (reference
+// pkg/src/moeplace/sim.py:441-463).  Memory per GPU:
+//   pool    (IPC-exported)  expert weight slots, n_slots = floor(GpuSpec.memory / m_e)
+//                           (domain.py:395-401): the per-GPU memory cap is real
+//   window  (IPC-exported)  receive rows, expert outputs, count tables, flags
+//   scratch (private)       router/permutation state, SwiGLU activations, maps
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "mp_internal.h"
+
+namespace mp {
+
+static thread_local char g_err[1024] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* what) {
+  return set_error(MP_E_CUDA, "%s: %s (%d)", what, cudaGetErrorString(e), int(e));
+}
+
+}  // namespace mp
+
+using namespace mp;
+
+#define MP_CUDA(call)                                                  \
+  do {                                                                 \
+    cudaError_t _e = (call);                                           \
+    if (_e != cudaSuccess) return set_cuda_error(_e, #call);           \
+  } while (0)
+#define MP_TRY(call)                 \
+  do {                               \
+    int _r = (call);                 \
+    if (_r != MP_OK) return _r;      \
+  } while (0)
+
+struct mp_layer {
+  mp_layer_desc desc;
+  int G = 1, rank = 0, nb_max = 0;
+  int64_t recv_cap = 0;
+  size_t w13_slot_elems = 0, w2_slot_elems = 0, slot_bytes = 0;
+
+  // allocations
+  uint8_t* pool = nullptr;
+  size_t pool_bytes = 0;
+  uint8_t* window = nullptr;
+  size_t window_bytes = 0;
+  uint8_t* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  size_t off_recv = 0, off_y = 0, off_counts = 0, off_flags = 0;
+
+  // pool / window views
+  __nv_bfloat16 *w13 = nullptr, *w2 = nullptr, *recv = nullptr, *y = nullptr;
+  int32_t* counts = nullptr;
+  uint32_t* flags = nullptr;
+  // scratch views
+  __nv_bfloat16 *h = nullptr, *wg = nullptr, *w13s = nullptr, *w2s = nullptr, *hs = nullptr, *ys = nullptr;
+  float *wg_packed = nullptr, *bias = nullptr, *w = nullptr, *sgate = nullptr;
+  int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr, *blk_prefix = nullptr,
+          *batch_counts = nullptr, *my_base = nullptr, *groups = nullptr, *n_groups = nullptr,
+          *recv_rows = nullptr, *route_d = nullptr, *slot_of_d = nullptr, *sh_groups = nullptr,
+          *sh_ngroups = nullptr;
+  uint32_t *hist = nullptr, *err = nullptr;
+  void** ptr_arrays = nullptr;  // device: recv[8], y[8], flags[8], counts0[8], counts1[8]
+
+  uint8_t* peer_window[8] = {};
+  uint8_t* peer_pool[8] = {};
+  bool peers_open = false, routes_set = false, router_ready = false;
+
+  CUtensorMap tm_recv, tm_w13, tm_h, tm_w2, tm_w13s, tm_hs, tm_w2s, tm_x;
+  const void* tm_x_ptr = nullptr;
+  int tm_x_rows = -1;
+
+  uint32_t epoch = 0;
+  uint64_t fwd_count = 0;
+  int last_launches = 0;
+};
+
+namespace {
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Carver {
+  uint8_t* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = reinterpret_cast<T*>(base + off);
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+int validate_desc(const mp_layer_desc& d) {
+  if (d.world < 1 || d.world > 8) return set_error(MP_E_SHAPE, "world=%d outside [1, 8]", d.world);
+  if (d.rank < 0 || d.rank >= d.world) return set_error(MP_E_SHAPE, "rank=%d outside [0, %d)", d.rank, d.world);
+  if (d.max_tokens < 1) return set_error(MP_E_SHAPE, "max_tokens=%d", d.max_tokens);
+  if (d.E < 1 || d.E > 64) return set_error(MP_E_SHAPE, "E=%d outside [1, 64]", d.E);
+  if (d.top_k < 1 || d.top_k > 8 || d.top_k > d.E) return set_error(MP_E_SHAPE, "top_k=%d invalid", d.top_k);
+  if (d.d % 256 != 0) return set_error(MP_E_SHAPE, "hidden width d=%d must be a multiple of 256", d.d);
+  if (d.f % 128 != 0) return set_error(MP_E_SHAPE, "FFN width f=%d must be a multiple of 128", d.f);
+  if (d.shared_f % 128 != 0 || d.shared_f < 0)
+    return set_error(MP_E_SHAPE, "shared FFN width %d must be a multiple of 128", d.shared_f);
+  if (d.score_mode != MP_SCORE_TOPK_SOFTMAX && d.score_mode != MP_SCORE_SOFTMAX_TOPK)
+    return set_error(MP_E_ARG, "score_mode=%d", d.score_mode);
+  if (d.n_slots < 0) return set_error(MP_E_CAPACITY, "n_slots=%d", d.n_slots);
+  if (d.shared_gate && d.shared_f == 0) return set_error(MP_E_ARG, "shared_gate without a shared expert");
+  return MP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mp_abi_version(void) { return MP_ABI_VERSION; }
+
+int mp_last_error(char* buf, int buf_len) {
+  if (!buf || buf_len <= 0) return MP_E_ARG;
+  strncpy(buf, g_err, size_t(buf_len) - 1);
+  buf[buf_len - 1] = 0;
+  return MP_OK;
+}
+
+int mp_router_pack(const void* wg_bf16, int E_tot, int d, float* packed, void* stream) {
+  if (!wg_bf16 || !packed) return set_error(MP_E_ARG, "mp_router_pack: null pointer");
+  return launch_router_pack(static_cast<const __nv_bfloat16*>(wg_bf16), E_tot, d, packed,
+                            static_cast<cudaStream_t>(stream));
+}
+
+int mp_router_topk_hist(const void* x, const float* packed, const float* bias, int T, int d, int E, int has_gate,
+                        int k, int score_mode, int renorm, int32_t* idx, float* w, float* gate_out, uint32_t* hist,
+                        void* stream) {
+  if (!x || !packed || !idx || !w) return set_error(MP_E_ARG, "mp_router_topk_hist: null pointer");
+  return launch_router(static_cast<const __nv_bfloat16*>(x), packed, bias, T, d, E, has_gate, k, score_mode, renorm,
+                       idx, w, gate_out, hist, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+int mp_grouped_gemm(const void* a, int64_t a_rows, const void* b, int64_t b_rows, const int32_t* groups,
+                    const int32_t* n_groups, int N, int K, void* out, int out_ld, int swiglu, void* stream) {
+  if (!a || !b || !groups || !n_groups || !out) return set_error(MP_E_ARG, "mp_grouped_gemm: null pointer");
+  CUtensorMap ta, tb;
+  MP_TRY(encode_tmap_bf16_2d(&ta, a, uint64_t(a_rows), uint64_t(K), 128));
+  MP_TRY(encode_tmap_bf16_2d(&tb, b, uint64_t(b_rows), uint64_t(K), 256));
+  return launch_grouped_gemm(ta, tb, groups, n_groups, N, K, N, 0, static_cast<__nv_bfloat16*>(out), out_ld,
+                             swiglu, 0, static_cast<cudaStream_t>(stream));
+}
+
+int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
+  if (!desc || !out) return set_error(MP_E_ARG, "mp_layer_create: null pointer");
+  MP_TRY(validate_desc(*desc));
+  MP_CUDA(cudaSetDevice(desc->device));
+  cudaDeviceProp prop;
+  MP_CUDA(cudaGetDeviceProperties(&prop, desc->device));
+  if (prop.major != 10)
+    return set_error(MP_E_CUDA, "device %d is sm_%d%d; this library is built for sm_100a (B200)", desc->device,
+                     prop.major, prop.minor);
+
+  mp_layer* L = new mp_layer();
+  L->desc = *desc;
+  const mp_layer_desc& D = L->desc;
+  L->G = D.world;
+  L->rank = D.rank;
+  L->nb_max = (D.max_tokens + router_block_tokens() - 1) / router_block_tokens();
+  L->recv_cap = int64_t(D.world) * D.max_tokens * D.top_k;
+  L->w13_slot_elems = size_t(2) * D.f * D.d;
+  L->w2_slot_elems = size_t(D.d) * D.f;
+
+  auto fail = [&](int code) {
+    mp_layer_destroy(L);
+    return code;
+  };
+  cudaError_t e;
+
+  // ---- pool: slot s = [w13 (2f x d) | w2 (d x f)], exactly m_e = 3*d*f*2 bytes
+  L->slot_bytes = (L->w13_slot_elems + L->w2_slot_elems) * 2;
+  L->pool_bytes = std::max<size_t>(256, size_t(D.n_slots) * L->slot_bytes);
+  if ((e = cudaMalloc(&L->pool, L->pool_bytes)) != cudaSuccess)
+    return fail(set_error(MP_E_CAPACITY, "cannot allocate %d expert slots (%zu bytes): %s", D.n_slots,
+                          L->pool_bytes, cudaGetErrorString(e)));
+  L->w13 = reinterpret_cast<__nv_bfloat16*>(L->pool);
+  L->w2 = L->w13 + L->w13_slot_elems;
+
+  // ---- window (identical layout on every rank)
+  {
+    size_t off = 0;
+    L->off_recv = off;
+    off = align_up(off + size_t(L->recv_cap) * D.d * 2, 1024);
+    L->off_y = off;
+    off = align_up(off + size_t(L->recv_cap) * D.d * 2, 1024);
+    L->off_counts = off;
+    off = align_up(off + size_t(2) * 8 * 64 * 4, 256);
+    L->off_flags = off;
+    off = align_up(off + 64 * 4, 256);
+    L->window_bytes = off;
+  }
+  if ((e = cudaMalloc(&L->window, L->window_bytes)) != cudaSuccess)
+    return fail(set_error(MP_E_CAPACITY, "cannot allocate the exchange window (%zu bytes): %s", L->window_bytes,
+                          cudaGetErrorString(e)));
+  L->recv = reinterpret_cast<__nv_bfloat16*>(L->window + L->off_recv);
+  L->y = reinterpret_cast<__nv_bfloat16*>(L->window + L->off_y);
+  L->counts = reinterpret_cast<int32_t*>(L->window + L->off_counts);
+  L->flags = reinterpret_cast<uint32_t*>(L->window + L->off_flags);
+  if ((e = cudaMemset(L->window + L->off_counts, 0, L->window_bytes - L->off_counts)) != cudaSuccess)
+    return fail(set_cuda_error(e, "cudaMemset(window)"));
+
+  // ---- scratch
+  {
+    const int T = D.max_tokens, k = D.top_k, E = D.E;
+    const int E_tot = E + (D.shared_gate ? 1 : 0);
+    Carver c{nullptr};
+    auto plan = [&](Carver& cv) {
+      L->h = cv.take<__nv_bfloat16>(size_t(L->recv_cap) * D.f);
+      L->wg = cv.take<__nv_bfloat16>(size_t(E_tot) * D.d);
+      L->wg_packed = cv.take<float>(size_t(E_tot) * D.d);
+      L->bias = cv.take<float>(E);
+      L->w = cv.take<float>(size_t(T) * k);
+      L->sgate = D.shared_gate ? cv.take<float>(T) : nullptr;
+      L->idx = cv.take<int32_t>(size_t(T) * k);
+      L->pos_dst = cv.take<int32_t>(size_t(T) * k);
+      L->pos_row = cv.take<int32_t>(size_t(T) * k);
+      L->blk_counts = cv.take<int32_t>(size_t(L->nb_max) * E);
+      L->blk_prefix = cv.take<int32_t>(size_t(L->nb_max) * E);
+      L->batch_counts = cv.take<int32_t>(64);
+      L->my_base = cv.take<int32_t>(64);
+      L->groups = cv.take<int32_t>(64 * 4);
+      L->n_groups = cv.take<int32_t>(4);
+      L->recv_rows = cv.take<int32_t>(4);
+      L->route_d = cv.take<int32_t>(8 * 64);
+      L->slot_of_d = cv.take<int32_t>(64);
+      L->sh_groups = cv.take<int32_t>(4);
+      L->sh_ngroups = cv.take<int32_t>(4);
+      L->hist = cv.take<uint32_t>(64);
+      L->err = cv.take<uint32_t>(4);
+      L->ptr_arrays = cv.take<void*>(5 * 8);
+      if (D.shared_f > 0) {
+        L->w13s = cv.take<__nv_bfloat16>(size_t(2) * D.shared_f * D.d);
+        L->w2s = cv.take<__nv_bfloat16>(size_t(D.d) * D.shared_f);
+        L->hs = cv.take<__nv_bfloat16>(size_t(T) * D.shared_f);
+        L->ys = cv.take<__nv_bfloat16>(size_t(T) * D.d);
+      }
+    };
+    plan(c);
+    L->scratch_bytes = align_up(c.off, 256);
+    if ((e = cudaMalloc(&L->scratch, L->scratch_bytes)) != cudaSuccess)
+      return fail(set_error(MP_E_CAPACITY, "cannot allocate layer scratch (%zu bytes): %s", L->scratch_bytes,
+                            cudaGetErrorString(e)));
+    Carver real{L->scratch};
+    plan(real);
+    // zero the small control region (everything but the big activation buffers)
+    if ((e = cudaMemset(L->scratch, 0, L->scratch_bytes)) != cudaSuccess)
+      return fail(set_cuda_error(e, "cudaMemset(scratch)"));
+  }
+
+  // ---- own pointer arrays (peers filled by mp_layer_open_peers)
+  {
+    void* host[5 * 8] = {};
+    host[0 * 8 + L->rank] = L->recv;
+    host[1 * 8 + L->rank] = L->y;
+    host[2 * 8 + L->rank] = L->flags;
+    host[3 * 8 + L->rank] = L->counts;
+    host[4 * 8 + L->rank] = L->counts + L->G * D.E;
+    if ((e = cudaMemcpy(L->ptr_arrays, host, sizeof(host), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return fail(set_cuda_error(e, "cudaMemcpy(ptr arrays)"));
+  }
+
+  // ---- tensor maps over fixed buffers
+  int r;
+  if ((r = encode_tmap_bf16_2d(&L->tm_recv, L->recv, uint64_t(L->recv_cap), uint64_t(D.d), 128)) != MP_OK)
+    return fail(r);
+  if ((r = encode_tmap_bf16_2d(&L->tm_h, L->h, uint64_t(L->recv_cap), uint64_t(D.f), 128)) != MP_OK) return fail(r);
+  if (D.n_slots > 0) {
+    // W13 viewed as [n_slots * 3f, d] (slot s rows start at 3f*s); W2 as
+    // [n_slots * 3d, f] (slot s rows start at 3d*s + 2d)
+    if ((r = encode_tmap_bf16_2d(&L->tm_w13, L->pool, uint64_t(D.n_slots) * 3 * D.f, uint64_t(D.d), 256)) != MP_OK)
+      return fail(r);
+    if ((r = encode_tmap_bf16_2d(&L->tm_w2, L->pool, uint64_t(D.n_slots) * 3 * D.d, uint64_t(D.f), 256)) != MP_OK)
+      return fail(r);
+  }
+  if (D.shared_f > 0) {
+    if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
+      return fail(r);
+    if ((r = encode_tmap_bf16_2d(&L->tm_w2s, L->w2s, uint64_t(D.d), uint64_t(D.shared_f), 256)) != MP_OK)
+      return fail(r);
+    if ((r = encode_tmap_bf16_2d(&L->tm_hs, L->hs, uint64_t(D.max_tokens), uint64_t(D.shared_f), 128)) != MP_OK)
+      return fail(r);
+  }
+  if (L->G == 1) L->peers_open = true;
+  *out = L;
+  return MP_OK;
+}
+
+int mp_layer_destroy(mp_layer* L) {
+  if (!L) return MP_OK;
+  cudaSetDevice(L->desc.device);
+  for (int p = 0; p < 8; ++p) {
+    if (L->peer_window[p]) cudaIpcCloseMemHandle(L->peer_window[p]);
+    if (L->peer_pool[p]) cudaIpcCloseMemHandle(L->peer_pool[p]);
+  }
+  if (L->scratch) cudaFree(L->scratch);
+  if (L->window) cudaFree(L->window);
+  if (L->pool) cudaFree(L->pool);
+  delete L;
+  return MP_OK;
+}
+
+int mp_layer_get_ptrs(mp_layer* L, mp_layer_ptrs* o) {
+  if (!L || !o) return set_error(MP_E_ARG, "mp_layer_get_ptrs: null pointer");
+  memset(o, 0, sizeof(*o));
+  o->w13_pool = L->w13;
+  o->w2_pool = L->w2;
+  o->wg = L->wg;
+  o->bias = L->bias;
+  o->w13_shared = L->w13s;
+  o->w2_shared = L->w2s;
+  o->idx = L->idx;
+  o->w = L->w;
+  o->pos_dst = L->pos_dst;
+  o->pos_row = L->pos_row;
+  o->recv = L->recv;
+  o->h = L->h;
+  o->y = L->y;
+  o->hist = L->hist;
+  o->counts = L->counts;
+  o->groups = L->groups;
+  o->n_groups = L->n_groups;
+  o->shared_gate = L->sgate;
+  o->recv_cap = L->recv_cap;
+  o->slot_bytes = int64_t(L->slot_bytes);
+  return MP_OK;
+}
+
+int mp_layer_export_handles(mp_layer* L, void* handles_out) {
+  if (!L || !handles_out) return set_error(MP_E_ARG, "mp_layer_export_handles: null pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  MP_CUDA(cudaSetDevice(L->desc.device));
+  cudaIpcMemHandle_t hw, hp;
+  MP_CUDA(cudaIpcGetMemHandle(&hw, L->window));
+  MP_CUDA(cudaIpcGetMemHandle(&hp, L->pool));
+  memcpy(handles_out, &hw, 64);
+  memcpy(static_cast<uint8_t*>(handles_out) + 64, &hp, 64);
+  return MP_OK;
+}
+
+int mp_layer_open_peers(mp_layer* L, const void* all_handles) {
+  if (!L || !all_handles) return set_error(MP_E_ARG, "mp_layer_open_peers: null pointer");
+  MP_CUDA(cudaSetDevice(L->desc.device));
+  const uint8_t* h = static_cast<const uint8_t*>(all_handles);
+  void* host[5 * 8] = {};
+  for (int p = 0; p < L->G; ++p) {
+    uint8_t* win;
+    if (p == L->rank) {
+      win = L->window;
+    } else {
+      if (!L->peer_window[p]) {
+        cudaIpcMemHandle_t hw, hp;
+        memcpy(&hw, h + 128 * p, 64);
+        memcpy(&hp, h + 128 * p + 64, 64);
+        void* pw = nullptr;
+        void* pp = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&pw, hw, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess)
+          return set_error(MP_E_PEER, "cudaIpcOpenMemHandle(window of rank %d): %s", p, cudaGetErrorString(e));
+        e = cudaIpcOpenMemHandle(&pp, hp, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess)
+          return set_error(MP_E_PEER, "cudaIpcOpenMemHandle(pool of rank %d): %s", p, cudaGetErrorString(e));
+        L->peer_window[p] = static_cast<uint8_t*>(pw);
+        L->peer_pool[p] = static_cast<uint8_t*>(pp);
+      }
+      win = L->peer_window[p];
+    }
+    host[0 * 8 + p] = win + L->off_recv;
+    host[1 * 8 + p] = win + L->off_y;
+    host[2 * 8 + p] = win + L->off_flags;
+    host[3 * 8 + p] = win + L->off_counts;
+    host[4 * 8 + p] = win + L->off_counts + size_t(L->G) * L->desc.E * 4;
+  }
+  MP_CUDA(cudaMemcpy(L->ptr_arrays, host, sizeof(host), cudaMemcpyHostToDevice));
+  L->peers_open = true;
+  return MP_OK;
+}
+
+int mp_layer_set_routes(mp_layer* L, const int32_t* route, const int32_t* slot_of, void* stream) {
+  if (!L || !route || !slot_of) return set_error(MP_E_ARG, "mp_layer_set_routes: null pointer");
+  const int G = L->G, E = L->desc.E;
+  for (int s = 0; s < G; ++s)
+    for (int e = 0; e < E; ++e) {
+      const int t = route[s * E + e];
+      if (t < 0 || t >= G)
+        return set_error(MP_E_UNPLACED, "expert %d routed from GPU %d to GPU %d: placed nowhere", e, s, t);
+      if (t == L->rank && (slot_of[e] < 0 || slot_of[e] >= L->desc.n_slots))
+        return set_error(MP_E_UNPLACED, "expert %d of GPU %d's traffic is routed here but holds no slot (slot %d)", e,
+                         s, slot_of[e]);
+    }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MP_CUDA(cudaSetDevice(L->desc.device));
+  // small synchronous staging: route tables change once per placement
+  std::vector<int32_t> r(route, route + G * E), so(slot_of, slot_of + E);
+  MP_CUDA(cudaMemcpyAsync(L->route_d, r.data(), r.size() * 4, cudaMemcpyHostToDevice, st));
+  MP_CUDA(cudaMemcpyAsync(L->slot_of_d, so.data(), so.size() * 4, cudaMemcpyHostToDevice, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  L->routes_set = true;
+  return MP_OK;
+}
+
+int mp_layer_prepare_router(mp_layer* L, void* stream) {
+  if (!L) return set_error(MP_E_ARG, "mp_layer_prepare_router: null layer");
+  MP_CUDA(cudaSetDevice(L->desc.device));
+  MP_TRY(launch_router_pack(L->wg, L->desc.E + (L->desc.shared_gate ? 1 : 0), L->desc.d, L->wg_packed,
+                            static_cast<cudaStream_t>(stream)));
+  L->router_ready = true;
+  return MP_OK;
+}
+
+int mp_layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream) {
+  if (!L) return set_error(MP_E_ARG, "mp_layer_forward: null layer");
+  if ((!x || !out) && T > 0) return set_error(MP_E_ARG, "mp_layer_forward: null x/out with T=%d", T);
+  const mp_layer_desc& D = L->desc;
+  if (T < 0 || T > D.max_tokens) return set_error(MP_E_SHAPE, "T=%d exceeds max_tokens=%d", T, D.max_tokens);
+  if (!L->routes_set) return set_error(MP_E_UNPLACED, "mp_layer_forward: route table not set");
+  if (!L->router_ready) return set_error(MP_E_ARG, "mp_layer_forward: router weights not prepared");
+  if (!L->peers_open) return set_error(MP_E_PEER, "mp_layer_forward: peers not opened (G=%d)", L->G);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int G = L->G, E = D.E, k = D.top_k, rank = L->rank;
+  const int nb = (T + router_block_tokens() - 1) / router_block_tokens();
+  const int par = int(L->fwd_count & 1);
+  auto** recv_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 0 * 8);
+  auto** y_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 1 * 8);
+  auto** flag_ptrs = reinterpret_cast<uint32_t**>(L->ptr_arrays + 2 * 8);
+  auto** count_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + (3 + par) * 8);
+  int launches = 0;
+
+  if (D.shared_f > 0 && T > 0 && (L->tm_x_ptr != x || L->tm_x_rows != T)) {
+    MP_TRY(encode_tmap_bf16_2d(&L->tm_x, x, uint64_t(std::max(T, 1)), uint64_t(D.d), 128));
+    L->tm_x_ptr = x;
+    L->tm_x_rows = T;
+  }
+
+  MP_CUDA(cudaMemsetAsync(L->batch_counts, 0, size_t(E) * 4, st));
+  MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
+                       D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts, st));
+  ++launches;
+  const int32_t* counts_all = L->batch_counts;
+  if (G > 1) {
+    MP_TRY(launch_publish_barrier(flag_ptrs, count_ptrs, L->batch_counts, E, G, rank, ++L->epoch, L->err, st));
+    ++launches;
+    counts_all = L->counts + size_t(par) * G * E;
+  }
+  MP_TRY(launch_layout(counts_all, L->route_d, L->slot_of_d, L->blk_counts, nb, G, E, rank, L->my_base,
+                       L->blk_prefix, L->groups, L->n_groups, L->recv_rows, st));
+  ++launches;
+  MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d + rank * E, L->my_base,
+                        L->blk_prefix, T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st));
+  ++launches;
+  if (D.shared_f > 0 && T > 0) {
+    const int32_t hg[4] = {0, T, 0, 0};
+    // group table of the dense shared expert: one group of all T local tokens
+    MP_CUDA(cudaMemcpyAsync(L->sh_groups, hg, sizeof(hg), cudaMemcpyHostToDevice, st));
+    const int32_t one = 1;
+    MP_CUDA(cudaMemcpyAsync(L->sh_ngroups, &one, 4, cudaMemcpyHostToDevice, st));
+    MP_TRY(launch_grouped_gemm(L->tm_x, L->tm_w13s, L->sh_groups, L->sh_ngroups, 2 * D.shared_f, D.d, 0, 0, L->hs,
+                               D.shared_f, 1, 0, st));
+    MP_TRY(launch_grouped_gemm(L->tm_hs, L->tm_w2s, L->sh_groups, L->sh_ngroups, D.d, D.shared_f, 0, 0, L->ys, D.d,
+                               0, 0, st));
+    launches += 2;
+  }
+  if (G > 1) {
+    MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, ++L->epoch, L->err, st));
+    ++launches;
+  }
+  if (D.n_slots > 0) {
+    MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, L->groups, L->n_groups, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f,
+                               1, 0, st));
+    MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, L->groups, L->n_groups, D.d, D.f, 3 * D.d, 2 * D.d, L->y, D.d, 0,
+                               0, st));
+    launches += 2;
+  }
+  if (G > 1) {
+    MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, ++L->epoch, L->err, st));
+    ++launches;
+  }
+  MP_TRY(launch_combine(y_ptrs, L->pos_dst, L->pos_row, L->w, T, D.d, k, D.shared_f > 0 ? L->ys : nullptr,
+                        D.shared_gate ? L->sgate : nullptr, static_cast<__nv_bfloat16*>(out), st));
+  ++launches;
+  L->last_launches = launches;
+  ++L->fwd_count;
+  return MP_OK;
+}
+
+int mp_layer_last_launches(mp_layer* L) { return L ? L->last_launches : 0; }
+
+int mp_layer_read_counts(mp_layer* L, int32_t* host_counts, void* stream) {
+  if (!L || !host_counts) return set_error(MP_E_ARG, "mp_layer_read_counts: null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MP_CUDA(cudaStreamSynchronize(st));
+  const int G = L->G, E = L->desc.E;
+  if (G == 1) {
+    MP_CUDA(cudaMemcpy(host_counts, L->batch_counts, size_t(E) * 4, cudaMemcpyDeviceToHost));
+  } else {
+    const int par = int((L->fwd_count + 1) & 1);  // parity of the last completed forward
+    MP_CUDA(cudaMemcpy(host_counts, L->counts + size_t(par) * G * E, size_t(G) * E * 4, cudaMemcpyDeviceToHost));
+  }
+  return MP_OK;
+}
+
+int mp_layer_check(mp_layer* L, void* stream) {
+  if (!L) return set_error(MP_E_ARG, "mp_layer_check: null layer");
+  MP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  uint32_t err = 0;
+  MP_CUDA(cudaMemcpy(&err, L->err, 4, cudaMemcpyDeviceToHost));
+  if (err) return set_error(MP_E_PEER, "NVLink barrier timed out waiting for ranks mask 0x%x", err);
+  return MP_OK;
+}
+
+int mp_layer_migrate(mp_layer* L, const mp_copy_op* ops, int n_ops, void* stream, void* done_event) {
+  if (!L || (n_ops > 0 && !ops)) return set_error(MP_E_ARG, "mp_layer_migrate: null pointer");
+  MP_CUDA(cudaSetDevice(L->desc.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int S = L->desc.n_slots;
+  for (int i = 0; i < n_ops; ++i) {
+    const mp_copy_op& op = ops[i];
+    if (op.dst_slot < 0 || op.dst_slot >= S)
+      return set_error(MP_E_CAPACITY, "migration target slot %d outside [0, %d)", op.dst_slot, S);
+    if (op.src_rank < 0 || op.src_rank >= L->G) return set_error(MP_E_ARG, "migration source rank %d", op.src_rank);
+    if (op.src_slot < 0) return set_error(MP_E_ARG, "migration source slot %d", op.src_slot);
+    const uint8_t* src_pool = op.src_rank == L->rank ? L->pool : L->peer_pool[op.src_rank];
+    if (!src_pool) return set_error(MP_E_PEER, "pool of rank %d not opened", op.src_rank);
+    if (op.src_rank == L->rank && op.src_slot == op.dst_slot) continue;
+    // one contiguous m_e-byte copy per slot; peer sources go over NVLink
+    MP_CUDA(cudaMemcpyAsync(L->pool + size_t(op.dst_slot) * L->slot_bytes, src_pool + size_t(op.src_slot) * L->slot_bytes,
+                            L->slot_bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  if (done_event) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(done_event), st));
+  return MP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,306 @@
+// K3: grouped expert FFN on the 5th-generation tensor cores (sm_100a).
+//
+// Stands in for the reference's analytic compute estimate
+// `comp_time = (comp_base + comp_per_token * tokens) * load` (reference
+// pkg/src/moeplace/cost.py:132-136): here the expert work is real.
+//
+// For every local expert slot s with M_s routed rows (contiguous in the
+// receive buffer), the layer runs two launches of one persistent kernel:
+//   GEMM1  H[M_s, f] = silu(X W1^T) * (X W3^T)      (SwiGLU fused in the epilogue)
+//   GEMM2  Y[M_s, d] = H W2^T
+// W13 is stored per slot as [2f, d] with gate/up rows interleaved in blocks of
+// 128 (rows 256b..256b+127 = gate rows 128b.., rows 256b+128.. = up rows
+// 128b..), so one 128x256 accumulator tile holds matching gate and up columns.
+//
+// Kernel anatomy (one CTA per SM, persistent, static round-robin tiles):
+//   warp 0      TMA producer: A (128x64) + B (256x64) bf16 tiles, 128B swizzle,
+//               4-stage smem ring guarded by full/empty mbarriers
+//   warp 1      MMA issuer: one thread issues tcgen05.mma M=128 N=256 K=16 into
+//               a double-buffered TMEM accumulator (2 x 256 fp32 columns)
+//   warp 2      TMEM allocator (512 columns)
+//   warps 4..7  epilogue: tcgen05.ld -> (SwiGLU) -> bf16 -> global
+#include "common.cuh"
+#include "mp_internal.h"
+
+namespace mp {
+
+namespace gg {
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int kStages = 4;
+constexpr int kABytes = BM * BK * 2;  // 16 KB
+constexpr int kBBytes = BN * BK * 2;  // 32 KB
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kMaxGroups = 128;
+constexpr int kThreads = 256;
+constexpr int kTmemCols = 512;
+constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * kStageBytes + 4096;
+}  // namespace gg
+
+struct GemmSmemTail {
+  uint64_t full[gg::kStages];
+  uint64_t empty[gg::kStages];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  int n_groups;
+  int total_tiles;
+  int tile_prefix[gg::kMaxGroups + 1];
+  int g_arow[gg::kMaxGroups];
+  int g_m[gg::kMaxGroups];
+  int g_slot[gg::kMaxGroups];
+  int g_orow[gg::kMaxGroups];
+};
+
+struct TileCoord {
+  int g, m_blk, n_blk;
+};
+
+MP_DEV TileCoord decode_tile(const GemmSmemTail& s, int tile, int n_blocks) {
+  int g = 0;
+  while (s.tile_prefix[g + 1] <= tile) ++g;
+  const int local = tile - s.tile_prefix[g];
+  const int m_blocks = (s.g_m[g] + gg::BM - 1) / gg::BM;
+  TileCoord c;
+  c.g = g;
+  c.n_blk = local / m_blocks;
+  c.m_blk = local - c.n_blk * m_blocks;
+  return c;
+}
+
+__global__ void __launch_bounds__(gg::kThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const int32_t* __restrict__ groups, const int32_t* __restrict__ n_groups_dev,
+                        int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out,
+                        int out_ld, int swiglu) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + gg::kStages * gg::kABytes;
+  GemmSmemTail& st = *reinterpret_cast<GemmSmemTail*>(smem + gg::kStages * gg::kStageBytes);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int n_blocks = N / gg::BN;
+  const int k_blocks = K / gg::BK;
+
+  // ---- prologue: group table -> smem, barriers, TMEM
+  if (threadIdx.x == 0) {
+    int ng = *n_groups_dev;
+    if (ng > gg::kMaxGroups) ng = gg::kMaxGroups;
+    st.n_groups = ng;
+  }
+  __syncthreads();
+  const int ng = st.n_groups;
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+    st.g_arow[g] = groups[4 * g + 0];
+    st.g_m[g] = groups[4 * g + 1];
+    st.g_slot[g] = groups[4 * g + 2];
+    st.g_orow[g] = groups[4 * g + 3];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    st.tile_prefix[0] = 0;
+    for (int g = 0; g < ng; ++g) {
+      acc += ((st.g_m[g] + gg::BM - 1) / gg::BM) * n_blocks;
+      st.tile_prefix[g + 1] = acc;
+    }
+    st.total_tiles = acc;
+    for (int i = 0; i < gg::kStages; ++i) {
+      mbar_init(&st.full[i], 1);
+      mbar_init(&st.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&st.tfull[i], 1);
+      mbar_init(&st.tempty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 2) tmem_alloc<gg::kTmemCols>(&st.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = st.tmem_base;
+  const int total = st.total_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const TileCoord c = decode_tile(st, tile, n_blocks);
+        const int a_row = st.g_arow[c.g] + c.m_blk * gg::BM;
+        const int b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * gg::BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&st.empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&st.full[stage], gg::kStageBytes);
+          tma_load_2d(smA + stage * gg::kABytes, &tmA, &st.full[stage], kb * gg::BK, a_row);
+          tma_load_2d(smB + stage * gg::kBBytes, &tmB, &st.full[stage], kb * gg::BK, b_row);
+          if (++stage == gg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer
+      constexpr uint32_t idesc = make_idesc_bf16(gg::BM, gg::BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        mbar_wait(&st.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * gg::BN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&st.full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = make_sdesc_sw128(smem_u32(smA + stage * gg::kABytes));
+          const uint64_t bdesc = make_sdesc_sw128(smem_u32(smB + stage * gg::kBBytes));
+#pragma unroll
+          for (int k = 0; k < gg::BK / 16; ++k) {
+            // advance 16 bf16 (32 B) along K inside the 128 B swizzle atom
+            umma_bf16(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc,
+                      (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&st.empty[stage]);
+          if (++stage == gg::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&st.tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue (warp w owns TMEM lanes 32*(w%4) .. +31)
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const TileCoord c = decode_tile(st, tile, n_blocks);
+      const int row = c.m_blk * gg::BM + q * 32 + lane;
+      const bool valid = row < st.g_m[c.g];
+      const size_t orow = size_t(st.g_orow[c.g] + row);
+      mbar_wait(&st.tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * gg::BN);
+      if (swiglu) {
+        __nv_bfloat16* dst = out + orow * size_t(out_ld) + size_t(c.n_blk) * (gg::BN / 2);
+#pragma unroll 1
+        for (int cc = 0; cc < gg::BN / 2; cc += 32) {
+          uint32_t gv[32], uv[32];
+          tmem_ld_32x32b_x32(taddr + cc, gv);
+          tmem_ld_32x32b_x32(taddr + gg::BN / 2 + cc, uv);
+          tmem_ld_wait();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float g0 = __uint_as_float(gv[2 * i]), g1 = __uint_as_float(gv[2 * i + 1]);
+            float u0 = __uint_as_float(uv[2 * i]), u1 = __uint_as_float(uv[2 * i + 1]);
+            float h0 = g0 / (1.0f + __expf(-g0)) * u0;
+            float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+            packed[i] = pack_bf16x2(h0, h1);
+          }
+          if (valid) {
+            uint4* p = reinterpret_cast<uint4*>(dst + cc);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              p[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          }
+        }
+      } else {
+        __nv_bfloat16* dst = out + orow * size_t(out_ld) + size_t(c.n_blk) * gg::BN;
+#pragma unroll 1
+        for (int cc = 0; cc < gg::BN; cc += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(taddr + cc, v);
+          tmem_ld_wait();
+          uint32_t packed[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+          if (valid) {
+            uint4* p = reinterpret_cast<uint4*>(dst + cc);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              p[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st.tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<gg::kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return set_error(MP_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  if (cols % 64 != 0) return set_error(MP_E_SHAPE, "tensor map inner dimension %llu not a multiple of 64",
+                                       (unsigned long long)cols);
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(MP_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return MP_OK;
+}
+
+int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const int32_t* groups,
+                        const int32_t* n_groups_dev, int N, int K, int b_slot_stride, int b_offset,
+                        __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream) {
+  if (N % gg::BN != 0) return set_error(MP_E_SHAPE, "grouped GEMM N=%d not a multiple of %d", N, gg::BN);
+  if (K % gg::BK != 0) return set_error(MP_E_SHAPE, "grouped GEMM K=%d not a multiple of %d", K, gg::BK);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(gg::kSmemBytes));
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(grouped_gemm)");
+    attr_set = true;
+  }
+  if (grid <= 0) grid = kNumSMs;
+  grouped_gemm_kernel<<<grid, gg::kThreads, gg::kSmemBytes, stream>>>(tmA, tmB, groups, n_groups_dev, N, K,
+                                                                      b_slot_stride, b_offset, out, out_ld, swiglu);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_kernel launch");
+  return MP_OK;
+}
+
+}  // namespace mp

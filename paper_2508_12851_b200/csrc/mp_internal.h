@@ -1,0 +1,54 @@
+// Internal (C++) declarations shared by the kernel translation units and the
+// C-ABI layer in abi.cu.  Nothing here crosses the extern "C" boundary.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/moeplace_b200.h"
+
+namespace mp {
+
+// Error state (thread-local, read through mp_last_error).
+int set_error(int code, const char* fmt, ...);
+int set_cuda_error(cudaError_t e, const char* what);
+
+// ---- K1 router
+int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* bias, int T, int d, int E,
+                  int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
+                  uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, cudaStream_t stream);
+int router_block_tokens();
+int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, float* packed, cudaStream_t stream);
+
+// ---- layout (count exchange result -> offsets, group table)
+int launch_layout(const int32_t* counts_all /*[G][E]*/, const int32_t* route /*[G][E]*/,
+                  const int32_t* slot_of /*[E]*/, const int32_t* blk_counts /*[nb][E]*/, int nb, int G, int E,
+                  int rank, int32_t* my_base /*[E]*/, int32_t* blk_prefix /*[nb][E]*/, int32_t* groups /*[E][4]*/,
+                  int32_t* n_groups, int32_t* recv_rows, cudaStream_t stream);
+
+// ---- K2 permute (+ dispatch through peer pointers)
+int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route_row /*[E] for this origin*/,
+                   const int32_t* my_base, const int32_t* blk_prefix, int T, int d, int E, int k,
+                   __nv_bfloat16* const* recv_ptrs /*[G] device array*/, int32_t* pos_dst, int32_t* pos_row,
+                   cudaStream_t stream);
+
+// ---- K3 grouped GEMM
+int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const int32_t* groups,
+                        const int32_t* n_groups_dev, int N, int K, int b_slot_stride, int b_offset,
+                        __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream);
+
+// ---- K5 combine (+ return through peer pointers)
+int launch_combine(__nv_bfloat16* const* y_ptrs /*[G] device array*/, const int32_t* pos_dst,
+                   const int32_t* pos_row, const float* w, int T, int d, int k, const __nv_bfloat16* shared_y,
+                   const float* shared_gate, __nv_bfloat16* out, cudaStream_t stream);
+
+// ---- exchange / barrier over NVLink peer memory
+int launch_publish_barrier(uint32_t* const* flag_ptrs /*[G] device array, each -> flags[G]*/,
+                           int32_t* const* count_ptrs /*[G] device array, each -> table[G][E] or null*/,
+                           const int32_t* my_counts, int E, int G, int rank, uint32_t epoch,
+                           uint32_t* error_word, cudaStream_t stream);
+
+}  // namespace mp

@@ -1,0 +1,298 @@
+"""`B200MoELayer`: the GPU drop-in for the reference's per-layer dispatch.
+
+One object per (process, GPU).  It owns an `mp_layer` of the C ABI
+(include/moeplace_b200.h) and exposes the reference-facing operations:
+
+* `set_placement(placement, cluster)` -- route table by `_choose_target`'s rule
+  (sim.py:433-439) + expert slots filled from a weight source;
+* `forward(x)` -- one MoE-layer forward, the counterpart of `_dispatch_layer`
+  (sim.py:441-463), all kernels hand-written for sm_100a;
+* `activation_counts()` / `activation_stats()` -- the fused GPU histogram as
+  reference `ActivationStats.from_counts` (stats.py:67-80);
+* `dispatch_accounting()` -- remote invocations / bytes of the last forward in
+  the reference's accounting (sim.py:452-456);
+* `migrate(...)` -- executes `migration_cost`'s slot diff (cost.py:186-187)
+  with NVLink peer copies on a side stream, then swaps routes after
+  completion (sim.py:520-525).
+
+PyTorch is used for device memory views, streams and `torch.distributed`
+plumbing only; every kernel on the path lives in the CUDA library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from ctypes import byref, c_void_p
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InfeasibleError
+from .routing import dispatch_accounting, gpu_expert_sets, route_table_for, server_expert_sets, route_table
+from .shapes import LayerShape
+
+
+class _CudaBuf:
+    """Minimal __cuda_array_interface__ exporter for library-owned memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _view(ptr: int, shape, dtype: torch.dtype, device: torch.device) -> torch.Tensor:
+    typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.int32: "<i4"}[dtype]
+    t = torch.as_tensor(_CudaBuf(ptr, shape, typestr), device=device)
+    return t.view(torch.bfloat16) if dtype is torch.bfloat16 else t
+
+
+def interleave_w13(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
+    """[2f, d]: per 128-row block b, gate rows W1[128b:128b+128] then up rows W3[...]."""
+    f, d = w1.shape
+    return torch.stack([w1.reshape(f // 128, 128, d), w3.reshape(f // 128, 128, d)], dim=1).reshape(2 * f, d)
+
+
+class B200MoELayer:
+    def __init__(self, shape: LayerShape, *, rank: int = 0, world: int = 1, device: int | None = None,
+                 max_tokens: int = 4096, cap_slots: int | None = None, staging_slots: int | None = None):
+        """cap_slots = floor(GpuSpec.memory / m_e) (domain.py:395-401); staging slots (default =
+        cap) hold incoming experts while a migration is in flight, so old copies retire only after
+        new ones land."""
+        self.lib = _lib.load()
+        self.shape = shape
+        self.rank, self.world = rank, world
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.max_tokens = max_tokens
+        self.cap_slots = shape.E if cap_slots is None else int(cap_slots)
+        self.staging_slots = self.cap_slots if staging_slots is None else int(staging_slots)
+        n_phys = self.cap_slots + self.staging_slots
+        desc = _lib.LayerDesc(rank=rank, world=world, device=self.device.index, max_tokens=max_tokens, d=shape.d,
+                              f=shape.f, E=shape.E, top_k=shape.k, score_mode=shape.score_mode, renorm=shape.renorm,
+                              n_slots=n_phys, shared_f=shape.shared_f, shared_gate=shape.shared_gate)
+        h = c_void_p()
+        _lib.check(self.lib.mp_layer_create(byref(desc), byref(h)), "mp_layer_create")
+        self._h = h
+        p = _lib.LayerPtrs()
+        _lib.check(self.lib.mp_layer_get_ptrs(h, byref(p)), "mp_layer_get_ptrs")
+        self._ptrs = p
+        d, f, E, k, T = shape.d, shape.f, shape.E, shape.k, max_tokens
+        dev = self.device
+        self.n_phys_slots = n_phys
+        self.slot_elems = int(p.slot_bytes) // 2
+        self.pool = _view(p.w13_pool, (n_phys, self.slot_elems), torch.bfloat16, dev) if n_phys else None
+        self.wg = _view(p.wg, (E + shape.shared_gate, d), torch.bfloat16, dev)
+        self.bias = _view(p.bias, (E,), torch.float32, dev)
+        self.idx = _view(p.idx, (T, k), torch.int32, dev)
+        self.gate_w = _view(p.w, (T, k), torch.float32, dev)
+        self.pos_dst = _view(p.pos_dst, (T, k), torch.int32, dev)
+        self.pos_row = _view(p.pos_row, (T, k), torch.int32, dev)
+        self.recv = _view(p.recv, (p.recv_cap, d), torch.bfloat16, dev)
+        self.y = _view(p.y, (p.recv_cap, d), torch.bfloat16, dev)
+        self.hist = _view(p.hist, (E,), torch.int32, dev)
+        self.w13_shared = _view(p.w13_shared, (2 * shape.shared_f, d), torch.bfloat16, dev) if shape.shared_f else None
+        self.w2_shared = _view(p.w2_shared, (d, shape.shared_f), torch.bfloat16, dev) if shape.shared_f else None
+        self.shared_gate = _view(p.shared_gate, (T,), torch.float32, dev) if shape.shared_gate else None
+        self.slot_of = np.full(E, -1, dtype=np.int32)     # expert -> physical slot on this GPU
+        self.route = None
+        self._free = list(range(n_phys))
+        self._peers_open = world == 1
+        self._stream = lambda: ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    # ------------------------------------------------------------------ lifecycle
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self.lib.mp_layer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def open_peers(self, group=None) -> None:
+        """Exchange CUDA IPC handles of the NVLink window / weight pool with all ranks."""
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+
+        buf = (ctypes.c_uint8 * 128)()
+        _lib.check(self.lib.mp_layer_export_handles(self._h, buf), "mp_layer_export_handles")
+        mine = bytes(buf)
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, mine, group=group)
+        allh = b"".join(gathered)
+        _lib.check(self.lib.mp_layer_open_peers(self._h, allh), "mp_layer_open_peers")
+        dist.barrier(group=group)
+        self._peers_open = True
+
+    # ------------------------------------------------------------------ weights
+    def set_router(self, wg: torch.Tensor, bias: torch.Tensor | None = None, w_shared_gate: torch.Tensor | None = None):
+        """Router weights Wg [E, d] (+ shared gate row [d]) and the per-origin logit bias [E]."""
+        E = self.shape.E
+        with torch.no_grad():
+            self.wg[:E].copy_(wg.to(self.device, torch.bfloat16))
+            if self.shape.shared_gate:
+                if w_shared_gate is None:
+                    raise ValueError("this shape needs the shared-expert gate row")
+                self.wg[E].copy_(w_shared_gate.to(self.device, torch.bfloat16))
+            self.bias.copy_(bias.to(self.device, torch.float32) if bias is not None else torch.zeros(E))
+        _lib.check(self.lib.mp_layer_prepare_router(self._h, self._stream()), "mp_layer_prepare_router")
+
+    def write_slot(self, slot: int, w1: torch.Tensor, w3: torch.Tensor, w2: torch.Tensor) -> None:
+        d, f = self.shape.d, self.shape.f
+        with torch.no_grad():
+            s = self.pool[slot]
+            s[: 2 * f * d].view(2 * f, d).copy_(interleave_w13(w1.to(self.device, torch.bfloat16),
+                                                               w3.to(self.device, torch.bfloat16)))
+            s[2 * f * d:].view(d, f).copy_(w2.to(self.device, torch.bfloat16))
+
+    def read_slot(self, slot: int):
+        d, f = self.shape.d, self.shape.f
+        s = self.pool[slot]
+        w13 = s[: 2 * f * d].view(f // 128, 2, 128, d)
+        return w13[:, 0].reshape(f, d), w13[:, 1].reshape(f, d), s[2 * f * d:].view(d, f)
+
+    def set_shared(self, w1: torch.Tensor, w3: torch.Tensor, w2: torch.Tensor) -> None:
+        with torch.no_grad():
+            self.w13_shared.copy_(interleave_w13(w1.to(self.device, torch.bfloat16), w3.to(self.device, torch.bfloat16)))
+            self.w2_shared.copy_(w2.to(self.device, torch.bfloat16))
+
+    # ------------------------------------------------------------------ placement
+    def set_routes(self, route: np.ndarray, slot_of: np.ndarray) -> None:
+        route = np.ascontiguousarray(route, dtype=np.int32)
+        slot_of = np.ascontiguousarray(slot_of, dtype=np.int32)
+        if route.shape != (self.world, self.shape.E):
+            raise ValueError(f"route table shape {route.shape} != ({self.world}, {self.shape.E})")
+        _lib.check(self.lib.mp_layer_set_routes(self._h, route.ctypes.data, slot_of.ctypes.data, self._stream()),
+                   "mp_layer_set_routes")
+        self.route = route.copy()
+        self.slot_of = slot_of.copy()
+
+    def load_experts(self, experts, weight_source) -> np.ndarray:
+        """Place `experts` into free slots (those not yet resident); returns slot_of."""
+        if len(experts) > self.cap_slots:
+            raise InfeasibleError(f"GPU {self.rank}: {len(experts)} experts exceed its {self.cap_slots} slots")
+        slot_of = self.slot_of.copy()
+        keep = set(int(e) for e in experts)
+        for e in range(self.shape.E):
+            if slot_of[e] >= 0 and e not in keep:
+                self._free.append(int(slot_of[e]))
+                slot_of[e] = -1
+        self._free.sort()
+        for e in sorted(keep):
+            if slot_of[e] < 0:
+                s = self._free.pop(0)
+                self.write_slot(s, *weight_source(e))
+                slot_of[e] = s
+        return slot_of
+
+    def set_placement(self, placement, cluster, weight_source, layer: int = 0) -> None:
+        """Adopt a reference Placement: route table + resident expert slots."""
+        route = route_table_for(placement, cluster, self.shape.E, self.shape.d, 2, layer)
+        mine = gpu_expert_sets(placement, layer)[self.rank]
+        slot_of = self.load_experts(mine, weight_source)
+        torch.cuda.synchronize(self.device)
+        self.set_routes(route, slot_of)
+
+    def set_placement_sets(self, gpu_sets, weight_source, link_latency=None, link_bandwidth=None) -> None:
+        """Same as set_placement from plain per-GPU expert lists (uniform links by default)."""
+        G, E = self.world, self.shape.E
+        if link_latency is None:
+            link_latency = np.full((G, G), 3e-6)
+            np.fill_diagonal(link_latency, 0.0)
+        if link_bandwidth is None:
+            link_bandwidth = np.full((G, G), 770e9)
+        route = route_table([frozenset(s) for s in gpu_sets], E, link_latency, link_bandwidth, self.shape.d)
+        slot_of = self.load_experts(gpu_sets[self.rank], weight_source)
+        torch.cuda.synchronize(self.device)
+        self.set_routes(route, slot_of)
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        if x.dtype != torch.bfloat16 or x.device != self.device or not x.is_contiguous():
+            raise ValueError("x must be a contiguous bf16 tensor on the layer's device")
+        T = x.shape[0]
+        if out is None:
+            out = torch.empty_like(x)
+        _lib.check(self.lib.mp_layer_forward(self._h, x.data_ptr(), out.data_ptr(), T, self._stream()),
+                   "mp_layer_forward")
+        return out
+
+    __call__ = forward
+
+    def last_launches(self) -> int:
+        return int(self.lib.mp_layer_last_launches(self._h))
+
+    def check(self) -> None:
+        _lib.check(self.lib.mp_layer_check(self._h, self._stream()), "mp_layer_check")
+
+    # ------------------------------------------------------------------ statistics / accounting
+    def activation_counts(self) -> np.ndarray:
+        """Cumulative per-expert token counts of this origin (fused router histogram)."""
+        return self.hist.cpu().numpy().astype(np.int64)
+
+    def reset_counts(self) -> None:
+        self.hist.zero_()
+
+    def read_counts(self) -> np.ndarray:
+        """Exchanged count table C[src][e] of the last forward (G x E)."""
+        buf = np.zeros((self.world, self.shape.E), dtype=np.int32)
+        _lib.check(self.lib.mp_layer_read_counts(self._h, buf.ctypes.data, self._stream()), "mp_layer_read_counts")
+        return buf
+
+    def dispatch_accounting(self) -> dict:
+        """Reference-accounted remote invocations / bytes of the last forward (all origins)."""
+        return dispatch_accounting(self.read_counts(), self.route, self.shape.d)
+
+    # ------------------------------------------------------------------ migration
+    def plan_migration(self, old_sets, new_sets):
+        """Copy ops for this GPU: every expert added here pulls from the lowest-id old holder
+        (the slot diff `new.slots - old.slots` of migration_cost, cost.py:186-187)."""
+        mine_old = set(old_sets[self.rank])
+        ops, adds = [], []
+        free = [s for s in self._free]
+        for e in sorted(set(new_sets[self.rank]) - mine_old):
+            holders = [n for n in range(self.world) if e in old_sets[n]]
+            if not holders:
+                raise RuntimeError(f"expert {e} has no holder in the old placement")
+            if not free:
+                raise InfeasibleError(f"GPU {self.rank}: no staging slot left for expert {e}")
+            dst = free.pop(0)
+            adds.append((e, dst))
+            ops.append((holders[0], e, dst))
+        return ops, adds
+
+    def migrate_async(self, old_sets, new_sets, peer_slot_of, stream: torch.cuda.Stream, event: torch.cuda.Event):
+        """Issue this GPU's weight pulls on `stream`; `peer_slot_of[n][e]` = slot of e on GPU n."""
+        ops, adds = self.plan_migration(old_sets, new_sets)
+        arr = (_lib.CopyOp * max(1, len(ops)))()
+        for i, (src, e, dst) in enumerate(ops):
+            arr[i] = _lib.CopyOp(src, int(peer_slot_of[src][e]), dst)
+        with torch.cuda.stream(stream):
+            _lib.check(self.lib.mp_layer_migrate(self._h, arr, len(ops), c_void_p(stream.cuda_stream),
+                                                 c_void_p(event.cuda_event)), "mp_layer_migrate")
+        for _, dst in adds:
+            self._free.remove(dst)
+        return adds
+
+    def finish_migration(self, new_sets, adds, link_latency=None, link_bandwidth=None) -> None:
+        """After the copies landed everywhere: swap routes, retire evicted slots (migration_complete)."""
+        G, E = self.world, self.shape.E
+        slot_of = self.slot_of.copy()
+        for e, dst in adds:
+            slot_of[e] = dst
+        keep = set(new_sets[self.rank])
+        for e in range(E):
+            if slot_of[e] >= 0 and e not in keep:
+                self._free.append(int(slot_of[e]))
+                slot_of[e] = -1
+        self._free.sort()
+        if link_latency is None:
+            link_latency = np.full((G, G), 3e-6)
+            np.fill_diagonal(link_latency, 0.0)
+        if link_bandwidth is None:
+            link_bandwidth = np.full((G, G), 770e9)
+        route = route_table([frozenset(s) for s in new_sets], E, link_latency, link_bandwidth, self.shape.d)
+        self.set_routes(route, slot_of)

@@ -1,0 +1,134 @@
+"""GPU parity of the individual kernels through the C ABI.
+
+* K3 grouped GEMM (tcgen05): against a plain PyTorch fp32 reference of the
+  same op on identical bf16 inputs (floating-point kernel).
+* K1 router: against the CPU oracle -- indices and histogram bit-exact,
+  gate weights within 1e-5 (fp32 exp differences only).
+"""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import moe_oracle as orc
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    from paper_2508_12851_b200 import _lib as L
+    return L, L.load()
+
+
+def _vp(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _groups(ms, slots, a_offsets=None):
+    rows, arr = 0, []
+    for i, (m, s) in enumerate(zip(ms, slots)):
+        a = rows if a_offsets is None else a_offsets[i]
+        arr.append([a, m, s, a])
+        rows = a + m
+    g = torch.tensor(arr, dtype=torch.int32, device="cuda").reshape(-1)
+    n = torch.tensor([len(ms)], dtype=torch.int32, device="cuda")
+    return g, n, rows
+
+
+def _ref_gemm(a, b, ms, slots, N, swiglu):
+    outs, r = [], 0
+    for m, s in zip(ms, slots):
+        acc = a[r:r + m].float() @ b[s * N:(s + 1) * N].float().T
+        if swiglu:
+            nb = N // 256
+            acc = acc.view(m, nb, 2, 128)
+            g, u = acc[:, :, 0, :].reshape(m, -1), acc[:, :, 1, :].reshape(m, -1)
+            acc = torch.nn.functional.silu(g) * u
+        outs.append(acc)
+        r += m
+    return torch.cat(outs)
+
+
+@pytest.mark.parametrize("swiglu", [0, 1])
+@pytest.mark.parametrize("ms,K,N", [([128], 64, 256), ([300, 5, 128, 0 + 1], 512, 512), ([1000, 37], 2048, 768)])
+def test_grouped_gemm_matches_torch(swiglu, ms, K, N):
+    L, lib = _lib()
+    torch.manual_seed(0)
+    S = len(ms) + 1
+    slots = [(i * 2 + 1) % S for i in range(len(ms))]
+    rows = sum(ms)
+    a = (torch.randn(rows + 7, K, device="cuda") / 4).bfloat16()
+    b = (torch.randn(S * N, K, device="cuda") / np.sqrt(K)).bfloat16()
+    g, n, _ = _groups(ms, slots)
+    out_ld = N // 2 if swiglu else N
+    out = torch.full((rows + 7, out_ld), float("nan"), device="cuda", dtype=torch.bfloat16)
+    rc = lib.mp_grouped_gemm(_vp(a), a.shape[0], _vp(b), b.shape[0], _vp(g), _vp(n), N, K, _vp(out), out_ld, swiglu,
+                             _stream())
+    L.check(rc, "mp_grouped_gemm")
+    torch.cuda.synchronize()
+    ref = _ref_gemm(a, b, ms, slots, N, swiglu)
+    got = out[:rows].float()
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    assert err <= 2e-2 * scale + 1e-3, (err, scale)
+    rel = ((got - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2, rel
+    # rows outside every group are untouched
+    assert torch.isnan(out[rows:].float()).all()
+
+
+def test_grouped_gemm_large_k_many_tiles():
+    """More tiles than SMs (persistent loop + TMEM double buffer + smem ring wrap)."""
+    L, lib = _lib()
+    torch.manual_seed(1)
+    ms, K, N = [2048, 1500, 900], 1024, 1024
+    slots = [0, 2, 1]
+    rows = sum(ms)
+    a = (torch.randn(rows, K, device="cuda") / 4).bfloat16()
+    b = (torch.randn(3 * N, K, device="cuda") / np.sqrt(K)).bfloat16()
+    g, n, _ = _groups(ms, slots)
+    out = torch.empty(rows, N, device="cuda", dtype=torch.bfloat16)
+    L.check(lib.mp_grouped_gemm(_vp(a), rows, _vp(b), 3 * N, _vp(g), _vp(n), N, K, _vp(out), N, 0, _stream()))
+    torch.cuda.synchronize()
+    ref = _ref_gemm(a, b, ms, slots, N, 0)
+    rel = ((out.float() - ref).norm() / ref.norm()).item()
+    assert rel < 1e-2, rel
+
+
+@pytest.mark.parametrize("E,k,mode,gate,d,T", [(8, 2, 0, 0, 512, 333), (64, 6, 1, 0, 256, 200), (60, 4, 1, 1, 512, 64),
+                                               (8, 2, 0, 0, 4096, 48)])
+def test_router_bit_exact(E, k, mode, gate, d, T):
+    L, lib = _lib()
+    x = orc.synthetic_tokens(0, T, d, seed=3)
+    wg = orc.synthetic_router(E + gate, d, seed=3)
+    bias = orc.origin_bias(1, E, seed=3)
+    lg = orc.router_logits(x, wg, bias)
+    idx_ref, w_ref = orc.topk_route(lg, E, k, mode)
+    hist_ref = orc.histogram(idx_ref, E)
+
+    xt = torch.from_numpy(x).cuda().bfloat16()
+    wgt = torch.from_numpy(wg).cuda().bfloat16()
+    packed = torch.empty((E + gate) * d, device="cuda", dtype=torch.float32)
+    L.check(lib.mp_router_pack(_vp(wgt), E + gate, d, _vp(packed), _stream()))
+    bt = torch.from_numpy(bias).cuda()
+    idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    w = torch.empty(T, k, dtype=torch.float32, device="cuda")
+    go = torch.empty(T, dtype=torch.float32, device="cuda")
+    hist = torch.zeros(E, dtype=torch.int32, device="cuda")
+    L.check(lib.mp_router_topk_hist(_vp(xt), _vp(packed), _vp(bt), T, d, E, gate, k, mode, 0, _vp(idx), _vp(w),
+                                    _vp(go) if gate else None, _vp(hist), _stream()))
+    torch.cuda.synchronize()
+    assert np.array_equal(idx.cpu().numpy(), idx_ref)
+    assert np.array_equal(hist.cpu().numpy(), hist_ref)
+    np.testing.assert_allclose(w.cpu().numpy(), w_ref, rtol=1e-5, atol=1e-6)
+    if gate:
+        g_ref = 1.0 / (1.0 + np.exp(-lg[:, E].astype(np.float64)))
+        np.testing.assert_allclose(go.cpu().numpy(), g_ref, rtol=1e-5, atol=1e-6)
