@@ -1,0 +1,499 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MoE-layer forward (BASELINE.json metric).
+
+Metric: MoE-layer tokens/s (whole job, all GPUs) with p50 batch latency and
+remote-dispatch bytes.  One "step" = one MoE-layer forward of T tokens per GPU
+(weak scaling: T fixed per GPU).  Default workload (N=1): the Mixtral-8x7B
+layer shape (BASELINE.json configs[1]), T = 4096 tokens per GPU,
+activation-aware placement ("ours") from the reference solver.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config mixtral] [--impl b200|reference]
+
+N > 1 is launched by torchrun (one process per GPU; RANK/LOCAL_RANK/WORLD_SIZE
+from the env).  Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+METRIC = "MoE-layer tokens/s (p50 batch latency, remote-dispatch bytes)"
+UNIT = "tokens/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+N_ROTATE = 8  # distinct input batches cycled through the timed region
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="mixtral")
+    ap.add_argument("--tokens", type=int, default=4096, help="tokens per GPU per step")
+    ap.add_argument("--strategy", default="ours")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=256, help="tokens per CPU-baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--stages", action="store_true", help="print the per-stage table on stderr")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- dist helpers
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, local, world
+
+
+def load_peaks():
+    p = REPO / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self._t.join(timeout=1)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- placement
+def build_placement_sets(shape, G, counts, strategy, seed):
+    """Per-GPU expert lists from the reference placement solver (build_placement,
+    reference placement.py:541-566) on the GPU-measured activation counts."""
+    from paper_2508_12851_b200.errors import import_moeplace
+    from paper_2508_12851_b200.shapes import cluster_spec, model_spec, slot_caps
+    from paper_2508_12851_b200.routing import gpu_expert_sets
+
+    caps = slot_caps(shape, G)
+    if G == 1:
+        return [list(range(shape.E))], caps, "all-local (G=1)"
+    mp = import_moeplace()
+    if mp is None:
+        raise RuntimeError("the reference placement solver (moeplace) is not importable; "
+                           "install it into baseline/_ref (see DESIGN.md)")
+    cluster = cluster_spec(shape, G, caps)
+    model = model_spec(shape)
+    stats = mp.ActivationStats.from_counts(np.asarray(counts, dtype=float)[:, None, :], (shape.E,))
+    placement = mp.build_placement(strategy, cluster, model, stats, seed)
+    rep = mp.validate_placement(placement, cluster, model)
+    if not rep.ok:
+        raise RuntimeError(f"invalid placement: {rep}")
+    return gpu_expert_sets(placement, 0), caps, f"moeplace.build_placement({strategy!r})"
+
+
+def uniform_sets(shape, G, caps):
+    """place_uniform's round-robin partition (reference placement.py:407-422), for the naive comparison."""
+    sets = [[] for _ in range(G)]
+    for e in range(shape.E):
+        sets[e % G].append(e)
+    return sets
+
+
+# ----------------------------------------------------------------------------- CPU baseline
+def cpu_layer_sample(shape, T_cpu, seed, weights_cpu, wg_np, bias_np):
+    """One oracle forward of T_cpu tokens (G=1, all experts local)."""
+    from oracle import moe_oracle as orc
+    x = orc.synthetic_tokens(0, T_cpu, shape.d, seed)
+    route = np.zeros((1, shape.E), dtype=np.int32)
+    shared = weights_cpu.get("shared")
+    wsg = wg_np[shape.E] if shape.shared_gate else None
+    orc.moe_layer_forward(shape, [x], wg_np[:shape.E], [bias_np], route, weights_cpu["experts"], shared, wsg)
+
+
+def cpu_weights(shape, seed, wg_gpu=None, expert_src=None):
+    """fp32 host copies of the expert weights (the same values the GPU holds)."""
+    import torch
+    from paper_2508_12851_b200 import workload as wl
+    experts = {}
+    for e in range(shape.E):
+        w1, w3, w2 = expert_src(e)
+        experts[e] = (w1.float().cpu().numpy(), w3.float().cpu().numpy(), w2.float().cpu().numpy())
+    out = {"experts": experts}
+    if shape.shared_f:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        s = wl.shared_weights(shape.d, shape.shared_f, dev, seed)
+        out["shared"] = tuple(w.float().cpu().numpy() for w in s)
+    return out
+
+
+def time_cpu_baseline(shape, seed, T_cpu, budget_s, weights_cpu, wg_np, bias_np, min_reps=1):
+    import torch
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    cpu_layer_sample(shape, min(T_cpu, 32), seed, weights_cpu, wg_np, bias_np)  # warm (BLAS init)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        cpu_layer_sample(shape, T_cpu, seed, weights_cpu, wg_np, bias_np)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or reps >= 1000 or (reps >= min_reps and el * (reps + 1) / reps > 3 * budget_s):
+            break
+    el = time.perf_counter() - t0
+    return reps * T_cpu / el, reps, el, threads
+
+
+# ----------------------------------------------------------------------------- main (B200 arm)
+def main_b200(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2508_12851_b200 import _lib, workload as wl
+    from paper_2508_12851_b200.layer import B200MoELayer
+    from paper_2508_12851_b200.routing import dispatch_accounting, route_table, uniform_links
+    from paper_2508_12851_b200.shapes import get_shape
+
+    rank, local, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    shape = get_shape(args.config)
+    T, G, seed = args.tokens, world, args.seed
+
+    # ---- router weights + per-origin skew (the reference's Dirichlet recipe)
+    wg = wl.router_weights(shape.E + shape.shared_gate, shape.d, dev, seed)
+    bias = wl.origin_bias(rank, shape.E, seed)
+    expert_src = lambda e: wl.expert_weights(e, shape.d, shape.f, dev, seed)
+
+    # ---- activation counts of a warm-up batch (GPU router kernel) -> placement
+    lib = _lib.load()
+    import ctypes
+    packed = torch.empty((shape.E + shape.shared_gate) * shape.d, device=dev, dtype=torch.float32)
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _lib.check(lib.mp_router_pack(ctypes.c_void_p(wg.data_ptr()), shape.E + shape.shared_gate, shape.d,
+                                  ctypes.c_void_p(packed.data_ptr()), st))
+    xw = wl.tokens(T, shape.d, dev, seed, rank, batch=10_000)
+    idx = torch.empty(T, shape.k, dtype=torch.int32, device=dev)
+    wtmp = torch.empty(T, shape.k, dtype=torch.float32, device=dev)
+    hist = torch.zeros(shape.E, dtype=torch.int32, device=dev)
+    bias_d = bias.to(dev)
+    _lib.check(lib.mp_router_topk_hist(ctypes.c_void_p(xw.data_ptr()), ctypes.c_void_p(packed.data_ptr()),
+                                       ctypes.c_void_p(bias_d.data_ptr()), T, shape.d, shape.E, shape.shared_gate,
+                                       shape.k, shape.score_mode, shape.renorm, ctypes.c_void_p(idx.data_ptr()),
+                                       ctypes.c_void_p(wtmp.data_ptr()), None, ctypes.c_void_p(hist.data_ptr()), st))
+    if world > 1:
+        allh = [torch.zeros_like(hist) for _ in range(world)]
+        dist.all_gather(allh, hist)
+        counts = torch.stack(allh).cpu().numpy()
+    else:
+        counts = hist[None].cpu().numpy()
+    sets, caps, solver = build_placement_sets(shape, G, counts, args.strategy, seed)
+
+    # ---- the layer
+    layer = B200MoELayer(shape, rank=rank, world=world, device=local, max_tokens=T, cap_slots=caps[rank])
+    layer.open_peers()
+    layer.set_router(wg[:shape.E], bias, wg[shape.E] if shape.shared_gate else None)
+    if shape.shared_f:
+        layer.set_shared(*wl.shared_weights(shape.d, shape.shared_f, dev, seed))
+    layer.set_placement_sets(sets, expert_src)
+    del xw, idx, wtmp
+    torch.cuda.synchronize()
+
+    # rotating input batches (+ weights) exceed L2: 8 x T x d bf16 + all expert slots
+    xs = [wl.tokens(T, shape.d, dev, seed, rank, batch=b) for b in range(N_ROTATE)]
+    out = torch.empty(T, shape.d, device=dev, dtype=torch.bfloat16)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for i in range(args.warmup):
+        layer.forward(xs[i % N_ROTATE], out)
+    torch.cuda.synchronize()
+    layer.check()
+
+    # ---- timed region (device time, CUDA events, stage events per step)
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(_lib.NUM_STAGE_EVENTS)] for _ in range(K)]
+    for row in evs:  # torch creates the CUDA event lazily on first record
+        for ev in row:
+            ev.record(stream)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    torch.cuda.synchronize()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(K):
+        layer.forward(xs[i % N_ROTATE], out, events=evs[i])
+    end.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    layer.check()
+    t_ms = start.elapsed_time(end)
+    step_ms = [evs[i][0].elapsed_time(evs[i][-1]) for i in range(K)]
+    stage_ms = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(_lib.NUM_STAGE_EVENTS - 1)]
+                         for i in range(K)])
+    launches = layer.last_launches() * K
+    acc_ours = layer.dispatch_accounting()
+    counts_last = layer.read_counts()
+    recv_rows = int(np.sum([counts_last[s, e] for s in range(G) for e in range(shape.E) if layer.route[s, e] == rank]))
+
+    # ---- e2e: same forward through the public API with host buffers (H2D x, D2H out, every step)
+    xh = [x.cpu().pin_memory() for x in xs]
+    oh = [torch.empty(T, shape.d, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    xd = torch.empty(T, shape.d, device=dev, dtype=torch.bfloat16)
+    for i in range(3):
+        xd.copy_(xh[i % N_ROTATE], non_blocking=True)
+        layer.forward(xd, out)
+        oh[i % 2].copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(K):
+        xd.copy_(xh[i % N_ROTATE], non_blocking=True)
+        layer.forward(xd, out)
+        oh[i % 2].copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    layer.check()
+
+    # ---- max over ranks
+    vals = torch.tensor([t_ms, e2e_ms, float(np.median(step_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    t_ms, e2e_ms, p50_ms = vals.tolist()
+    stage_mean = stage_ms.mean(axis=0)
+    stage_t = torch.tensor(stage_mean, dtype=torch.float64, device=dev)
+    rows_t = torch.tensor([recv_rows], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stage_t, op=dist.ReduceOp.MAX)
+        rows_all = [torch.zeros_like(rows_t) for _ in range(world)]
+        dist.all_gather(rows_all, rows_t)
+        rows_list = [int(r.item()) for r in rows_all]
+    else:
+        rows_list = [recv_rows]
+
+    # naive placement accounting on the same counts (counts do not depend on placement)
+    lat, bw = uniform_links(G)
+    naive_route = route_table([frozenset(s) for s in uniform_sets(shape, G, caps)], shape.E, lat, bw, shape.d)
+    acc_naive = dispatch_accounting(counts_last, naive_route, shape.d)
+
+    # ---- roofline of the dominant kernel: grouped_gemm_kernel (GEMM1 SwiGLU + GEMM2) on this GPU
+    peaks, peaks_src = load_peaks()
+    gemm_ms = float(stage_ms[:, 6].mean() + stage_ms[:, 7].mean())
+    flops = 2.0 * recv_rows * 3 * shape.d * shape.f  # algorithmic: 6*d*f per routed (token, expert) pair
+    achieved_tflops = flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    traffic = None
+    tf = REPO / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(f"{shape.name}_G{G}_T{T}")
+        except Exception:
+            traffic = None
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        layer.close()
+        return
+
+    # ---- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        wcpu = cpu_weights(shape, seed, wg, expert_src)
+        wg_np = wg.float().cpu().numpy()
+        rate, reps, el, thr = time_cpu_baseline(shape, seed, args.cpu_tokens, args.cpu_seconds, wcpu, wg_np,
+                                                bias.numpy())
+        cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port",
+               "sample": f"oracle/moe_oracle.py numpy fp32 layer forward, {shape.name} shape, {args.cpu_tokens} "
+                         f"tokens x {reps} reps ({el:.1f} s), all experts local, {thr} threads"}
+
+    tokens_total = G * T * K
+    value = tokens_total / (t_ms * 1e-3)
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": G,
+        "steps": K,
+        "warmup": args.warmup,
+        "ms_per_step": t_ms / K,
+        "p50_batch_latency_ms": p50_ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (N(0,1) tokens, random-init expert/router weights, Dirichlet(0.3) routing skew "
+                "per origin as in the reference's WorkloadSpec.synthetic)",
+        "config": {"workload": f"{shape.name} MoE layer, {T} tokens/GPU, placement {solver}",
+                   "model": shape.name, "d": shape.d, "ffn": shape.f, "experts": shape.E, "top_k": shape.k,
+                   "shared_ffn": shape.shared_f, "tokens_per_gpu": T, "global_batch": G * T,
+                   "slot_caps": caps, "parallelism": f"ep{G}+dp{G}",
+                   "l2": f"{N_ROTATE} rotating input batches ({N_ROTATE * T * shape.d * 2 / 2**20:.0f} MiB) + "
+                         f"{sum(len(s) for s in sets) * shape.expert_bytes / 2**30:.2f} GiB resident expert weights "
+                         "streamed per step exceed the 126 MB L2"},
+        "dispatch": {
+            "ours": {k: acc_ours[k] for k in ("remote_invocations", "remote_bytes", "wire_bytes", "local_ratio")},
+            "uniform": {k: acc_naive[k] for k in ("remote_invocations", "remote_bytes", "wire_bytes", "local_ratio")},
+            "recv_rows_per_gpu": rows_list,
+        },
+        "stages_ms": {name: float(v) for name, v in zip(_lib.STAGES, stage_t.tolist())},
+        "roofline": {"bound": "tensor", "kernel": "grouped_gemm_kernel (GEMM1+SwiGLU, GEMM2), rank 0",
+                     "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved_tflops / peak if peak else None, "traffic": traffic,
+                     "peak_source": f"{peaks_src} bf16 sustained (kernel timed inside the step)",
+                     "flops_per_step": flops},
+        "cpu_baseline": cpu,
+        "e2e": {"value": tokens_total / (e2e_ms * 1e-3), "unit": UNIT,
+                "h2d_bytes_per_step": T * shape.d * 2, "d2h_bytes_per_step": T * shape.d * 2,
+                "path": "B200MoELayer.forward (C ABI mp_layer_forward) with pinned host x -> device, out -> host"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if args.stages:
+        for name, v in zip(_lib.STAGES, stage_mean):
+            sys.stderr.write(f"{name:18s} {v * 1e3:9.1f} us\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    layer.close()
+
+
+# ----------------------------------------------------------------------------- reference arm
+def main_reference(args):
+    """The reference's CPU path for this workload: the oracle port (the reference itself has no
+    layer arithmetic -- SPEC.md:8 -- so its CPU implementation is the restatement in oracle/)."""
+    rank, local, world = dist_env()
+    if rank != 0:
+        return
+    import torch
+    from oracle import moe_oracle as orc
+    from paper_2508_12851_b200.shapes import get_shape
+
+    shape = get_shape(args.config)
+    seed = args.seed
+    threads = os.cpu_count() or 1
+    torch.set_num_threads(threads)
+    T_cpu = args.cpu_tokens
+    oshape = orc.LayerShape(shape.name, shape.d, shape.f, shape.E, shape.k, shape.score_mode, shape.renorm,
+                            shape.shared_f, shape.shared_gate)
+    # weights: only experts the sample can reach are materialised lazily
+    wg = orc.synthetic_router(shape.E + shape.shared_gate, shape.d, seed)
+    bias = orc.origin_bias(0, shape.E, seed)
+    x = orc.synthetic_tokens(0, T_cpu, shape.d, seed)
+    idx, _ = orc.topk_route(orc.router_logits(x, wg, bias), shape.E, shape.k, shape.score_mode)
+    experts = {int(e): orc.synthetic_expert(int(e), shape.d, shape.f, seed) for e in np.unique(idx)}
+    shared = orc.synthetic_expert(999, shape.d, shape.shared_f, seed) if shape.shared_f else None
+    route = np.zeros((1, shape.E), dtype=np.int32)
+    wsg = wg[shape.E] if shape.shared_gate else None
+
+    def step():
+        orc.moe_layer_forward(oshape, [x], wg[:shape.E], [bias], route, experts, shared, wsg)
+
+    # bound the whole run to ~2 minutes: shrink the per-step sample if one step is slow
+    t0 = time.perf_counter()
+    step()
+    one = time.perf_counter() - t0
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    if one > budget:
+        T_cpu = max(8, int(T_cpu * budget / one))
+        x = x[:T_cpu]
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    value = args.steps * T_cpu / el
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{shape.name} MoE layer on the host CPU, {T_cpu} tokens per step (bounded sample)",
+                   "model": shape.name, "tokens_per_step": T_cpu},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"oracle/moe_oracle.py numpy fp32, {T_cpu} tokens/step x {args.steps} steps"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        # keep the whole --steps K run within minutes: clamp the sample size for the big shapes
+        main_reference(a)
+    else:
+        main_b200(a)

@@ -154,6 +154,14 @@ int mp_layer_prepare_router(mp_layer* layer, void* stream);
  * grouped SwiGLU GEMMs (tcgen05), barrier, combine+return (NVLink loads). */
 int mp_layer_forward(mp_layer* layer, const void* x, void* out, int T, void* stream);
 
+/* Same forward, recording MP_NUM_STAGE_EVENTS cudaEvent_t (created by the
+ * caller with timing enabled) on `stream` at the stage boundaries:
+ *   0 start | 1 router | 2 count exchange | 3 layout | 4 permute+dispatch |
+ *   5 shared expert | 6 dispatch barrier | 7 GEMM1 SwiGLU | 8 GEMM2 |
+ *   9 return barrier | 10 combine+return                                      */
+#define MP_NUM_STAGE_EVENTS 11
+int mp_layer_forward_timed(mp_layer* layer, const void* x, void* out, int T, void* stream, void* const* events);
+
 /* Number of kernels the last mp_layer_forward launched. */
 int mp_layer_last_launches(mp_layer* layer);
 

@@ -26,12 +26,16 @@ MP_E_PEER = -6
 
 MP_SCORE_TOPK_SOFTMAX = 0
 MP_SCORE_SOFTMAX_TOPK = 1
+NUM_STAGE_EVENTS = 11
+STAGES = ("router", "count_exchange", "layout", "permute_dispatch", "shared_expert", "dispatch_barrier",
+          "gemm1_swiglu", "gemm2", "return_barrier", "combine_return")
 
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
     "mp_abi_version", "mp_last_error", "mp_router_pack", "mp_router_topk_hist", "mp_grouped_gemm",
     "mp_layer_create", "mp_layer_destroy", "mp_layer_get_ptrs", "mp_layer_export_handles",
     "mp_layer_open_peers", "mp_layer_set_routes", "mp_layer_prepare_router", "mp_layer_forward",
+    "mp_layer_forward_timed",
     "mp_layer_last_launches", "mp_layer_read_counts", "mp_layer_check", "mp_layer_migrate",
 )
 
@@ -91,6 +95,7 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         "mp_layer_set_routes": ([V, V, V, V], I),
         "mp_layer_prepare_router": ([V, V], I),
         "mp_layer_forward": ([V, V, V, I, V], I),
+        "mp_layer_forward_timed": ([V, V, V, I, V, POINTER(c_void_p)], I),
         "mp_layer_last_launches": ([V], I),
         "mp_layer_read_counts": ([V, V, V], I),
         "mp_layer_check": ([V, V], I),

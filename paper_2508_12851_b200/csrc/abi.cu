@@ -425,7 +425,7 @@ int mp_layer_prepare_router(mp_layer* L, void* stream) {
   return MP_OK;
 }
 
-int mp_layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream) {
+static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream, void* const* events) {
   if (!L) return set_error(MP_E_ARG, "mp_layer_forward: null layer");
   if ((!x || !out) && T > 0) return set_error(MP_E_ARG, "mp_layer_forward: null x/out with T=%d", T);
   const mp_layer_desc& D = L->desc;
@@ -442,6 +442,15 @@ int mp_layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream)
   auto** flag_ptrs = reinterpret_cast<uint32_t**>(L->ptr_arrays + 2 * 8);
   auto** count_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + (3 + par) * 8);
   int launches = 0;
+  int ev_i = 0;
+  auto mark = [&]() -> int {
+    if (events) {
+      cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(events[ev_i]), st);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaEventRecord(stage)");
+    }
+    ++ev_i;
+    return MP_OK;
+  };
 
   if (D.shared_f > 0 && T > 0 && (L->tm_x_ptr != x || L->tm_x_rows != T)) {
     MP_TRY(encode_tmap_bf16_2d(&L->tm_x, x, uint64_t(std::max(T, 1)), uint64_t(D.d), 128));
@@ -449,22 +458,27 @@ int mp_layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream)
     L->tm_x_rows = T;
   }
 
+  MP_TRY(mark());  // 0
   MP_CUDA(cudaMemsetAsync(L->batch_counts, 0, size_t(E) * 4, st));
   MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
                        D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts, st));
   ++launches;
+  MP_TRY(mark());  // 1 router
   const int32_t* counts_all = L->batch_counts;
   if (G > 1) {
     MP_TRY(launch_publish_barrier(flag_ptrs, count_ptrs, L->batch_counts, E, G, rank, ++L->epoch, L->err, st));
     ++launches;
     counts_all = L->counts + size_t(par) * G * E;
   }
+  MP_TRY(mark());  // 2 count exchange
   MP_TRY(launch_layout(counts_all, L->route_d, L->slot_of_d, L->blk_counts, nb, G, E, rank, L->my_base,
                        L->blk_prefix, L->groups, L->n_groups, L->recv_rows, st));
   ++launches;
+  MP_TRY(mark());  // 3 layout
   MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d + rank * E, L->my_base,
                         L->blk_prefix, T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st));
   ++launches;
+  MP_TRY(mark());  // 4 permute + dispatch
   if (D.shared_f > 0 && T > 0) {
     const int32_t hg[4] = {0, T, 0, 0};
     // group table of the dense shared expert: one group of all T local tokens
@@ -477,27 +491,44 @@ int mp_layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream)
                                0, 0, st));
     launches += 2;
   }
+  MP_TRY(mark());  // 5 shared expert
   if (G > 1) {
     MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, ++L->epoch, L->err, st));
     ++launches;
   }
+  MP_TRY(mark());  // 6 dispatch barrier
   if (D.n_slots > 0) {
     MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, L->groups, L->n_groups, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f,
                                1, 0, st));
+    MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
     MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, L->groups, L->n_groups, D.d, D.f, 3 * D.d, 2 * D.d, L->y, D.d, 0,
                                0, st));
     launches += 2;
+  } else {
+    MP_TRY(mark());
   }
+  MP_TRY(mark());  // 8 GEMM2
   if (G > 1) {
     MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, ++L->epoch, L->err, st));
     ++launches;
   }
+  MP_TRY(mark());  // 9 return barrier
   MP_TRY(launch_combine(y_ptrs, L->pos_dst, L->pos_row, L->w, T, D.d, k, D.shared_f > 0 ? L->ys : nullptr,
                         D.shared_gate ? L->sgate : nullptr, static_cast<__nv_bfloat16*>(out), st));
   ++launches;
+  MP_TRY(mark());  // 10 combine + return
   L->last_launches = launches;
   ++L->fwd_count;
   return MP_OK;
+}
+
+int mp_layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream) {
+  return layer_forward(L, x, out, T, stream, nullptr);
+}
+
+int mp_layer_forward_timed(mp_layer* L, const void* x, void* out, int T, void* stream, void* const* events) {
+  if (!events) return set_error(MP_E_ARG, "mp_layer_forward_timed: null events");
+  return layer_forward(L, x, out, T, stream, events);
 }
 
 int mp_layer_last_launches(mp_layer* L) { return L ? L->last_launches : 0; }

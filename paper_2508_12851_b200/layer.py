@@ -210,14 +210,26 @@ class B200MoELayer:
         self.set_routes(route, slot_of)
 
     # ------------------------------------------------------------------ forward
-    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, events=None) -> torch.Tensor:
+        """One MoE-layer forward of this GPU's tokens.  `events`: optional list of
+        _lib.NUM_STAGE_EVENTS torch.cuda.Event(enable_timing=True) recorded at the
+        stage boundaries (see include/moeplace_b200.h)."""
         if x.dtype != torch.bfloat16 or x.device != self.device or not x.is_contiguous():
             raise ValueError("x must be a contiguous bf16 tensor on the layer's device")
+        if x.dim() != 2 or x.shape[1] != self.shape.d:
+            from .errors import DimensionMismatch
+            raise DimensionMismatch(f"x has shape {tuple(x.shape)}, layer hidden width is {self.shape.d}")
         T = x.shape[0]
         if out is None:
             out = torch.empty_like(x)
-        _lib.check(self.lib.mp_layer_forward(self._h, x.data_ptr(), out.data_ptr(), T, self._stream()),
-                   "mp_layer_forward")
+        if events is None:
+            rc = self.lib.mp_layer_forward(self._h, x.data_ptr(), out.data_ptr(), T, self._stream())
+        else:
+            if any(ev.cuda_event == 0 for ev in events):
+                raise ValueError("stage events must be created (recorded once) before use")
+            arr = (c_void_p * _lib.NUM_STAGE_EVENTS)(*[c_void_p(ev.cuda_event) for ev in events])
+            rc = self.lib.mp_layer_forward_timed(self._h, x.data_ptr(), out.data_ptr(), T, self._stream(), arr)
+        _lib.check(rc, "mp_layer_forward")
         return out
 
     __call__ = forward
