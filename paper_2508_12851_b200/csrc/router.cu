@@ -19,8 +19,9 @@
 // compares logits only, so the indices do not depend on the exp implementation.
 //
 // Layout: Wg is repacked once into [d/4][E_tot][4] fp32 so that threads owning
-// consecutive experts read consecutive 16 B words.  A CTA owns 16 tokens; x is
-// staged to shared memory as fp32 in 256-column chunks.
+// consecutive experts read consecutive 16 B words.  A CTA owns 16 tokens; the x
+// rows and the matching Wg columns are staged through shared memory in k-chunks
+// by a double-buffered cp.async pipeline, so the FMA chains only see LDS latency.
 #include "common.cuh"
 #include "mp_internal.h"
 
@@ -29,7 +30,6 @@ namespace mp {
 namespace rt {
 constexpr int kThreads = 128;
 constexpr int kTokens = 16;    // tokens per CTA
-constexpr int kChunk = 256;    // k-columns staged per step
 constexpr int kMaxE = 64;      // routed experts
 constexpr int kMaxItems = (kTokens * (kMaxE + 1) + kThreads - 1) / kThreads;
 constexpr int kMaxK = 8;
@@ -55,22 +55,36 @@ int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, float* packed,
 // Larger logit wins; equal logits -> lower expert id.
 MP_DEV bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
 
+MP_DEV void cp_async_16(void* smem, const void* gmem, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+MP_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+MP_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Shared memory per stage: x chunk [16][kc] bf16 + Wg chunk [kc/4][E_tot][4] fp32,
+// double-buffered and filled with cp.async while the previous chunk is consumed.
 template <int kItems>
 __global__ void __launch_bounds__(rt::kThreads)
     router_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict__ wp, const float* __restrict__ bias,
-                  int T, int d, int E, int has_gate, int k, int score_mode, int renorm, int32_t* __restrict__ idx,
-                  float* __restrict__ wout, float* __restrict__ shared_gate, uint32_t* __restrict__ hist,
-                  int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts) {
-  __shared__ __align__(16) float xs[rt::kTokens][rt::kChunk];
+                  int T, int d, int E, int has_gate, int k, int score_mode, int renorm, int kc,
+                  int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
+                  uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts) {
+  extern __shared__ __align__(16) uint8_t rsm[];
   __shared__ float logits[rt::kTokens][rt::kMaxE + 1];
   __shared__ int cnt_s[rt::kMaxE];
 
   const int E_tot = E + has_gate;
   const int t0 = blockIdx.x * rt::kTokens;
   const int tid = threadIdx.x;
+  const int x_bytes = rt::kTokens * kc * 2;
+  const int w_bytes = E_tot * kc * 4;
+  const int stage_bytes = x_bytes + w_bytes;
   for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
 
-  // item m of this thread -> (token, expert)
   int it_t[kItems], it_e[kItems];
   float acc[kItems];
 #pragma unroll
@@ -81,39 +95,61 @@ __global__ void __launch_bounds__(rt::kThreads)
     acc[m] = 0.0f;
   }
   const int n_items = rt::kTokens * E_tot;
+  const int n_chunks = d / kc;
 
-  for (int k0 = 0; k0 < d; k0 += rt::kChunk) {
-    const int kc = min(rt::kChunk, d - k0);
-    __syncthreads();
-    // stage x[t0..t0+16, k0..k0+kc) as fp32 (16 B bf16 loads, 8 values each)
-    for (int v = tid; v < rt::kTokens * (kc / 8); v += blockDim.x) {
-      const int tt = v / (kc / 8);
-      const int c8 = (v - tt * (kc / 8)) * 8;
-      float4 lo = make_float4(0.f, 0.f, 0.f, 0.f), hi = lo;
-      if (t0 + tt < T) {
-        const uint4 raw = ld_nc_v4(x + size_t(t0 + tt) * d + k0 + c8);
-        lo = make_float4(bf16_lo(raw.x), bf16_hi(raw.x), bf16_lo(raw.y), bf16_hi(raw.y));
-        hi = make_float4(bf16_lo(raw.z), bf16_hi(raw.z), bf16_lo(raw.w), bf16_hi(raw.w));
-      }
-      *reinterpret_cast<float4*>(&xs[tt][c8]) = lo;
-      *reinterpret_cast<float4*>(&xs[tt][c8 + 4]) = hi;
+  auto issue = [&](int c) {
+    uint8_t* base = rsm + (c & 1) * stage_bytes;
+    const int k0 = c * kc;
+    const int xv = kc / 8;  // 16 B vectors per token row
+    for (int v = tid; v < rt::kTokens * xv; v += blockDim.x) {
+      const int tt = v / xv, c8 = (v - tt * xv) * 8;
+      const bool ok = t0 + tt < T;
+      const __nv_bfloat16* src = ok ? x + size_t(t0 + tt) * d + k0 + c8 : x;
+      cp_async_16(base + (tt * kc + c8) * 2, src, ok ? 16u : 0u);
+    }
+    const float4* wsrc = wp + size_t(k0 >> 2) * E_tot;
+    float4* wdst = reinterpret_cast<float4*>(base + x_bytes);
+    for (int v = tid; v < (kc >> 2) * E_tot; v += blockDim.x) cp_async_16(wdst + v, wsrc + v, 16u);
+    cp_async_commit();
+  };
+
+  issue(0);
+  for (int c = 0; c < n_chunks; ++c) {
+    if (c + 1 < n_chunks) {
+      issue(c + 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    const float4* wrow = wp + size_t(k0 >> 2) * E_tot;
-#pragma unroll 2
-    for (int kk = 0; kk < kc; kk += 4) {
+    const uint8_t* base = rsm + (c & 1) * stage_bytes;
+    const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(base);
+    const float4* ws = reinterpret_cast<const float4*>(base + x_bytes);
 #pragma unroll
-      for (int m = 0; m < kItems; ++m) {
-        if (tid + m * rt::kThreads < n_items) {
-          const float4 xv = *reinterpret_cast<const float4*>(&xs[it_t[m]][kk]);
-          const float4 wv = __ldg(wrow + size_t(kk >> 2) * E_tot + it_e[m]);
-          acc[m] = fmaf(xv.x, wv.x, acc[m]);
-          acc[m] = fmaf(xv.y, wv.y, acc[m]);
-          acc[m] = fmaf(xv.z, wv.z, acc[m]);
-          acc[m] = fmaf(xv.w, wv.w, acc[m]);
+    for (int m = 0; m < kItems; ++m) {
+      if (tid + m * rt::kThreads < n_items) {
+        const uint4* xrow = reinterpret_cast<const uint4*>(xs + it_t[m] * kc);
+        const float4* wcol = ws + it_e[m];
+        float a = acc[m];
+#pragma unroll 4
+        for (int kk = 0; kk < kc; kk += 8) {
+          const uint4 xv = xrow[kk >> 3];
+          const float4 w0 = wcol[(kk >> 2) * E_tot];
+          const float4 w1 = wcol[((kk >> 2) + 1) * E_tot];
+          // strictly ascending k: one fp32 FMA chain per logit
+          a = fmaf(bf16_lo(xv.x), w0.x, a);
+          a = fmaf(bf16_hi(xv.x), w0.y, a);
+          a = fmaf(bf16_lo(xv.y), w0.z, a);
+          a = fmaf(bf16_hi(xv.y), w0.w, a);
+          a = fmaf(bf16_lo(xv.z), w1.x, a);
+          a = fmaf(bf16_hi(xv.z), w1.y, a);
+          a = fmaf(bf16_lo(xv.w), w1.z, a);
+          a = fmaf(bf16_hi(xv.w), w1.w, a);
         }
+        acc[m] = a;
       }
     }
+    __syncthreads();
   }
 #pragma unroll
   for (int m = 0; m < kItems; ++m) {
@@ -204,11 +240,17 @@ int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* b
   const int items = (rt::kTokens * E_tot + rt::kThreads - 1) / rt::kThreads;
   const int grid = (T + rt::kTokens - 1) / rt::kTokens;
   const float4* wp = reinterpret_cast<const float4*>(wg_packed);
+  int kc = E_tot <= 16 ? 256 : 128;
+  while (d % kc) kc >>= 1;
+  if (kc < 8) return set_error(MP_E_SHAPE, "router: d=%d not a multiple of 8", d);
+  const size_t smem = size_t(2) * (rt::kTokens * kc * 2 + E_tot * kc * 4);
 #define MP_ROUTER_CASE(N)                                                                                       \
   case N:                                                                                                      \
-    router_kernel<N><<<grid, rt::kThreads, 0, stream>>>(x, wp, bias, T, d, E, has_gate ? 1 : 0, k, score_mode, \
-                                                        renorm, idx, w, shared_gate, hist, blk_counts,          \
-                                                        batch_counts);                                          \
+    if (smem > 48 * 1024)                                                                                      \
+      cudaFuncSetAttribute(router_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
+    router_kernel<N><<<grid, rt::kThreads, smem, stream>>>(x, wp, bias, T, d, E, has_gate ? 1 : 0, k, score_mode, \
+                                                           renorm, kc, idx, w, shared_gate, hist, blk_counts,    \
+                                                           batch_counts);                                        \
     break;
   switch (items) {
     MP_ROUTER_CASE(1)

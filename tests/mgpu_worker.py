@@ -1,0 +1,133 @@
+"""Multi-GPU parity worker (one process per GPU, launched by torchrun from test_gpu_multi.py).
+
+Every rank builds the same G-origin problem, runs its own origin through the
+B200 layer (count exchange + NVLink dispatch + tcgen05 experts + NVLink return)
+and checks against the CPU oracle computed for all origins:
+  * bit-exact: routed indices, the exchanged count table, per-pair target GPU
+    and receive row, reference-accounted remote bytes;
+  * tolerance: layer output (same bound as the single-GPU tests).
+Then it executes a migration (NVLink peer copies on a side stream, route swap
+after completion) and checks the new placement the same way.
+"""
+
+import os
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from oracle import moe_oracle as orc
+from paper_2508_12851_b200.layer import B200MoELayer
+from paper_2508_12851_b200.routing import route_table, uniform_links
+from paper_2508_12851_b200.shapes import LayerShape
+
+
+def check_close(got, ref, what):
+    err = float(np.abs(got - ref).max())
+    scale = float(np.abs(ref).max())
+    rel = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30))
+    assert err <= 2e-2 * scale + 1e-3 and rel <= 1e-2, f"{what}: max err {err} scale {scale} rel {rel}"
+
+
+def run_case(shape, G, rank, sets, sets2, T_list, seed):
+    dev = torch.device("cuda", torch.cuda.current_device())
+    E = shape.E
+    experts = {e: orc.synthetic_expert(e, shape.d, shape.f, seed) for e in range(E)}
+    shared = orc.synthetic_expert(999, shape.d, shape.shared_f, seed) if shape.shared_f else None
+    wg = orc.synthetic_router(E + shape.shared_gate, shape.d, seed)
+    biases = [orc.origin_bias(s, E, seed) for s in range(G)]
+    xs = [orc.synthetic_tokens(s, T_list[s], shape.d, seed) for s in range(G)]
+    lat, bw = uniform_links(G)
+
+    cap = max(len(s) for s in sets + sets2)
+    layer = B200MoELayer(shape, rank=rank, world=G, max_tokens=max(T_list), cap_slots=cap)
+    layer.open_peers()
+    layer.set_router(torch.from_numpy(wg[:E]), torch.from_numpy(biases[rank]),
+                     torch.from_numpy(wg[E]) if shape.shared_gate else None)
+    if shared is not None:
+        layer.set_shared(*(torch.from_numpy(w) for w in shared))
+    src = lambda e: tuple(torch.from_numpy(w) for w in experts[e])
+    layer.set_placement_sets(sets, src)
+    x = torch.from_numpy(xs[rank]).to(dev).bfloat16().contiguous()
+
+    def check(route, tag):
+        out = layer.forward(x)
+        torch.cuda.synchronize()
+        layer.check()
+        dist.barrier()
+        ref = orc.moe_layer_forward(shape, xs, wg[:E], biases, route, experts, shared,
+                                    wg[E] if shape.shared_gate else None)
+        T = T_list[rank]
+        assert np.array_equal(layer.idx[:T].cpu().numpy(), ref.idx[rank]), f"{tag}: idx"
+        assert np.array_equal(layer.read_counts(), ref.counts), f"{tag}: counts"
+        assert np.array_equal(layer.pos_dst[:T].cpu().numpy(), ref.pos_dst[rank]), f"{tag}: pos_dst"
+        assert np.array_equal(layer.pos_row[:T].cpu().numpy(), ref.pos_row[rank]), f"{tag}: pos_row"
+        acc = layer.dispatch_accounting()
+        assert acc["remote_bytes"] == orc.reference_remote_bytes(ref.counts, route, shape.d), f"{tag}: bytes"
+        check_close(out.float().cpu().numpy(), ref.out[rank], tag)
+        return out
+
+    route1 = route_table([frozenset(s) for s in sets], E, lat, bw, shape.d)
+    assert np.array_equal(layer.route, route1)
+    check(route1, "placement A")
+    # repeated forwards reuse the parity-double-buffered count tables
+    check(route1, "placement A again")
+
+    # ---- migration A -> B: gather every GPU's slot map, pull added experts over NVLink
+    slot_maps = [None] * G
+    dist.all_gather_object(slot_maps, layer.slot_of.tolist())
+    side = torch.cuda.Stream(dev)
+    done = torch.cuda.Event()
+    adds = layer.migrate_async(sets, sets2, slot_maps, side, done)
+    done.synchronize()
+    dist.barrier()  # every GPU's copies have landed
+    layer.finish_migration(sets2, adds)
+    route2 = route_table([frozenset(s) for s in sets2], E, lat, bw, shape.d)
+    assert np.array_equal(layer.route, route2)
+    # migrated weights are bit-identical to the source copies
+    for e, dst in adds:
+        w1, w3, w2 = layer.read_slot(dst)
+        assert np.array_equal(w1.float().cpu().numpy(), experts[e][0]), f"migrated W1 of expert {e}"
+        assert np.array_equal(w2.float().cpu().numpy(), experts[e][2]), f"migrated W2 of expert {e}"
+    check(route2, "placement B (after migration)")
+    layer.close()
+
+
+def main():
+    dist.init_process_group("gloo")
+    rank, G = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+
+    # case 1: toy-like shape, replicated experts; origins with different T (ragged)
+    shape = LayerShape("toy_small", d=512, f=512, E=8, k=2)
+    sets = [sorted({(g * 8 // G + i) % 8 for i in range(8 // G + 1)}) for g in range(G)]
+    sets2 = [sorted({(g * 8 // G + i + 3) % 8 for i in range(8 // G + 1)}) for g in range(G)]
+    run_case(shape, G, rank, sets, sets2, [200 + 37 * s for s in range(G)], seed=1)
+
+    # case 2: DeepSeek-like routing (64 experts, top-6, shared experts), one GPU holding few experts
+    shape = LayerShape("ds_small", d=256, f=256, E=64, k=6, score_mode=1, shared_f=512)
+    per = 64 // G
+    sets = [sorted(set(range(g * per, (g + 1) * per)) | {(g * per + per) % 64}) for g in range(G)]
+    sets2 = [sorted(set(range(g * per, (g + 1) * per)) | {(g * per + per + 1) % 64, (g * per + 2 * per + 5) % 64})
+             for g in range(G)]
+    run_case(shape, G, rank, sets, sets2, [150] * G, seed=2)
+
+    # case 3: Qwen-like (softmax-top4 + sigmoid-gated shared expert)
+    shape = LayerShape("qwen_small", d=256, f=384, E=60, k=4, score_mode=1, shared_f=512, shared_gate=1)
+    per = -(-60 // G)
+    sets = [sorted(set(range(g * per, min(60, (g + 1) * per)))) for g in range(G)]
+    sets2 = [sorted(set(range(g * per, min(60, (g + 1) * per))) | {(g * per + per + 2) % 60}) for g in range(G)]
+    run_case(shape, G, rank, sets, sets2, [96 + 16 * s for s in range(G)], seed=3)
+
+    dist.barrier()
+    if rank == 0:
+        print(f"mgpu ok: G={G}")
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
