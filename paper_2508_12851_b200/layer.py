@@ -29,6 +29,7 @@ import torch
 
 from . import _lib
 from .errors import InfeasibleError
+from .migration import plan_pulls
 from .routing import dispatch_accounting, gpu_expert_sets, route_table_for, server_expert_sets, route_table
 from .shapes import LayerShape
 
@@ -262,19 +263,8 @@ class B200MoELayer:
     def plan_migration(self, old_sets, new_sets):
         """Copy ops for this GPU: every expert added here pulls from the lowest-id old holder
         (the slot diff `new.slots - old.slots` of migration_cost, cost.py:186-187)."""
-        mine_old = set(old_sets[self.rank])
-        ops, adds = [], []
-        free = [s for s in self._free]
-        for e in sorted(set(new_sets[self.rank]) - mine_old):
-            holders = [n for n in range(self.world) if e in old_sets[n]]
-            if not holders:
-                raise RuntimeError(f"expert {e} has no holder in the old placement")
-            if not free:
-                raise InfeasibleError(f"GPU {self.rank}: no staging slot left for expert {e}")
-            dst = free.pop(0)
-            adds.append((e, dst))
-            ops.append((holders[0], e, dst))
-        return ops, adds
+        pulls = plan_pulls(self.rank, old_sets, new_sets, self._free)
+        return [(p.src_rank, p.expert, p.dst_slot) for p in pulls], [(p.expert, p.dst_slot) for p in pulls]
 
     def migrate_async(self, old_sets, new_sets, peer_slot_of, stream: torch.cuda.Stream, event: torch.cuda.Event):
         """Issue this GPU's weight pulls on `stream`; `peer_slot_of[n][e]` = slot of e on GPU n."""

@@ -122,3 +122,27 @@ def dispatch_accounting(counts: np.ndarray, route: np.ndarray, d: int, bpe: int 
         "local_ratio": local / total if total else 0.0,
         "pairs": P.tolist(),
     }
+
+
+def receive_layout(counts: np.ndarray, route: np.ndarray):
+    """Host mirror of the GPU layout kernel (csrc/dispatch.cu): per-GPU receive groups.
+
+    Returns (M[D][e] rows GPU D computes for expert e, send_base[s][e] first
+    row of origin s's expert-e rows in GPU route[s][e]'s receive buffer).
+    Receive buffers are ordered by expert, then source GPU, then (token, slot).
+    """
+    counts = np.asarray(counts, dtype=np.int64)
+    G, E = counts.shape
+    M = np.zeros((G, E), dtype=np.int64)
+    for s in range(G):
+        np.add.at(M, (route[s], np.arange(E)), counts[s])
+    base = np.zeros((G, E), dtype=np.int64)
+    base[:, 1:] = np.cumsum(M, axis=1)[:, :-1]
+    send = np.zeros((G, E), dtype=np.int64)
+    seen = np.zeros((G, E), dtype=np.int64)
+    for s in range(G):
+        for e in range(E):
+            D = route[s, e]
+            send[s, e] = base[D, e] + seen[D, e]
+            seen[D, e] += counts[s, e]
+    return M, send

@@ -1,0 +1,112 @@
+"""Host-side logic of the drop-in (CPU): shapes, route tables from reference placements,
+accounting, migration planning, the bench placement fallback documents."""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2508_12851_b200 import routing
+from paper_2508_12851_b200.errors import import_moeplace
+from paper_2508_12851_b200.migration import plan_pulls, slot_diff
+from paper_2508_12851_b200.shapes import DEEPSEEK, MIXTRAL, QWEN, SHAPES, TOY, get_shape, slot_caps
+
+REPO = Path(__file__).resolve().parent.parent
+
+
+def test_shapes_expert_bytes_and_flops():
+    assert MIXTRAL.expert_bytes == 352_321_536
+    assert QWEN.expert_bytes == DEEPSEEK.expert_bytes == 17_301_504
+    assert MIXTRAL.flops_per_token() == 704_643_072
+    assert QWEN.flops_per_token() == DEEPSEEK.flops_per_token() == 138_412_032
+    for s in SHAPES.values():
+        assert s.d % 256 == 0 and s.f % 128 == 0 and s.shared_f % 128 == 0
+    assert get_shape("ds") is DEEPSEEK
+
+
+@pytest.mark.parametrize("shape", [TOY, MIXTRAL, QWEN, DEEPSEEK], ids=lambda s: s.name)
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_caps_cover_all_experts(shape, G):
+    caps = slot_caps(shape, G)
+    assert len(caps) == G and sum(caps) >= shape.E
+    if shape is QWEN and G == 8:
+        assert caps == [12, 10, 8, 8, 8, 6, 6, 6]
+    if shape is MIXTRAL and G == 8:
+        assert caps == [2] * 8
+
+
+def test_route_table_from_placement_document():
+    doc = {"layers": [{"layer": 0, "servers": [{"server": 0, "gpus": [[0, 1, 2]]},
+                                                 {"server": 1, "gpus": [[2, 3]]}]}]}
+    lat, bw = routing.uniform_links(2)
+    r = routing.route_table(routing.server_expert_sets(doc), 4, lat, bw, 512)
+    assert r.tolist() == [[0, 0, 0, 1], [0, 0, 1, 1]]
+    assert routing.gpu_expert_sets(doc) == [[0, 1, 2], [2, 3]]
+
+
+def test_route_table_from_reference_placement_object():
+    mp = import_moeplace()
+    if mp is None:
+        pytest.skip("reference not importable")
+    p = mp.Placement(((frozenset({(0, 0), (0, 1)}),), (frozenset({(0, 1), (0, 2), (0, 3)}),)), 1)
+    servers = tuple(mp.ServerSpec(n, (mp.GpuSpec(4e6, 5e8),)) for n in range(2))
+    lat, bw = routing.uniform_links(2)
+    cluster = mp.ClusterSpec(servers, bw, lat)
+    r = routing.route_table_for(p, cluster, 4, 512)
+    assert r.tolist() == [[0, 0, 1, 1], [0, 1, 1, 1]]
+
+
+def test_slot_map_and_capacity():
+    from paper_2508_12851_b200 import InfeasibleError
+    assert routing.slot_map([5, 1], 8, 3).tolist() == [-1, 0, -1, -1, -1, 1, -1, -1]
+    with pytest.raises(InfeasibleError):
+        routing.slot_map([1, 2, 3], 8, 2)
+
+
+def test_dispatch_accounting_reference_formula():
+    counts = np.array([[5, 3, 0, 2], [1, 1, 1, 1]])
+    route = np.array([[0, 0, 1, 1], [0, 0, 1, 1]])
+    acc = routing.dispatch_accounting(counts, route, 4096)
+    assert acc["remote_invocations"] == 2 + 2
+    assert acc["remote_bytes"] == 2.0 * 4 * 4096 * 2   # sim.py:454, payload d*bpe per token
+    assert acc["local_ratio"] == pytest.approx((8 + 2) / 14)
+
+
+def test_plan_pulls_uses_lowest_old_holder_and_free_slots():
+    old = [[0, 1, 2], [2, 3], [0, 3]]
+    new = [[0, 1, 3], [1, 2, 3], [0, 2]]
+    p0 = plan_pulls(0, old, new, free_slots=[7, 5])
+    assert [(p.expert, p.src_rank, p.dst_slot) for p in p0] == [(3, 1, 5)]
+    p1 = plan_pulls(1, old, new, free_slots=[4])
+    assert [(p.expert, p.src_rank, p.dst_slot) for p in p1] == [(1, 0, 4)]
+    p2 = plan_pulls(2, old, new, free_slots=[9])
+    assert [(p.expert, p.src_rank) for p in p2] == [(2, 0)]
+    added, removed = slot_diff(old, new)
+    assert len(added) == 3 and len(removed) == 2
+    from paper_2508_12851_b200 import InfeasibleError
+    with pytest.raises(InfeasibleError):
+        plan_pulls(1, old, new, free_slots=[])
+
+
+def test_bench_placement_documents_are_valid():
+    docs = json.loads((REPO / "paper_2508_12851_b200" / "placements" / "bench_placements.json").read_text())
+    assert any(k.startswith("mixtral-8x7b_G8_ours") for k in docs)
+    for key, d in docs.items():
+        name, G, strat = key.rsplit("_", 2)
+        shape = get_shape(name)
+        sets = routing.gpu_expert_sets(d["placement"])
+        assert len(sets) == int(G[1:])
+        assert set().union(*map(set, sets)) == set(range(shape.E)), key          # coverage
+        assert all(len(s) <= c for s, c in zip(sets, d["caps"])), key           # memory caps
+
+
+def test_interleave_w13_layout():
+    torch = pytest.importorskip("torch")
+    from paper_2508_12851_b200.layer import interleave_w13
+    f, d = 256, 8
+    w1 = torch.arange(f * d).reshape(f, d).float()
+    w3 = -w1
+    w13 = interleave_w13(w1, w3)
+    assert torch.equal(w13[0:128], w1[0:128]) and torch.equal(w13[128:256], w3[0:128])
+    assert torch.equal(w13[256:384], w1[128:256]) and torch.equal(w13[384:512], w3[128:256])
