@@ -298,3 +298,51 @@ class B200MoELayer:
             link_bandwidth = np.full((G, G), 770e9)
         route = route_table([frozenset(s) for s in new_sets], E, link_latency, link_bandwidth, self.shape.d)
         self.set_routes(route, slot_of)
+
+
+class HostPipeline:
+    """Streams token batches from pinned host memory through a B200MoELayer.
+
+    Serving-style end-to-end path: batch i's host->device copy runs on a copy-in
+    stream while batch i-1 is in the layer and batch i-2's output drains on a
+    copy-out stream (PCIe is full duplex), with double-buffered device tensors.
+    Each batch still crosses the host boundary in full: x in, layer output out.
+    """
+
+    def __init__(self, layer: B200MoELayer, T: int):
+        self.layer = layer
+        dev = layer.device
+        d = layer.shape.d
+        self.xd = [torch.empty(T, d, device=dev, dtype=torch.bfloat16) for _ in range(2)]
+        self.od = [torch.empty(T, d, device=dev, dtype=torch.bfloat16) for _ in range(2)]
+        self.s_in = torch.cuda.Stream(dev)
+        self.s_out = torch.cuda.Stream(dev)
+        self.compute = torch.cuda.current_stream(dev)
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(2)]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.n = 0
+
+    def submit(self, x_host: torch.Tensor, out_host: torch.Tensor) -> None:
+        """Enqueue one batch: x_host [T, d] pinned bf16 -> layer -> out_host [T, d] pinned bf16."""
+        b = self.n & 1
+        if self.n >= 2:
+            self.s_in.wait_event(self.ev_comp[b])      # xd[b] free once batch n-2 left the layer
+        with torch.cuda.stream(self.s_in):
+            self.xd[b].copy_(x_host, non_blocking=True)
+            self.ev_in[b].record(self.s_in)
+        self.compute.wait_event(self.ev_in[b])
+        if self.n >= 2:
+            self.compute.wait_event(self.ev_out[b])    # od[b] drained to the host
+        with torch.cuda.stream(self.compute):
+            self.layer.forward(self.xd[b], self.od[b])
+            self.ev_comp[b].record(self.compute)
+        self.s_out.wait_event(self.ev_comp[b])
+        with torch.cuda.stream(self.s_out):
+            out_host.copy_(self.od[b], non_blocking=True)
+            self.ev_out[b].record(self.s_out)
+        self.n += 1
+
+    def drain(self) -> None:
+        self.s_out.synchronize()
+        self.compute.synchronize()
