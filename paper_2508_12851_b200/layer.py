@@ -246,6 +246,26 @@ class B200MoELayer:
         """Cumulative per-expert token counts of this origin (fused router histogram)."""
         return self.hist.cpu().numpy().astype(np.int64)
 
+    def gathered_counts(self, group=None) -> np.ndarray:
+        """[G, E] cumulative histograms of all origins (all-gather over torch.distributed)."""
+        h = self.hist.clone()
+        if self.world == 1:
+            return h[None].cpu().numpy().astype(np.int64)
+        import torch.distributed as dist
+        parts = [torch.zeros_like(h) for _ in range(self.world)]
+        dist.all_gather(parts, h, group=group) if dist.get_backend(group) == "nccl" else \
+            dist.all_gather(parts, h.cpu(), group=group)
+        return torch.stack([p.cpu() for p in parts]).numpy().astype(np.int64)
+
+    def activation_stats(self, group=None):
+        """The GPU histogram as reference ActivationStats (stats.py:67-80); token_count 1 per token."""
+        from .errors import import_moeplace
+        mp = import_moeplace()
+        if mp is None:
+            raise RuntimeError("the reference package moeplace is not importable")
+        counts = self.gathered_counts(group).astype(float)
+        return mp.ActivationStats.from_counts(counts[:, None, :], (self.shape.E,))
+
     def reset_counts(self) -> None:
         self.hist.zero_()
 
