@@ -56,8 +56,10 @@ int mp_last_error(char* buf, int buf_len);
  * --------------------------------------------------------------------- */
 
 /* Repack router weights Wg [E_tot, d] bf16 into the kernel layout
- * [d/4][E_tot][4] fp32 (E_tot = E, or E+1 with the shared-expert gate row). */
-int mp_router_pack(const void* wg_bf16, int E_tot, int d, float* packed, void* stream);
+ * [d][E_pad] fp32 (Wg transposed), E_pad = E_tot rounded up to a multiple of
+ * 8 (zero columns); `packed` must hold E_pad * d floats.  E_tot = E, or E+1
+ * with the shared-expert gate row. */
+int mp_router_pack(const void* wg_bf16, int E_tot, int d, void* packed, void* stream);
 
 /* K1 -- replaces ActivationStats.ingest (stats.py:82-96) fed by sampled expert
  * sets (sim.py:181-185): top-k routing of T tokens plus a fused histogram.
@@ -68,7 +70,7 @@ int mp_router_pack(const void* wg_bf16, int E_tot, int d, float* packed, void* s
  *   gate_out [T] fp32 out or NULL  sigmoid shared-expert gate (has_gate = 1)
  *   hist     [E] uint32 in/out     += tokens routed to each expert (token_count 1)
  */
-int mp_router_topk_hist(const void* x, const float* packed, const float* bias, int T, int d, int E, int has_gate,
+int mp_router_topk_hist(const void* x, const void* packed, const float* bias, int T, int d, int E, int has_gate,
                         int k, int score_mode, int renorm, int32_t* idx, float* w, float* gate_out, uint32_t* hist,
                         void* stream);
 

@@ -135,17 +135,18 @@ int mp_last_error(char* buf, int buf_len) {
   return MP_OK;
 }
 
-int mp_router_pack(const void* wg_bf16, int E_tot, int d, float* packed, void* stream) {
+int mp_router_pack(const void* wg_bf16, int E_tot, int d, void* packed, void* stream) {
   if (!wg_bf16 || !packed) return set_error(MP_E_ARG, "mp_router_pack: null pointer");
-  return launch_router_pack(static_cast<const __nv_bfloat16*>(wg_bf16), E_tot, d, packed,
+  return launch_router_pack(static_cast<const __nv_bfloat16*>(wg_bf16), E_tot, d, static_cast<float*>(packed),
                             static_cast<cudaStream_t>(stream));
 }
 
-int mp_router_topk_hist(const void* x, const float* packed, const float* bias, int T, int d, int E, int has_gate,
+int mp_router_topk_hist(const void* x, const void* packed, const float* bias, int T, int d, int E, int has_gate,
                         int k, int score_mode, int renorm, int32_t* idx, float* w, float* gate_out, uint32_t* hist,
                         void* stream) {
   if (!x || !packed || !idx || !w) return set_error(MP_E_ARG, "mp_router_topk_hist: null pointer");
-  return launch_router(static_cast<const __nv_bfloat16*>(x), packed, bias, T, d, E, has_gate, k, score_mode, renorm,
+  return launch_router(static_cast<const __nv_bfloat16*>(x), static_cast<const float*>(packed), bias, T, d,
+                       E, has_gate, k, score_mode, renorm,
                        idx, w, gate_out, hist, nullptr, nullptr, static_cast<cudaStream_t>(stream));
 }
 
@@ -225,7 +226,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
     auto plan = [&](Carver& cv) {
       L->h = cv.take<__nv_bfloat16>(size_t(L->recv_cap) * D.f);
       L->wg = cv.take<__nv_bfloat16>(size_t(E_tot) * D.d);
-      L->wg_packed = cv.take<float>(size_t(E_tot) * D.d);
+      L->wg_packed = cv.take<float>(size_t(router_e_pad(E_tot)) * D.d);
       L->bias = cv.take<float>(E);
       L->w = cv.take<float>(size_t(T) * k);
       L->sgate = D.shared_gate ? cv.take<float>(T) : nullptr;

@@ -20,33 +20,43 @@ namespace mp {
 
 // ------------------------------------------------------------------ layout
 // One CTA.  Computes this rank's send offsets, the per-router-block prefix and
-// the local GEMM group table from the all-gathered counts.
-__global__ void __launch_bounds__(256)
+// the local GEMM group table from the all-gathered counts.  Every global input
+// is first pulled into shared memory with coalesced loads (the block-count
+// matrix too), so no thread walks a chain of dependent global loads.
+__global__ void __launch_bounds__(1024)
     layout_kernel(const int32_t* __restrict__ counts_all, const int32_t* __restrict__ route,
                   const int32_t* __restrict__ slot_of, const int32_t* __restrict__ blk_counts, int nb, int G, int E,
                   int rank, int32_t* __restrict__ my_base, int32_t* __restrict__ blk_prefix,
                   int32_t* __restrict__ groups, int32_t* __restrict__ n_groups, int32_t* __restrict__ recv_rows) {
-  __shared__ int M[8][64];      // rows each GPU receives per expert
-  __shared__ int part[64][32];  // per-(expert, segment) block-count partial sums
-  const int tid = threadIdx.x;
-  for (int i = tid; i < G * E; i += blockDim.x) {
+  extern __shared__ int bc[];               // [nb][E] block counts
+  __shared__ int C[8][64], R[8][64];        // counts_all, route
+  __shared__ int M[8][64];                  // rows each GPU receives per expert
+  __shared__ int part[64][33];              // per-(expert, segment) partial sums
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < G * E; i += nt) {
+    C[i / E][i % E] = counts_all[i];
+    R[i / E][i % E] = route[i];
+  }
+  for (int i = tid; i < nb * E; i += nt) bc[i] = blk_counts[i];
+  __syncthreads();
+  for (int i = tid; i < G * E; i += nt) {
     const int D = i / E, e = i - D * E;
     int m = 0;
     for (int s = 0; s < G; ++s)
-      if (route[s * E + e] == D) m += counts_all[s * E + e];
+      if (R[s][e] == D) m += C[s][e];
     M[D][e] = m;
   }
   __syncthreads();
   if (tid < E) {
     const int e = tid;
-    const int D = route[rank * E + e];
+    const int D = R[rank][e];
     int base = 0;
     for (int e2 = 0; e2 < e; ++e2) base += M[D][e2];
     for (int s = 0; s < rank; ++s)
-      if (route[s * E + e] == D) base += counts_all[s * E + e];
+      if (R[s][e] == D) base += C[s][e];
     my_base[e] = base;
   }
-  if (tid == 0) {
+  if (tid == 32) {
     int ng = 0, row = 0;
     for (int e = 0; e < E; ++e) {
       const int m = M[rank][e];
@@ -62,23 +72,24 @@ __global__ void __launch_bounds__(256)
     *n_groups = ng;
     *recv_rows = row;
   }
-  // exclusive scan of blk_counts over blocks, per expert: P threads per expert
+  // exclusive scan of the block counts over blocks, per expert: P threads per expert
   int P = 1;
-  while (P * 2 * E <= int(blockDim.x) && P * 2 <= 32) P *= 2;
+  while (P * 2 * E <= nt && P * 2 <= 32) P *= 2;
   const int e = tid / P, p = tid - (tid / P) * P;
   const int seg = (nb + P - 1) / P;
   const int b0 = min(nb, p * seg), b1 = min(nb, b0 + seg);
-  int sum = 0;
-  if (e < E)
-    for (int b = b0; b < b1; ++b) sum += blk_counts[size_t(b) * E + e];
-  if (e < E) part[e][p] = sum;
+  if (e < E) {
+    int sum = 0;
+    for (int b = b0; b < b1; ++b) sum += bc[b * E + e];
+    part[e][p] = sum;
+  }
   __syncthreads();
   if (e < E) {
     int run = 0;
     for (int q = 0; q < p; ++q) run += part[e][q];
     for (int b = b0; b < b1; ++b) {
       blk_prefix[size_t(b) * E + e] = run;
-      run += blk_counts[size_t(b) * E + e];
+      run += bc[b * E + e];
     }
   }
 }
@@ -88,25 +99,33 @@ int launch_layout(const int32_t* counts_all, const int32_t* route, const int32_t
                   int32_t* n_groups, int32_t* recv_rows, cudaStream_t stream) {
   if (G < 1 || G > 8) return set_error(MP_E_SHAPE, "layout: G=%d outside [1, 8]", G);
   if (E < 1 || E > 64) return set_error(MP_E_SHAPE, "layout: E=%d outside [1, 64]", E);
-  layout_kernel<<<1, 256, 0, stream>>>(counts_all, route, slot_of, blk_counts, nb, G, E, rank, my_base, blk_prefix,
-                                       groups, n_groups, recv_rows);
+  const size_t smem = size_t(nb) * E * 4;
+  if (smem > 180 * 1024) return set_error(MP_E_SHAPE, "layout: %d router blocks x %d experts too large", nb, E);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(layout)");
+    attr = true;
+  }
+  layout_kernel<<<1, 1024, smem, stream>>>(counts_all, route, slot_of, blk_counts, nb, G, E, rank, my_base,
+                                           blk_prefix, groups, n_groups, recv_rows);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "layout_kernel launch");
 }
 
 // ------------------------------------------------------------------ K2 permute + dispatch
-// CTA = one router block of 16 tokens (the histogram blocks), 128 threads.
+// CTA = one router block of 32 tokens (the histogram blocks), 256 threads.
 // Phase 1: one thread per (token, slot) pair computes its stable in-block rank.
 // Phase 2: one warp per token loads the x row once (16 B per lane per step) and
 //          stores it to its k destinations, local or peer (NVLink) rows.
 template <int kVecPerLane>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
                    const int32_t* __restrict__ route_row, const int32_t* __restrict__ my_base,
                    const int32_t* __restrict__ blk_prefix, int T, int d, int E, int k,
                    __nv_bfloat16* const* __restrict__ recv_ptrs, int32_t* __restrict__ pos_dst,
                    int32_t* __restrict__ pos_row) {
-  constexpr int kTok = 16;
+  constexpr int kTok = 32;
   __shared__ int s_e[kTok * 8];
   __shared__ int s_dst[kTok * 8];
   __shared__ int s_row[kTok * 8];
@@ -131,7 +150,7 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
   const int warp = warp_id(), lane = lane_id();
   const int nvec = d / 8;  // 16 B vectors per row
-  for (int tt = warp; tt < nt; tt += 4) {
+  for (int tt = warp; tt < nt; tt += 8) {
     const __nv_bfloat16* src = x + size_t(t0 + tt) * d;
     uint4 v[kVecPerLane];
 #pragma unroll
@@ -156,10 +175,10 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "permute: d=%d not a multiple of 8", d);
   if (k > 8) return set_error(MP_E_SHAPE, "permute: top_k=%d > 8", k);
   if (T <= 0) return MP_OK;
-  const int grid = (T + 15) / 16;
+  const int grid = (T + 31) / 32;
   const int vpl = (d / 8 + 31) / 32;
 #define MP_PERM_LAUNCH(N)                                                                                  \
-  permute_kernel<N><<<grid, 128, 0, stream>>>(x, idx, route_row, my_base, blk_prefix, T, d, E, k, recv_ptrs, \
+  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route_row, my_base, blk_prefix, T, d, E, k, recv_ptrs, \
                                               pos_dst, pos_row)
   if (vpl <= 1) MP_PERM_LAUNCH(1);
   else if (vpl <= 2) MP_PERM_LAUNCH(2);
@@ -177,44 +196,44 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
 // One warp per token.  out[t] = bf16( sum_{j<k} w[t,j] * y_{dst_j}[row_j] (+ g[t] * ysh[t]) )
 // accumulated in fp32 in ascending j (deterministic).  y rows that live on a
 // peer GPU are read straight over NVLink (the "return all-to-all").
+template <int K>
 __global__ void __launch_bounds__(256)
     combine_kernel(__nv_bfloat16* const* __restrict__ y_ptrs, const int32_t* __restrict__ pos_dst,
-                   const int32_t* __restrict__ pos_row, const float* __restrict__ w, int T, int d, int k,
+                   const int32_t* __restrict__ pos_row, const float* __restrict__ w, int T, int d,
                    const __nv_bfloat16* __restrict__ shared_y, const float* __restrict__ shared_gate,
                    __nv_bfloat16* __restrict__ out) {
   const int t = blockIdx.x * 8 + warp_id();
   if (t >= T) return;
   const int lane = lane_id();
-  const __nv_bfloat16* src[8];
-  float wj[8];
-  for (int j = 0; j < k; ++j) {
-    src[j] = y_ptrs[pos_dst[size_t(t) * k + j]] + size_t(pos_row[size_t(t) * k + j]) * d;
-    wj[j] = w[size_t(t) * k + j];
+  const __nv_bfloat16* src[K];
+  float wj[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    src[j] = y_ptrs[pos_dst[size_t(t) * K + j]] + size_t(pos_row[size_t(t) * K + j]) * d;
+    wj[j] = w[size_t(t) * K + j];
   }
   const float g = shared_gate ? shared_gate[t] : 1.0f;
   const int nvec = d / 8;
+#pragma unroll 4
   for (int c = lane; c < nvec; c += 32) {
-    uint4 v[8];
+    uint4 v[K];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < k) v[j] = ld_v4(src[j] + 8 * c);
+    for (int j = 0; j < K; ++j) v[j] = ld_v4(src[j] + 8 * c);
     float acc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.f;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j < k) {
-        const uint32_t u[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+    for (int j = 0; j < K; ++j) {
+      const uint32_t u[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          acc[2 * q] = fmaf(wj[j], bf16_lo(u[q]), acc[2 * q]);
-          acc[2 * q + 1] = fmaf(wj[j], bf16_hi(u[q]), acc[2 * q + 1]);
-        }
+      for (int q = 0; q < 4; ++q) {
+        acc[2 * q] = fmaf(wj[j], bf16_lo(u[q]), acc[2 * q]);
+        acc[2 * q + 1] = fmaf(wj[j], bf16_hi(u[q]), acc[2 * q + 1]);
       }
     }
     if (shared_y) {
-      const uint4 s = ld_nc_v4(shared_y + size_t(t) * d + 8 * c);
-      const uint32_t u[4] = {s.x, s.y, s.z, s.w};
+      const uint4 sv = ld_nc_v4(shared_y + size_t(t) * d + 8 * c);
+      const uint32_t u[4] = {sv.x, sv.y, sv.z, sv.w};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         acc[2 * q] = fmaf(g, bf16_lo(u[q]), acc[2 * q]);
@@ -234,9 +253,16 @@ int launch_combine(__nv_bfloat16* const* y_ptrs, const int32_t* pos_dst, const i
                    int T, int d, int k, const __nv_bfloat16* shared_y, const float* shared_gate,
                    __nv_bfloat16* out, cudaStream_t stream) {
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "combine: d=%d not a multiple of 8", d);
-  if (k > 8) return set_error(MP_E_SHAPE, "combine: top_k=%d > 8", k);
+  if (k < 1 || k > 8) return set_error(MP_E_SHAPE, "combine: top_k=%d outside [1, 8]", k);
   if (T <= 0) return MP_OK;
-  combine_kernel<<<(T + 7) / 8, 256, 0, stream>>>(y_ptrs, pos_dst, pos_row, w, T, d, k, shared_y, shared_gate, out);
+  const int grid = (T + 7) / 8;
+  switch (k) {
+#define MP_COMBINE_CASE(N) \
+  case N: combine_kernel<N><<<grid, 256, 0, stream>>>(y_ptrs, pos_dst, pos_row, w, T, d, shared_y, shared_gate, out); break;
+    MP_COMBINE_CASE(1) MP_COMBINE_CASE(2) MP_COMBINE_CASE(3) MP_COMBINE_CASE(4)
+    MP_COMBINE_CASE(5) MP_COMBINE_CASE(6) MP_COMBINE_CASE(7) MP_COMBINE_CASE(8)
+#undef MP_COMBINE_CASE
+  }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "combine_kernel launch");
 }

@@ -20,6 +20,7 @@ int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* b
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, cudaStream_t stream);
 int router_block_tokens();
+__host__ __device__ int router_e_pad(int E_tot);
 int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, float* packed, cudaStream_t stream);
 
 // ---- layout (count exchange result -> offsets, group table)

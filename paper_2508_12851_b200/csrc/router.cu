@@ -18,38 +18,52 @@
 // rn(acc + x*w); the oracle restates this with numpy float32 adds.  Selection
 // compares logits only, so the indices do not depend on the exp implementation.
 //
-// Layout: Wg is repacked once into [d/4][E_tot][4] fp32 so that threads owning
-// consecutive experts read consecutive 16 B words.  A CTA owns 16 tokens; the x
-// rows and the matching Wg columns are staged through shared memory in k-chunks
-// by a double-buffered cp.async pipeline, so the FMA chains only see LDS latency.
+// Layout: Wg is repacked once into [d][E_pad] fp32 (Wg^T, E_pad = E_tot
+// rounded up to 8, zero columns), so the TE weights of one k are contiguous.  A CTA owns 32 tokens (one per lane) and all experts (TE per
+// warp); x rows and Wg columns are staged through shared memory in k-chunks by
+// a double-buffered cp.async pipeline.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "mp_internal.h"
 
 namespace mp {
 
 namespace rt {
-constexpr int kThreads = 128;
-constexpr int kTokens = 16;    // tokens per CTA
+constexpr int kTokens = 32;    // tokens per CTA (also the permute / histogram block)
 constexpr int kMaxE = 64;      // routed experts
-constexpr int kMaxItems = (kTokens * (kMaxE + 1) + kThreads - 1) / kThreads;
 constexpr int kMaxK = 8;
 }  // namespace rt
 
 int router_block_tokens() { return rt::kTokens; }
+__host__ __device__ int router_e_pad(int E_tot) { return (E_tot + 7) / 8 * 8; }
 
-__global__ void router_pack_kernel(const __nv_bfloat16* __restrict__ wg, int E_tot, int d, float* __restrict__ packed) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over E_tot * d
-  if (i >= E_tot * d) return;
-  const int e = i / d, k = i - e * d;
-  packed[(size_t(k >> 2) * E_tot + e) * 4 + (k & 3)] = __bfloat162float(wg[i]);
+// packed[k][E_pad] fp32 = Wg[e][k] (Wg transposed; zero columns pad E_tot up to E_pad)
+__global__ void router_pack_kernel(const __nv_bfloat16* __restrict__ wg, int E_tot, int E_pad, int d,
+                                   float* __restrict__ packed) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over d * E_pad
+  if (i >= E_pad * d) return;
+  const int k = i / E_pad, e = i - k * E_pad;
+  packed[i] = e < E_tot ? __bfloat162float(wg[size_t(e) * d + k]) : 0.0f;
 }
 
 int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, float* packed, cudaStream_t stream) {
-  if (d % 4 != 0) return set_error(MP_E_SHAPE, "router d=%d not a multiple of 4", d);
-  const int n = E_tot * d;
-  router_pack_kernel<<<(n + 255) / 256, 256, 0, stream>>>(wg, E_tot, d, packed);
+  if (d % 8 != 0) return set_error(MP_E_SHAPE, "router d=%d not a multiple of 8", d);
+  const int E_pad = router_e_pad(E_tot);
+  const int n = E_pad * d;
+  router_pack_kernel<<<(n + 255) / 256, 256, 0, stream>>>(wg, E_tot, E_pad, d, packed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_pack_kernel launch");
+}
+
+// acc = (acc.lo + x*w.lo, acc.hi + x*w.hi): two independent fp32 FMAs (FFMA2),
+// each rounded exactly like fmaf -- the per-logit chain contract is unchanged.
+MP_DEV void ffma2(unsigned long long& acc, float x, unsigned long long w) {
+  const unsigned long long xx = (unsigned long long)__float_as_uint(x) | ((unsigned long long)__float_as_uint(x) << 32);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xx), "l"(w));
+}
+MP_DEV unsigned long long pack2(float lo, float hi) {
+  return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
 }
 
 // Larger logit wins; equal logits -> lower expert id.
@@ -65,105 +79,104 @@ MP_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-// Shared memory per stage: x chunk [16][kc] bf16 + Wg chunk [kc/4][E_tot][4] fp32,
-// double-buffered and filled with cp.async while the previous chunk is consumed.
-template <int kItems>
-__global__ void __launch_bounds__(rt::kThreads)
-    router_kernel(const __nv_bfloat16* __restrict__ x, const float4* __restrict__ wp, const float* __restrict__ bias,
+// CTA = 32 tokens x (E_pad / TE) warps.  Lane = token, warp = a group of TE
+// consecutive experts: every x element is loaded once per thread and feeds TE
+// independent fp32 chains, two per FFMA2 instruction; the Wg values of one k
+// are warp-uniform (shared-memory broadcast).  Per stage, shared memory holds
+// the x chunk [32][kc+8] bf16 (padded rows: conflict-free 16 B lane loads) and
+// the Wg chunk [kc][E_pad] fp32; kStages-deep cp.async ring.
+constexpr int kStages = 4;
+template <int TE>
+__global__ void __launch_bounds__(256)
+    router_kernel(const __nv_bfloat16* __restrict__ x, const uint4* __restrict__ wp, const float* __restrict__ bias,
                   int T, int d, int E, int has_gate, int k, int score_mode, int renorm, int kc,
                   int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
                   uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts) {
   extern __shared__ __align__(16) uint8_t rsm[];
-  __shared__ float logits[rt::kTokens][rt::kMaxE + 1];
+  __shared__ float logits[rt::kTokens][rt::kMaxE + 2];
   __shared__ int cnt_s[rt::kMaxE];
 
   const int E_tot = E + has_gate;
+  const int E_pad = router_e_pad(E_tot);
   const int t0 = blockIdx.x * rt::kTokens;
-  const int tid = threadIdx.x;
-  const int x_bytes = rt::kTokens * kc * 2;
-  const int w_bytes = E_tot * kc * 4;
+  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  const int pitch = kc + 8;                       // bf16 elements per staged x row
+  const int x_bytes = rt::kTokens * pitch * 2;
+  const int w_bytes = kc * E_pad * 4;
   const int stage_bytes = x_bytes + w_bytes;
   for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
 
-  int it_t[kItems], it_e[kItems];
-  float acc[kItems];
+  unsigned long long acc[TE / 2];
 #pragma unroll
-  for (int m = 0; m < kItems; ++m) {
-    const int i = tid + m * rt::kThreads;
-    it_t[m] = i / E_tot;
-    it_e[m] = i - it_t[m] * E_tot;
-    acc[m] = 0.0f;
-  }
-  const int n_items = rt::kTokens * E_tot;
+  for (int j = 0; j < TE / 2; ++j) acc[j] = 0ull;
+  const int e0 = warp * TE;
   const int n_chunks = d / kc;
 
   auto issue = [&](int c) {
-    uint8_t* base = rsm + (c & 1) * stage_bytes;
+    uint8_t* base = rsm + (c % kStages) * stage_bytes;
     const int k0 = c * kc;
-    const int xv = kc / 8;  // 16 B vectors per token row
+    const int xv = kc / 8;
     for (int v = tid; v < rt::kTokens * xv; v += blockDim.x) {
       const int tt = v / xv, c8 = (v - tt * xv) * 8;
       const bool ok = t0 + tt < T;
       const __nv_bfloat16* src = ok ? x + size_t(t0 + tt) * d + k0 + c8 : x;
-      cp_async_16(base + (tt * kc + c8) * 2, src, ok ? 16u : 0u);
+      cp_async_16(base + (tt * pitch + c8) * 2, src, ok ? 16u : 0u);
     }
-    const float4* wsrc = wp + size_t(k0 >> 2) * E_tot;
-    float4* wdst = reinterpret_cast<float4*>(base + x_bytes);
-    for (int v = tid; v < (kc >> 2) * E_tot; v += blockDim.x) cp_async_16(wdst + v, wsrc + v, 16u);
-    cp_async_commit();
+    const uint4* wsrc = wp + size_t(k0) * E_pad / 4;
+    uint4* wdst = reinterpret_cast<uint4*>(base + x_bytes);
+    for (int v = tid; v < kc * E_pad / 4; v += blockDim.x) cp_async_16(wdst + v, wsrc + v, 16u);
   };
 
-  issue(0);
-  for (int c = 0; c < n_chunks; ++c) {
-    if (c + 1 < n_chunks) {
-      issue(c + 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const uint8_t* base = rsm + (c & 1) * stage_bytes;
-    const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(base);
-    const float4* ws = reinterpret_cast<const float4*>(base + x_bytes);
+  // prologue: kStages-1 chunks in flight (one commit group per chunk, empty groups past the end)
 #pragma unroll
-    for (int m = 0; m < kItems; ++m) {
-      if (tid + m * rt::kThreads < n_items) {
-        const uint4* xrow = reinterpret_cast<const uint4*>(xs + it_t[m] * kc);
-        const float4* wcol = ws + it_e[m];
-        float a = acc[m];
-#pragma unroll 4
-        for (int kk = 0; kk < kc; kk += 8) {
-          const uint4 xv = xrow[kk >> 3];
-          const float4 w0 = wcol[(kk >> 2) * E_tot];
-          const float4 w1 = wcol[((kk >> 2) + 1) * E_tot];
-          // strictly ascending k: one fp32 FMA chain per logit
-          a = fmaf(bf16_lo(xv.x), w0.x, a);
-          a = fmaf(bf16_hi(xv.x), w0.y, a);
-          a = fmaf(bf16_lo(xv.y), w0.z, a);
-          a = fmaf(bf16_hi(xv.y), w0.w, a);
-          a = fmaf(bf16_lo(xv.z), w1.x, a);
-          a = fmaf(bf16_hi(xv.z), w1.y, a);
-          a = fmaf(bf16_lo(xv.w), w1.z, a);
-          a = fmaf(bf16_hi(xv.w), w1.w, a);
+  for (int c = 0; c < kStages - 1; ++c) {
+    if (c < n_chunks) issue(c);
+    cp_async_commit();
+  }
+  for (int c = 0; c < n_chunks; ++c) {
+    if (c + kStages - 1 < n_chunks) issue(c + kStages - 1);
+    cp_async_commit();
+    cp_async_wait<kStages - 1>();
+    __syncthreads();
+    const uint8_t* base = rsm + (c % kStages) * stage_bytes;
+    const uint4* xrow = reinterpret_cast<const uint4*>(base + size_t(lane) * pitch * 2);
+    const float* ws = reinterpret_cast<const float*>(base + x_bytes) + e0;
+#pragma unroll 2
+    for (int kk = 0; kk < kc; kk += 8) {
+      const uint4 xv = xrow[kk >> 3];
+      const float xs[8] = {bf16_lo(xv.x), bf16_hi(xv.x), bf16_lo(xv.y), bf16_hi(xv.y),
+                           bf16_lo(xv.z), bf16_hi(xv.z), bf16_lo(xv.w), bf16_hi(xv.w)};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {   // strictly ascending k
+        const float* wr = ws + size_t(kk + q) * E_pad;
+        if constexpr (TE == 2) {
+          const float2 w = *reinterpret_cast<const float2*>(wr);
+          ffma2(acc[0], xs[q], pack2(w.x, w.y));
+        } else {
+#pragma unroll
+          for (int j = 0; j < TE / 4; ++j) {
+            const float4 w = reinterpret_cast<const float4*>(wr)[j];
+            ffma2(acc[2 * j], xs[q], pack2(w.x, w.y));
+            ffma2(acc[2 * j + 1], xs[q], pack2(w.z, w.w));
+          }
         }
-        acc[m] = a;
       }
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int m = 0; m < kItems; ++m) {
-    if (tid + m * rt::kThreads < n_items) {
-      float v = acc[m];
-      if (bias != nullptr && it_e[m] < E) v = __fadd_rn(v, bias[it_e[m]]);
-      logits[it_t[m]][it_e[m]] = v;
+  for (int j = 0; j < TE; ++j) {
+    const int e = e0 + j;
+    if (e < E_tot) {
+      float v = __uint_as_float(uint32_t(acc[j >> 1] >> ((j & 1) * 32)));
+      if (bias != nullptr && e < E) v = __fadd_rn(v, bias[e]);
+      logits[lane][e] = v;
     }
   }
   __syncthreads();
 
-  // ---- top-k + weights: one warp per token (4 warps x 4 rounds)
-  const int warp = warp_id(), lane = lane_id();
-  for (int tt = warp; tt < rt::kTokens; tt += rt::kThreads / 32) {
+  // ---- top-k + weights: one warp per token
+  for (int tt = warp; tt < rt::kTokens; tt += blockDim.x / 32) {
     const int t = t0 + tt;
     if (t >= T) break;
     float v0 = lane < E ? logits[tt][lane] : -INFINITY;
@@ -237,36 +250,34 @@ int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* b
   if (score_mode != 0 && score_mode != 1) return set_error(MP_E_ARG, "router: score_mode %d", score_mode);
   if (T <= 0) return MP_OK;
   const int E_tot = E + (has_gate ? 1 : 0);
-  const int items = (rt::kTokens * E_tot + rt::kThreads - 1) / rt::kThreads;
-  const int grid = (T + rt::kTokens - 1) / rt::kTokens;
-  const float4* wp = reinterpret_cast<const float4*>(wg_packed);
-  int kc = E_tot <= 16 ? 256 : 128;
-  while (d % kc) kc >>= 1;
-  if (kc < 8) return set_error(MP_E_SHAPE, "router: d=%d not a multiple of 8", d);
-  const size_t smem = size_t(2) * (rt::kTokens * kc * 2 + E_tot * kc * 4);
-#define MP_ROUTER_CASE(N)                                                                                       \
-  case N:                                                                                                      \
-    if (smem > 48 * 1024)                                                                                      \
-      cudaFuncSetAttribute(router_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));          \
-    router_kernel<N><<<grid, rt::kThreads, smem, stream>>>(x, wp, bias, T, d, E, has_gate ? 1 : 0, k, score_mode, \
-                                                           renorm, kc, idx, w, shared_gate, hist, blk_counts,    \
-                                                           batch_counts);                                        \
-    break;
-  switch (items) {
-    MP_ROUTER_CASE(1)
-    MP_ROUTER_CASE(2)
-    MP_ROUTER_CASE(3)
-    MP_ROUTER_CASE(4)
-    MP_ROUTER_CASE(5)
-    MP_ROUTER_CASE(6)
-    MP_ROUTER_CASE(7)
-    MP_ROUTER_CASE(8)
-    MP_ROUTER_CASE(9)
-    default:
-      return set_error(MP_E_SHAPE, "router: %d items per thread unsupported", items);
+  const int E_pad = router_e_pad(E_tot);
+  int TE = E_pad <= 16 ? 2 : 8;
+  if (const char* env = getenv("MP_ROUTER_TE")) {  // tuning override (2, 4 or 8)
+    const int v = atoi(env);
+    if ((v == 2 || v == 4 || v == 8) && E_pad % v == 0 && E_pad / v <= 8) TE = v;
   }
-#undef MP_ROUTER_CASE
-  cudaError_t e = cudaGetLastError();
+  const int warps = E_pad / TE;
+  const int grid = (T + rt::kTokens - 1) / rt::kTokens;
+  const uint4* wp = reinterpret_cast<const uint4*>(wg_packed);
+  int kc = E_pad <= 16 ? 256 : 128;
+  while (d % kc) kc >>= 1;
+  const size_t smem = size_t(kStages) * (rt::kTokens * (kc + 8) * 2 + size_t(kc) * E_pad * 4);
+  cudaError_t e;
+#define MP_ROUTER_LAUNCH(N)                                                                                    \
+  e = cudaFuncSetAttribute(router_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));        \
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router)");                            \
+  router_kernel<N><<<grid, 32 * warps, smem, stream>>>(x, wp, bias, T, d, E, has_gate ? 1 : 0, k, score_mode, \
+                                                       renorm, kc, idx, w, shared_gate, hist, blk_counts,     \
+                                                       batch_counts)
+  if (TE == 2) {
+    MP_ROUTER_LAUNCH(2);
+  } else if (TE == 4) {
+    MP_ROUTER_LAUNCH(4);
+  } else {
+    MP_ROUTER_LAUNCH(8);
+  }
+#undef MP_ROUTER_LAUNCH
+  e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_kernel launch");
 }
 

@@ -252,9 +252,9 @@ class B200MoELayer:
         if self.world == 1:
             return h[None].cpu().numpy().astype(np.int64)
         import torch.distributed as dist
-        parts = [torch.zeros_like(h) for _ in range(self.world)]
-        dist.all_gather(parts, h, group=group) if dist.get_backend(group) == "nccl" else \
-            dist.all_gather(parts, h.cpu(), group=group)
+        src = h if dist.get_backend(group) == "nccl" else h.cpu()
+        parts = [torch.zeros_like(src) for _ in range(self.world)]
+        dist.all_gather(parts, src, group=group)
         return torch.stack([p.cpu() for p in parts]).numpy().astype(np.int64)
 
     def activation_stats(self, group=None):
