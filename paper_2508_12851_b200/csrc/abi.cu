@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -81,6 +82,9 @@ struct mp_layer {
   bool peers_open = false, routes_set = false, router_ready = false;
 
   CUtensorMap tm_recv, tm_w13, tm_h, tm_w2, tm_w13s, tm_hs, tm_w2s, tm_x;
+  // B maps with 128-row boxes for the CTA-pair GEMM (each CTA loads half of N)
+  CUtensorMap tm_w13_p, tm_w2_p, tm_w13s_p, tm_w2s_p;
+  int pair_routed = 0, pair_shared = 1;
   const void* tm_x_ptr = nullptr;
   int tm_x_rows = -1;
 
@@ -154,10 +158,12 @@ int mp_grouped_gemm(const void* a, int64_t a_rows, const void* b, int64_t b_rows
                     const int32_t* n_groups, int N, int K, void* out, int out_ld, int swiglu, void* stream) {
   if (!a || !b || !groups || !n_groups || !out) return set_error(MP_E_ARG, "mp_grouped_gemm: null pointer");
   CUtensorMap ta, tb;
+  int pair = 0;
+  if (const char* env = getenv("MP_GEMM_PAIR")) pair = atoi(env);
   MP_TRY(encode_tmap_bf16_2d(&ta, a, uint64_t(a_rows), uint64_t(K), 128));
-  MP_TRY(encode_tmap_bf16_2d(&tb, b, uint64_t(b_rows), uint64_t(K), 256));
+  MP_TRY(encode_tmap_bf16_2d(&tb, b, uint64_t(b_rows), uint64_t(K), pair ? 128 : 256));
   return launch_grouped_gemm(ta, tb, groups, n_groups, N, K, N, 0, static_cast<__nv_bfloat16*>(out), out_ld,
-                             swiglu, 0, static_cast<cudaStream_t>(stream));
+                             swiglu, 0, static_cast<cudaStream_t>(stream), pair);
 }
 
 int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
@@ -290,13 +296,24 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       return fail(r);
     if ((r = encode_tmap_bf16_2d(&L->tm_w2, L->pool, uint64_t(D.n_slots) * 3 * D.d, uint64_t(D.f), 256)) != MP_OK)
       return fail(r);
+    if ((r = encode_tmap_bf16_2d(&L->tm_w13_p, L->pool, uint64_t(D.n_slots) * 3 * D.f, uint64_t(D.d), 128)) != MP_OK)
+      return fail(r);
+    if ((r = encode_tmap_bf16_2d(&L->tm_w2_p, L->pool, uint64_t(D.n_slots) * 3 * D.d, uint64_t(D.f), 128)) != MP_OK)
+      return fail(r);
   }
+  // CTA pairs (256-row tiles) when the average expert group is large
+  L->pair_routed = int64_t(D.world) * D.max_tokens * D.top_k >= int64_t(512) * D.E ? 1 : 0;
+  if (const char* env = getenv("MP_GEMM_PAIR")) L->pair_routed = L->pair_shared = atoi(env) ? 1 : 0;
   if (D.shared_f > 0) {
     if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
       return fail(r);
     if ((r = encode_tmap_bf16_2d(&L->tm_w2s, L->w2s, uint64_t(D.d), uint64_t(D.shared_f), 256)) != MP_OK)
       return fail(r);
     if ((r = encode_tmap_bf16_2d(&L->tm_hs, L->hs, uint64_t(D.max_tokens), uint64_t(D.shared_f), 128)) != MP_OK)
+      return fail(r);
+    if ((r = encode_tmap_bf16_2d(&L->tm_w13s_p, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 128)) != MP_OK)
+      return fail(r);
+    if ((r = encode_tmap_bf16_2d(&L->tm_w2s_p, L->w2s, uint64_t(D.d), uint64_t(D.shared_f), 128)) != MP_OK)
       return fail(r);
   }
   if (L->G == 1) L->peers_open = true;
@@ -486,10 +503,11 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     MP_CUDA(cudaMemcpyAsync(L->sh_groups, hg, sizeof(hg), cudaMemcpyHostToDevice, st));
     const int32_t one = 1;
     MP_CUDA(cudaMemcpyAsync(L->sh_ngroups, &one, 4, cudaMemcpyHostToDevice, st));
-    MP_TRY(launch_grouped_gemm(L->tm_x, L->tm_w13s, L->sh_groups, L->sh_ngroups, 2 * D.shared_f, D.d, 0, 0, L->hs,
-                               D.shared_f, 1, 0, st));
-    MP_TRY(launch_grouped_gemm(L->tm_hs, L->tm_w2s, L->sh_groups, L->sh_ngroups, D.d, D.shared_f, 0, 0, L->ys, D.d,
-                               0, 0, st));
+    const int ps = L->pair_shared;
+    MP_TRY(launch_grouped_gemm(L->tm_x, ps ? L->tm_w13s_p : L->tm_w13s, L->sh_groups, L->sh_ngroups, 2 * D.shared_f,
+                               D.d, 0, 0, L->hs, D.shared_f, 1, 0, st, ps));
+    MP_TRY(launch_grouped_gemm(L->tm_hs, ps ? L->tm_w2s_p : L->tm_w2s, L->sh_groups, L->sh_ngroups, D.d, D.shared_f,
+                               0, 0, L->ys, D.d, 0, 0, st, ps));
     launches += 2;
   }
   MP_TRY(mark());  // 5 shared expert
@@ -499,11 +517,12 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   }
   MP_TRY(mark());  // 6 dispatch barrier
   if (D.n_slots > 0) {
-    MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, L->groups, L->n_groups, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f,
-                               1, 0, st));
+    const int pr = L->pair_routed;
+    MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, L->groups, L->n_groups, 2 * D.f, D.d,
+                               3 * D.f, 0, L->h, D.f, 1, 0, st, pr));
     MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
-    MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, L->groups, L->n_groups, D.d, D.f, 3 * D.d, 2 * D.d, L->y, D.d, 0,
-                               0, st));
+    MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, L->groups, L->n_groups, D.d, D.f, 3 * D.d,
+                               2 * D.d, L->y, D.d, 0, 0, st, pr));
     launches += 2;
   } else {
     MP_TRY(mark());

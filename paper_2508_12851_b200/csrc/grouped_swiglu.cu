@@ -19,6 +19,8 @@
 //               a double-buffered TMEM accumulator (2 x 256 fp32 columns)
 //   warp 2      TMEM allocator (512 columns)
 //   warps 4..7  epilogue: tcgen05.ld -> (SwiGLU) -> bf16 -> global
+#include <cstdlib>
+
 #include "common.cuh"
 #include "mp_internal.h"
 
@@ -67,6 +69,56 @@ MP_DEV TileCoord decode_tile(const GemmSmemTail& s, int tile, int n_blocks) {
   c.n_blk = local / m_blocks;
   c.m_blk = local - c.n_blk * m_blocks;
   return c;
+}
+
+// Epilogue of one 128-row x 256-column accumulator: this thread owns one row
+// (TMEM lane), reads 32 columns per tcgen05.ld, applies SwiGLU (GEMM1: columns
+// [0,128) gate, [128,256) up) and writes bf16.
+MP_DEV void epilogue_store(uint32_t taddr, bool valid, __nv_bfloat16* __restrict__ out, size_t orow, int out_ld,
+                           int n_blk, int swiglu) {
+  if (swiglu) {
+    __nv_bfloat16* dst = out + orow * size_t(out_ld) + size_t(n_blk) * (gg::BN / 2);
+#pragma unroll 1
+    for (int cc = 0; cc < gg::BN / 2; cc += 32) {
+      uint32_t gv[32], uv[32];
+      tmem_ld_32x32b_x32(taddr + cc, gv);
+      tmem_ld_32x32b_x32(taddr + gg::BN / 2 + cc, uv);
+      tmem_ld_wait();
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float g0 = __uint_as_float(gv[2 * i]), g1 = __uint_as_float(gv[2 * i + 1]);
+        float u0 = __uint_as_float(uv[2 * i]), u1 = __uint_as_float(uv[2 * i + 1]);
+        float h0 = g0 / (1.0f + __expf(-g0)) * u0;
+        float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+        packed[i] = pack_bf16x2(h0, h1);
+      }
+      if (valid) {
+        uint4* p = reinterpret_cast<uint4*>(dst + cc);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          p[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+      }
+    }
+  } else {
+    __nv_bfloat16* dst = out + orow * size_t(out_ld) + size_t(n_blk) * gg::BN;
+#pragma unroll 1
+    for (int cc = 0; cc < gg::BN; cc += 32) {
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(taddr + cc, v);
+      tmem_ld_wait();
+      uint32_t packed[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+      if (valid) {
+        uint4* p = reinterpret_cast<uint4*>(dst + cc);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          p[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
+      }
+    }
+  }
 }
 
 __global__ void __launch_bounds__(gg::kThreads, 1)
@@ -197,49 +249,7 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
       mbar_wait(&st.tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * gg::BN);
-      if (swiglu) {
-        __nv_bfloat16* dst = out + orow * size_t(out_ld) + size_t(c.n_blk) * (gg::BN / 2);
-#pragma unroll 1
-        for (int cc = 0; cc < gg::BN / 2; cc += 32) {
-          uint32_t gv[32], uv[32];
-          tmem_ld_32x32b_x32(taddr + cc, gv);
-          tmem_ld_32x32b_x32(taddr + gg::BN / 2 + cc, uv);
-          tmem_ld_wait();
-          uint32_t packed[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float g0 = __uint_as_float(gv[2 * i]), g1 = __uint_as_float(gv[2 * i + 1]);
-            float u0 = __uint_as_float(uv[2 * i]), u1 = __uint_as_float(uv[2 * i + 1]);
-            float h0 = g0 / (1.0f + __expf(-g0)) * u0;
-            float h1 = g1 / (1.0f + __expf(-g1)) * u1;
-            packed[i] = pack_bf16x2(h0, h1);
-          }
-          if (valid) {
-            uint4* p = reinterpret_cast<uint4*>(dst + cc);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              p[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-          }
-        }
-      } else {
-        __nv_bfloat16* dst = out + orow * size_t(out_ld) + size_t(c.n_blk) * gg::BN;
-#pragma unroll 1
-        for (int cc = 0; cc < gg::BN; cc += 32) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(taddr + cc, v);
-          tmem_ld_wait();
-          uint32_t packed[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i)
-            packed[i] = pack_bf16x2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-          if (valid) {
-            uint4* p = reinterpret_cast<uint4*>(dst + cc);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              p[i] = make_uint4(packed[4 * i], packed[4 * i + 1], packed[4 * i + 2], packed[4 * i + 3]);
-          }
-        }
-      }
+      epilogue_store(taddr, valid, out, orow, out_ld, c.n_blk, swiglu);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&st.tempty[acc]);
@@ -253,6 +263,201 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<gg::kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ CTA-pair variant
+// Same tile math with tcgen05.mma.cta_group::2: a cluster of two CTAs on one
+// TPC computes a 256 x 256 tile.  CTA r loads A rows [128r, 128r+128) and B
+// rows (N) [128r, 128r+128) of the tile; the leader (r = 0) issues M=256 N=256
+// MMAs that read both CTAs' smem and write each CTA's 128 rows into its own
+// TMEM.  Per CTA and k-block only 32 KB cross L2 -> smem instead of 48 KB.
+//   * full[s]   (leader)  : leader's expect_tx(64 KB) + both CTAs' 2-SM TMA bytes
+//   * empty[s]  (both)    : multicast tcgen05.commit from the leader's MMA thread
+//   * tfull[a]  (both)    : multicast commit after the tile's last k-block
+//   * tempty[a] (leader)  : 8 arrivals = 4 epilogue warps x 2 CTAs (remote arrive)
+namespace g2 {
+constexpr int BM = 256;  // rows per pair tile (128 per CTA)
+constexpr int BN = 256;
+constexpr int BK = 64;
+constexpr int kStages = 6;
+constexpr int kABytes = 128 * BK * 2;  // 16 KB per CTA
+constexpr int kBBytes = 128 * BK * 2;  // 16 KB per CTA (its half of N)
+constexpr int kStageBytes = kABytes + kBBytes;
+constexpr size_t kSmemBytes = 1024 + size_t(kStages) * kStageBytes + 4096;
+}  // namespace g2
+
+struct Gemm2SmemTail {
+  uint64_t full[g2::kStages];
+  uint64_t empty[g2::kStages];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  int n_groups;
+  int total_tiles;
+  int tile_prefix[gg::kMaxGroups + 1];
+  int g_arow[gg::kMaxGroups];
+  int g_m[gg::kMaxGroups];
+  int g_slot[gg::kMaxGroups];
+  int g_orow[gg::kMaxGroups];
+};
+
+MP_DEV TileCoord decode_tile2(const Gemm2SmemTail& s, int tile, int n_blocks) {
+  int g = 0;
+  while (s.tile_prefix[g + 1] <= tile) ++g;
+  const int local = tile - s.tile_prefix[g];
+  const int m_pairs = (s.g_m[g] + g2::BM - 1) / g2::BM;
+  TileCoord c;
+  c.g = g;
+  c.n_blk = local / m_pairs;
+  c.m_blk = local - c.n_blk * m_pairs;
+  return c;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
+    grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                            const int32_t* __restrict__ groups, const int32_t* __restrict__ n_groups_dev, int N,
+                            int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out, int out_ld,
+                            int swiglu) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = smem;
+  uint8_t* smB = smem + g2::kStages * g2::kABytes;
+  Gemm2SmemTail& st = *reinterpret_cast<Gemm2SmemTail*>(smem + g2::kStages * g2::kStageBytes);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
+  const int n_blocks = N / g2::BN;
+  const int k_blocks = K / g2::BK;
+
+  if (threadIdx.x == 0) {
+    int ng = *n_groups_dev;
+    if (ng > gg::kMaxGroups) ng = gg::kMaxGroups;
+    st.n_groups = ng;
+  }
+  __syncthreads();
+  const int ng = st.n_groups;
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+    st.g_arow[g] = groups[4 * g + 0];
+    st.g_m[g] = groups[4 * g + 1];
+    st.g_slot[g] = groups[4 * g + 2];
+    st.g_orow[g] = groups[4 * g + 3];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    st.tile_prefix[0] = 0;
+    for (int g = 0; g < ng; ++g) {
+      acc += ((st.g_m[g] + g2::BM - 1) / g2::BM) * n_blocks;
+      st.tile_prefix[g + 1] = acc;
+    }
+    st.total_tiles = acc;
+    for (int i = 0; i < g2::kStages; ++i) {
+      mbar_init(&st.full[i], 1);
+      mbar_init(&st.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&st.tfull[i], 1);
+      mbar_init(&st.tempty[i], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 2) tmem_alloc_2sm<gg::kTmemCols>(&st.tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's barriers are initialised before any remote arrive / TMA
+  tc_fence_after();
+  const uint32_t tmem_base = st.tmem_base;
+  const int total = st.total_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer (both CTAs load their halves)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster_id; tile < total; tile += n_clusters) {
+        const TileCoord c = decode_tile2(st, tile, n_blocks);
+        const int a_row = st.g_arow[c.g] + c.m_blk * g2::BM + int(rank) * 128;
+        const int b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * g2::BN + int(rank) * 128;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&st.empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&st.full[stage], 2 * g2::kStageBytes);
+          tma_load_2d_2sm(smA + stage * g2::kABytes, &tmA, &st.full[stage], kb * g2::BK, a_row);
+          tma_load_2d_2sm(smB + stage * g2::kBBytes, &tmB, &st.full[stage], kb * g2::BK, b_row);
+          if (++stage == g2::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ================= MMA issuer (leader CTA only)
+      constexpr uint32_t idesc = make_idesc_bf16(g2::BM, g2::BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cluster_id; tile < total; tile += n_clusters) {
+        mbar_wait(&st.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * g2::BN);
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&st.full[stage], phase);
+          tc_fence_after();
+          const uint64_t adesc = make_sdesc_sw128(smem_u32(smA + stage * g2::kABytes));
+          const uint64_t bdesc = make_sdesc_sw128(smem_u32(smB + stage * g2::kBBytes));
+#pragma unroll
+          for (int k = 0; k < g2::BK / 16; ++k)
+            umma_bf16_2sm(d_tmem, adesc + uint64_t(2 * k), bdesc + uint64_t(2 * k), idesc, (kb | k) != 0 ? 1u : 0u);
+          umma_commit_2sm_mc(&st.empty[stage], 0x3);
+          if (++stage == g2::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2sm_mc(&st.tfull[acc], 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue (both CTAs: own 128 rows of the pair tile)
+    const int q = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cluster_id; tile < total; tile += n_clusters) {
+      const TileCoord c = decode_tile2(st, tile, n_blocks);
+      const int row = c.m_blk * g2::BM + int(rank) * 128 + q * 32 + lane;
+      const bool valid = row < st.g_m[c.g];
+      const size_t orow = size_t(st.g_orow[c.g] + row);
+      mbar_wait(&st.tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * g2::BN);
+      epilogue_store(taddr, valid, out, orow, out_ld, c.n_blk, swiglu);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&st.tempty[acc], 0);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs are done with TMEM and each other's barriers
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_2sm<gg::kTmemCols>(tmem_base);
   }
 }
 
@@ -285,9 +490,25 @@ int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
 
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const int32_t* groups,
                         const int32_t* n_groups_dev, int N, int K, int b_slot_stride, int b_offset,
-                        __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream) {
+                        __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream, int pair) {
   if (N % gg::BN != 0) return set_error(MP_E_SHAPE, "grouped GEMM N=%d not a multiple of %d", N, gg::BN);
   if (K % gg::BK != 0) return set_error(MP_E_SHAPE, "grouped GEMM K=%d not a multiple of %d", K, gg::BK);
+  if (pair) {  // the B map must have 128-row boxes (each CTA loads half of N)
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaError_t e = cudaFuncSetAttribute(grouped_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(g2::kSmemBytes));
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(grouped_gemm_2sm)");
+      attr2 = true;
+    }
+    if (grid <= 0) grid = kNumSMs;
+    grid &= ~1;
+    grouped_gemm_2sm_kernel<<<grid, gg::kThreads, g2::kSmemBytes, stream>>>(
+        tmA, tmB, groups, n_groups_dev, N, K, b_slot_stride, b_offset, out, out_ld, swiglu);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_2sm_kernel launch");
+    return MP_OK;
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -39,7 +39,8 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
 int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const int32_t* groups,
                         const int32_t* n_groups_dev, int N, int K, int b_slot_stride, int b_offset,
-                        __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream);
+                        __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream,
+                        int pair = 0);
 
 // ---- K5 combine (+ return through peer pointers)
 int launch_combine(__nv_bfloat16* const* y_ptrs /*[G] device array*/, const int32_t* pos_dst,

@@ -56,9 +56,12 @@ def _ref_gemm(a, b, ms, slots, N, swiglu):
     return torch.cat(outs)
 
 
+@pytest.mark.parametrize("pair", [0, 1], ids=["cta1", "cta_pair"])
 @pytest.mark.parametrize("swiglu", [0, 1])
-@pytest.mark.parametrize("ms,K,N", [([128], 64, 256), ([300, 5, 128, 0 + 1], 512, 512), ([1000, 37], 2048, 768)])
-def test_grouped_gemm_matches_torch(swiglu, ms, K, N):
+@pytest.mark.parametrize("ms,K,N", [([128], 64, 256), ([300, 5, 128, 0 + 1], 512, 512), ([1000, 37], 2048, 768),
+                                    ([257, 511, 256], 256, 512)])
+def test_grouped_gemm_matches_torch(swiglu, ms, K, N, pair, monkeypatch):
+    monkeypatch.setenv("MP_GEMM_PAIR", str(pair))
     L, lib = _lib()
     torch.manual_seed(0)
     S = len(ms) + 1
@@ -85,8 +88,10 @@ def test_grouped_gemm_matches_torch(swiglu, ms, K, N):
     assert torch.isnan(out[rows:].float()).all()
 
 
-def test_grouped_gemm_large_k_many_tiles():
+@pytest.mark.parametrize("pair", [0, 1], ids=["cta1", "cta_pair"])
+def test_grouped_gemm_large_k_many_tiles(pair, monkeypatch):
     """More tiles than SMs (persistent loop + TMEM double buffer + smem ring wrap)."""
+    monkeypatch.setenv("MP_GEMM_PAIR", str(pair))
     L, lib = _lib()
     torch.manual_seed(1)
     ms, K, N = [2048, 1500, 900], 1024, 1024

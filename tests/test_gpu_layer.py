@@ -55,9 +55,11 @@ def _check_close(got, ref):
     assert rel <= RTOL_FRO, rel
 
 
+@pytest.mark.parametrize("pair", ["0", "1"], ids=["cta1", "cta_pair"])
 @pytest.mark.parametrize("name,T", [("toy", 256), ("toy", 77), ("qwen_small", 200), ("ds_small", 300),
                                     ("mixtral_narrow", 130)])
-def test_layer_g1_matches_oracle(name, T):
+def test_layer_g1_matches_oracle(name, T, pair, monkeypatch):
+    monkeypatch.setenv("MP_GEMM_PAIR", pair)
     shape = _shape(name)
     experts, shared, wg = _weights(shape)
     x = orc.synthetic_tokens(0, T, shape.d, seed=5)
