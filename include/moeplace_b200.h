@@ -122,8 +122,6 @@ typedef struct mp_layer_ptrs {
   void* y;           /* [recv_cap][d] bf16 expert outputs                        */
   uint32_t* hist;    /* [E] cumulative activation histogram (this origin)        */
   int32_t* counts;   /* [2][G][E] exchanged batch counts C[src][e] (parity halves) */
-  int32_t* groups;   /* [E][4] local GEMM groups                                 */
-  int32_t* n_groups; /* [1]                                                      */
   float* shared_gate;/* [max_tokens] or NULL                                     */
   int64_t recv_cap;  /* rows                                                     */
   int64_t slot_bytes;/* bytes of one expert slot (w13 + w2) = ModelSpec.expert_size */
@@ -157,8 +155,9 @@ int mp_layer_prepare_router(mp_layer* layer, void* stream);
 int mp_layer_forward(mp_layer* layer, const void* x, void* out, int T, void* stream);
 
 /* Same forward, recording MP_NUM_STAGE_EVENTS cudaEvent_t (created by the
- * caller with timing enabled) on `stream` at the stage boundaries:
- *   0 start | 1 router | 2 count exchange | 3 layout | 4 permute+dispatch |
+ * caller with timing enabled; NULL entries are skipped) on `stream` at the
+ * stage boundaries:
+ *   0 start | 1 router | 2 count exchange | 3 (unused) | 4 permute+dispatch |
  *   5 shared expert | 6 dispatch barrier | 7 GEMM1 SwiGLU | 8 GEMM2 |
  *   9 return barrier | 10 combine+return                                      */
 #define MP_NUM_STAGE_EVENTS 11

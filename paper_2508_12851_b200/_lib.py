@@ -27,8 +27,9 @@ MP_E_PEER = -6
 MP_SCORE_TOPK_SOFTMAX = 0
 MP_SCORE_SOFTMAX_TOPK = 1
 NUM_STAGE_EVENTS = 11
-STAGES = ("router", "count_exchange", "layout", "permute_dispatch", "shared_expert", "dispatch_barrier",
+STAGES = ("router", "count_exchange", "unused", "permute_dispatch", "shared_expert", "dispatch_barrier",
           "gemm1_swiglu", "gemm2", "return_barrier", "combine_return")
+GEMM_START, GEMM1_END, GEMM_END = 6, 7, 8
 
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
@@ -54,7 +55,7 @@ class LayerPtrs(Structure):
         ("w13_pool", c_void_p), ("w2_pool", c_void_p), ("wg", c_void_p), ("bias", c_void_p),
         ("w13_shared", c_void_p), ("w2_shared", c_void_p), ("idx", c_void_p), ("w", c_void_p),
         ("pos_dst", c_void_p), ("pos_row", c_void_p), ("recv", c_void_p), ("h", c_void_p), ("y", c_void_p),
-        ("hist", c_void_p), ("counts", c_void_p), ("groups", c_void_p), ("n_groups", c_void_p),
+        ("hist", c_void_p), ("counts", c_void_p),
         ("shared_gate", c_void_p), ("recv_cap", c_int64), ("slot_bytes", c_int64),
     ]
 

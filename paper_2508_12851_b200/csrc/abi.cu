@@ -70,11 +70,10 @@ struct mp_layer {
   // scratch views
   __nv_bfloat16 *h = nullptr, *wg = nullptr, *w13s = nullptr, *w2s = nullptr, *hs = nullptr, *ys = nullptr;
   float *wg_packed = nullptr, *bias = nullptr, *w = nullptr, *sgate = nullptr;
-  int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr, *blk_prefix = nullptr,
-          *batch_counts = nullptr, *my_base = nullptr, *groups = nullptr, *n_groups = nullptr,
-          *recv_rows = nullptr, *route_d = nullptr, *slot_of_d = nullptr, *sh_groups = nullptr,
-          *sh_ngroups = nullptr;
-  uint32_t *hist = nullptr, *err = nullptr;
+  int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr,
+          *batch_counts = nullptr, *route_d = nullptr,
+          *slot_of_d = nullptr;
+  uint32_t *hist = nullptr, *err = nullptr, *ticket = nullptr;
   void** ptr_arrays = nullptr;  // device: recv[8], y[8], flags[8], counts0[8], counts1[8]
 
   uint8_t* peer_window[8] = {};
@@ -151,7 +150,7 @@ int mp_router_topk_hist(const void* x, const void* packed, const float* bias, in
   if (!x || !packed || !idx || !w) return set_error(MP_E_ARG, "mp_router_topk_hist: null pointer");
   return launch_router(static_cast<const __nv_bfloat16*>(x), static_cast<const float*>(packed), bias, T, d,
                        E, has_gate, k, score_mode, renorm,
-                       idx, w, gate_out, hist, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+                       idx, w, gate_out, hist, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream));
 }
 
 int mp_grouped_gemm(const void* a, int64_t a_rows, const void* b, int64_t b_rows, const int32_t* groups,
@@ -162,8 +161,12 @@ int mp_grouped_gemm(const void* a, int64_t a_rows, const void* b, int64_t b_rows
   if (const char* env = getenv("MP_GEMM_PAIR")) pair = atoi(env);
   MP_TRY(encode_tmap_bf16_2d(&ta, a, uint64_t(a_rows), uint64_t(K), 128));
   MP_TRY(encode_tmap_bf16_2d(&tb, b, uint64_t(b_rows), uint64_t(K), pair ? 128 : 256));
-  return launch_grouped_gemm(ta, tb, groups, n_groups, N, K, N, 0, static_cast<__nv_bfloat16*>(out), out_ld,
-                             swiglu, 0, static_cast<cudaStream_t>(stream), pair);
+  GroupSpec gs;
+  gs.mode = 0;
+  gs.groups = groups;
+  gs.n_groups = n_groups;
+  return launch_grouped_gemm(ta, tb, gs, N, K, N, 0, static_cast<__nv_bfloat16*>(out), out_ld, swiglu, 0,
+                             static_cast<cudaStream_t>(stream), pair);
 }
 
 int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
@@ -240,18 +243,12 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       L->pos_dst = cv.take<int32_t>(size_t(T) * k);
       L->pos_row = cv.take<int32_t>(size_t(T) * k);
       L->blk_counts = cv.take<int32_t>(size_t(L->nb_max) * E);
-      L->blk_prefix = cv.take<int32_t>(size_t(L->nb_max) * E);
       L->batch_counts = cv.take<int32_t>(64);
-      L->my_base = cv.take<int32_t>(64);
-      L->groups = cv.take<int32_t>(64 * 4);
-      L->n_groups = cv.take<int32_t>(4);
-      L->recv_rows = cv.take<int32_t>(4);
       L->route_d = cv.take<int32_t>(8 * 64);
       L->slot_of_d = cv.take<int32_t>(64);
-      L->sh_groups = cv.take<int32_t>(4);
-      L->sh_ngroups = cv.take<int32_t>(4);
       L->hist = cv.take<uint32_t>(64);
       L->err = cv.take<uint32_t>(4);
+      L->ticket = cv.take<uint32_t>(4);
       L->ptr_arrays = cv.take<void*>(5 * 8);
       if (D.shared_f > 0) {
         L->w13s = cv.take<__nv_bfloat16>(size_t(2) * D.shared_f * D.d);
@@ -353,8 +350,6 @@ int mp_layer_get_ptrs(mp_layer* L, mp_layer_ptrs* o) {
   o->y = L->y;
   o->hist = L->hist;
   o->counts = L->counts;
-  o->groups = L->groups;
-  o->n_groups = L->n_groups;
   o->shared_gate = L->sgate;
   o->recv_cap = L->recv_cap;
   o->slot_bytes = int64_t(L->slot_bytes);
@@ -453,7 +448,6 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   if (!L->peers_open) return set_error(MP_E_PEER, "mp_layer_forward: peers not opened (G=%d)", L->G);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int G = L->G, E = D.E, k = D.top_k, rank = L->rank;
-  const int nb = (T + router_block_tokens() - 1) / router_block_tokens();
   const int par = int(L->fwd_count & 1);
   auto** recv_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 0 * 8);
   auto** y_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 1 * 8);
@@ -462,7 +456,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   int launches = 0;
   int ev_i = 0;
   auto mark = [&]() -> int {
-    if (events) {
+    if (events && events[ev_i]) {
       cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(events[ev_i]), st);
       if (e != cudaSuccess) return set_cuda_error(e, "cudaEventRecord(stage)");
     }
@@ -477,11 +471,11 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   }
 
   MP_TRY(mark());  // 0
-  MP_CUDA(cudaMemsetAsync(L->batch_counts, 0, size_t(E) * 4, st));
   MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
-                       D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts, st));
+                       D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
+                       L->ticket, st));
   ++launches;
-  MP_TRY(mark());  // 1 router
+  MP_TRY(mark());  // 1 router (+ per-batch counts)
   const int32_t* counts_all = L->batch_counts;
   if (G > 1) {
     MP_TRY(launch_publish_barrier(flag_ptrs, count_ptrs, L->batch_counts, E, G, rank, ++L->epoch, L->err, st));
@@ -489,25 +483,20 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     counts_all = L->counts + size_t(par) * G * E;
   }
   MP_TRY(mark());  // 2 count exchange
-  MP_TRY(launch_layout(counts_all, L->route_d, L->slot_of_d, L->blk_counts, nb, G, E, rank, L->my_base,
-                       L->blk_prefix, L->groups, L->n_groups, L->recv_rows, st));
-  ++launches;
-  MP_TRY(mark());  // 3 layout
-  MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d + rank * E, L->my_base,
-                        L->blk_prefix, T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st));
+  MP_TRY(mark());  // 3 (layout: folded into permute / GEMM prologues)
+  MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, L->blk_counts, rank, G,
+                        T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st));
   ++launches;
   MP_TRY(mark());  // 4 permute + dispatch
   if (D.shared_f > 0 && T > 0) {
-    const int32_t hg[4] = {0, T, 0, 0};
-    // group table of the dense shared expert: one group of all T local tokens
-    MP_CUDA(cudaMemcpyAsync(L->sh_groups, hg, sizeof(hg), cudaMemcpyHostToDevice, st));
-    const int32_t one = 1;
-    MP_CUDA(cudaMemcpyAsync(L->sh_ngroups, &one, 4, cudaMemcpyHostToDevice, st));
+    GroupSpec gsh;
+    gsh.mode = 2;
+    gsh.single_m = T;
     const int ps = L->pair_shared;
-    MP_TRY(launch_grouped_gemm(L->tm_x, ps ? L->tm_w13s_p : L->tm_w13s, L->sh_groups, L->sh_ngroups, 2 * D.shared_f,
-                               D.d, 0, 0, L->hs, D.shared_f, 1, 0, st, ps));
-    MP_TRY(launch_grouped_gemm(L->tm_hs, ps ? L->tm_w2s_p : L->tm_w2s, L->sh_groups, L->sh_ngroups, D.d, D.shared_f,
-                               0, 0, L->ys, D.d, 0, 0, st, ps));
+    MP_TRY(launch_grouped_gemm(L->tm_x, ps ? L->tm_w13s_p : L->tm_w13s, gsh, 2 * D.shared_f, D.d, 0, 0, L->hs,
+                               D.shared_f, 1, 0, st, ps));
+    MP_TRY(launch_grouped_gemm(L->tm_hs, ps ? L->tm_w2s_p : L->tm_w2s, gsh, D.d, D.shared_f, 0, 0, L->ys, D.d, 0, 0,
+                               st, ps));
     launches += 2;
   }
   MP_TRY(mark());  // 5 shared expert
@@ -517,12 +506,20 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   }
   MP_TRY(mark());  // 6 dispatch barrier
   if (D.n_slots > 0) {
+    GroupSpec gs;
+    gs.mode = 1;
+    gs.counts = counts_all;
+    gs.route = L->route_d;
+    gs.slot_of = L->slot_of_d;
+    gs.G = G;
+    gs.E = E;
+    gs.rank = rank;
     const int pr = L->pair_routed;
-    MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, L->groups, L->n_groups, 2 * D.f, D.d,
-                               3 * D.f, 0, L->h, D.f, 1, 0, st, pr));
+    MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
+                               0, st, pr));
     MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
-    MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, L->groups, L->n_groups, D.d, D.f, 3 * D.d,
-                               2 * D.d, L->y, D.d, 0, 0, st, pr));
+    MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->y, D.d, 0, 0,
+                               st, pr));
     launches += 2;
   } else {
     MP_TRY(mark());

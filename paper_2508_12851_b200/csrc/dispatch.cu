@@ -1,4 +1,4 @@
-// Layout, K2 permute+dispatch and K5 combine+return.
+// K2 permute+dispatch and K5 combine+return.
 //
 // Reference anchors:
 //   * target rule  `_choose_target` (reference pkg/src/moeplace/sim.py:433-439):
@@ -12,136 +12,74 @@
 // Receive-buffer layout on GPU D (identical formula on every rank, so no
 // per-row metadata crosses NVLink): rows grouped by expert id ascending; inside
 // an expert group, rows ordered by source GPU ascending, then by (token, slot)
-// of that source.  M[D][e] = sum_s [route[s][e]==D] * C[s][e].
+// of that source.  M[D][e] = sum_s [route[s][e]==D] * C[s][e].  The offsets are
+// recomputed where they are needed (permute CTAs, GEMM prologues) from the
+// exchanged count table -- there is no separate layout kernel.
 #include "common.cuh"
 #include "mp_internal.h"
 
 namespace mp {
 
-// ------------------------------------------------------------------ layout
-// One CTA.  Computes this rank's send offsets, the per-router-block prefix and
-// the local GEMM group table from the all-gathered counts.  Every global input
-// is first pulled into shared memory with coalesced loads (the block-count
-// matrix too), so no thread walks a chain of dependent global loads.
-__global__ void __launch_bounds__(1024)
-    layout_kernel(const int32_t* __restrict__ counts_all, const int32_t* __restrict__ route,
-                  const int32_t* __restrict__ slot_of, const int32_t* __restrict__ blk_counts, int nb, int G, int E,
-                  int rank, int32_t* __restrict__ my_base, int32_t* __restrict__ blk_prefix,
-                  int32_t* __restrict__ groups, int32_t* __restrict__ n_groups, int32_t* __restrict__ recv_rows) {
-  extern __shared__ int bc[];               // [nb][E] block counts
-  __shared__ int C[8][64], R[8][64];        // counts_all, route
-  __shared__ int M[8][64];                  // rows each GPU receives per expert
-  __shared__ int part[64][33];              // per-(expert, segment) partial sums
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int i = tid; i < G * E; i += nt) {
-    C[i / E][i % E] = counts_all[i];
-    R[i / E][i % E] = route[i];
-  }
-  for (int i = tid; i < nb * E; i += nt) bc[i] = blk_counts[i];
-  __syncthreads();
-  for (int i = tid; i < G * E; i += nt) {
-    const int D = i / E, e = i - D * E;
-    int m = 0;
-    for (int s = 0; s < G; ++s)
-      if (R[s][e] == D) m += C[s][e];
-    M[D][e] = m;
-  }
-  __syncthreads();
-  if (tid < E) {
-    const int e = tid;
-    const int D = R[rank][e];
-    int base = 0;
-    for (int e2 = 0; e2 < e; ++e2) base += M[D][e2];
-    for (int s = 0; s < rank; ++s)
-      if (R[s][e] == D) base += C[s][e];
-    my_base[e] = base;
-  }
-  if (tid == 32) {
-    int ng = 0, row = 0;
-    for (int e = 0; e < E; ++e) {
-      const int m = M[rank][e];
-      if (m > 0) {
-        groups[4 * ng + 0] = row;
-        groups[4 * ng + 1] = m;
-        groups[4 * ng + 2] = slot_of[e];
-        groups[4 * ng + 3] = row;
-        ++ng;
-      }
-      row += m;
-    }
-    *n_groups = ng;
-    *recv_rows = row;
-  }
-  // exclusive scan of the block counts over blocks, per expert: P threads per expert
-  int P = 1;
-  while (P * 2 * E <= nt && P * 2 <= 32) P *= 2;
-  const int e = tid / P, p = tid - (tid / P) * P;
-  const int seg = (nb + P - 1) / P;
-  const int b0 = min(nb, p * seg), b1 = min(nb, b0 + seg);
-  if (e < E) {
-    int sum = 0;
-    for (int b = b0; b < b1; ++b) sum += bc[b * E + e];
-    part[e][p] = sum;
-  }
-  __syncthreads();
-  if (e < E) {
-    int run = 0;
-    for (int q = 0; q < p; ++q) run += part[e][q];
-    for (int b = b0; b < b1; ++b) {
-      blk_prefix[size_t(b) * E + e] = run;
-      run += bc[b * E + e];
-    }
-  }
-}
-
-int launch_layout(const int32_t* counts_all, const int32_t* route, const int32_t* slot_of, const int32_t* blk_counts,
-                  int nb, int G, int E, int rank, int32_t* my_base, int32_t* blk_prefix, int32_t* groups,
-                  int32_t* n_groups, int32_t* recv_rows, cudaStream_t stream) {
-  if (G < 1 || G > 8) return set_error(MP_E_SHAPE, "layout: G=%d outside [1, 8]", G);
-  if (E < 1 || E > 64) return set_error(MP_E_SHAPE, "layout: E=%d outside [1, 64]", E);
-  const size_t smem = size_t(nb) * E * 4;
-  if (smem > 180 * 1024) return set_error(MP_E_SHAPE, "layout: %d router blocks x %d experts too large", nb, E);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(layout_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 180 * 1024);
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(layout)");
-    attr = true;
-  }
-  layout_kernel<<<1, 1024, smem, stream>>>(counts_all, route, slot_of, blk_counts, nb, G, E, rank, my_base,
-                                           blk_prefix, groups, n_groups, recv_rows);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? MP_OK : set_cuda_error(e, "layout_kernel launch");
-}
-
 // ------------------------------------------------------------------ K2 permute + dispatch
 // CTA = one router block of 32 tokens (the histogram blocks), 256 threads.
+// Prologue (the "layout", recomputed per CTA from tiny inputs, no extra launch):
+//   * my_base[e]: first row of this origin's expert-e rows in the target GPU's
+//     receive buffer = rows of lower experts on that GPU + rows of lower-ranked
+//     sources for e (from the exchanged counts C[G][E] and the route table);
+//   * prefix[e]: rows of expert e in this origin's earlier router blocks.
 // Phase 1: one thread per (token, slot) pair computes its stable in-block rank.
 // Phase 2: one warp per token loads the x row once (16 B per lane per step) and
 //          stores it to its k destinations, local or peer (NVLink) rows.
 template <int kVecPerLane>
 __global__ void __launch_bounds__(256)
     permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
-                   const int32_t* __restrict__ route_row, const int32_t* __restrict__ my_base,
-                   const int32_t* __restrict__ blk_prefix, int T, int d, int E, int k,
+                   const int32_t* __restrict__ route, const int32_t* __restrict__ counts_all,
+                   const int32_t* __restrict__ blk_counts, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* __restrict__ recv_ptrs, int32_t* __restrict__ pos_dst,
                    int32_t* __restrict__ pos_row) {
   constexpr int kTok = 32;
   __shared__ int s_e[kTok * 8];
   __shared__ int s_dst[kTok * 8];
   __shared__ int s_row[kTok * 8];
+  __shared__ int C[8][64], R[8][64];
+  __shared__ int base_s[64];
   const int b = blockIdx.x;
   const int t0 = b * kTok;
   const int nt = min(kTok, T - t0);
   const int np = nt * k;
   const int tid = threadIdx.x;
+  for (int i = tid; i < G * E; i += blockDim.x) {
+    C[i / E][i % E] = counts_all[i];
+    R[i / E][i % E] = route[i];
+  }
+  if (tid < E) base_s[tid] = 0;
   if (tid < np) s_e[tid] = idx[size_t(t0) * k + tid];
+  __syncthreads();
+  // rows of this origin's earlier blocks, per expert (integer sums: order-free)
+  const int per = (int(blockDim.x) / E) * E;
+  if (tid < per) {
+    const int e = tid % E;
+    int sum = 0;
+    for (int i = tid; i < b * E; i += per) sum += blk_counts[i];
+    if (sum) atomicAdd(&base_s[e], sum);
+  }
+  if (tid < E) {
+    const int e = tid, D = R[rank][e];
+    int base = 0;
+    for (int e2 = 0; e2 < e; ++e2)
+      for (int s = 0; s < G; ++s)
+        if (R[s][e2] == D) base += C[s][e2];
+    for (int s = 0; s < rank; ++s)
+      if (R[s][e] == D) base += C[s][e];
+    atomicAdd(&base_s[e], base);
+  }
   __syncthreads();
   if (tid < np) {
     const int e = s_e[tid];
-    int rank = 0;
-    for (int q = 0; q < tid; ++q) rank += (s_e[q] == e);
-    const int dst = route_row[e];
-    const int row = my_base[e] + blk_prefix[size_t(b) * E + e] + rank;
+    int r = 0;
+    for (int q = 0; q < tid; ++q) r += (s_e[q] == e);
+    const int dst = R[rank][e];
+    const int row = base_s[e] + r;
     s_dst[tid] = dst;
     s_row[tid] = row;
     pos_dst[size_t(t0) * k + tid] = dst;
@@ -169,16 +107,17 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route_row, const int32_t* my_base,
-                   const int32_t* blk_prefix, int T, int d, int E, int k, __nv_bfloat16* const* recv_ptrs,
-                   int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream) {
+int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
+                   const int32_t* blk_counts, int rank, int G, int T, int d, int E, int k,
+                   __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream) {
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "permute: d=%d not a multiple of 8", d);
   if (k > 8) return set_error(MP_E_SHAPE, "permute: top_k=%d > 8", k);
+  if (G < 1 || G > 8 || E < 1 || E > 64) return set_error(MP_E_SHAPE, "permute: G=%d E=%d", G, E);
   if (T <= 0) return MP_OK;
   const int grid = (T + 31) / 32;
   const int vpl = (d / 8 + 31) / 32;
-#define MP_PERM_LAUNCH(N)                                                                                  \
-  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route_row, my_base, blk_prefix, T, d, E, k, recv_ptrs, \
+#define MP_PERM_LAUNCH(N)                                                                                       \
+  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route, counts_all, blk_counts, rank, G, T, d, E, k, recv_ptrs, \
                                               pos_dst, pos_row)
   if (vpl <= 1) MP_PERM_LAUNCH(1);
   else if (vpl <= 2) MP_PERM_LAUNCH(2);

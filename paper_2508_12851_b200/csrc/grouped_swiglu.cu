@@ -53,11 +53,71 @@ struct GemmSmemTail {
   int g_m[gg::kMaxGroups];
   int g_slot[gg::kMaxGroups];
   int g_orow[gg::kMaxGroups];
+  int g_tmp[64];
 };
 
 struct TileCoord {
   int g, m_blk, n_blk;
 };
+
+// Prologue shared by both kernels: build the group table in shared memory
+// (explicit, derived from the exchanged counts, or a single dense group) and
+// the per-group tile prefix.  Called by every thread.
+template <class Tail>
+MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
+  const int tid = threadIdx.x;
+  if (gs.mode == 1) {
+    if (tid < gs.E) {
+      int m = 0;
+      for (int s = 0; s < gs.G; ++s)
+        if (gs.route[s * gs.E + tid] == gs.rank) m += gs.counts[s * gs.E + tid];
+      st.g_tmp[tid] = m;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int ng = 0, row = 0;
+      for (int e = 0; e < gs.E; ++e) {
+        const int m = st.g_tmp[e];
+        if (m > 0) {
+          st.g_arow[ng] = row;
+          st.g_m[ng] = m;
+          st.g_slot[ng] = gs.slot_of[e];
+          st.g_orow[ng] = row;
+          ++ng;
+        }
+        row += m;
+      }
+      st.n_groups = ng;
+    }
+  } else if (gs.mode == 2) {
+    if (tid == 0) {
+      st.g_arow[0] = 0;
+      st.g_m[0] = gs.single_m;
+      st.g_slot[0] = 0;
+      st.g_orow[0] = 0;
+      st.n_groups = gs.single_m > 0 ? 1 : 0;
+    }
+  } else {
+    if (tid == 0) st.n_groups = min(*gs.n_groups, gg::kMaxGroups);
+    __syncthreads();
+    for (int g = tid; g < st.n_groups; g += blockDim.x) {
+      st.g_arow[g] = gs.groups[4 * g + 0];
+      st.g_m[g] = gs.groups[4 * g + 1];
+      st.g_slot[g] = gs.groups[4 * g + 2];
+      st.g_orow[g] = gs.groups[4 * g + 3];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    st.tile_prefix[0] = 0;
+    for (int g = 0; g < st.n_groups; ++g) {
+      acc += ((st.g_m[g] + bm - 1) / bm) * n_blocks;
+      st.tile_prefix[g + 1] = acc;
+    }
+    st.total_tiles = acc;
+  }
+}
 
 MP_DEV TileCoord decode_tile(const GemmSmemTail& s, int tile, int n_blocks) {
   int g = 0;
@@ -123,8 +183,7 @@ MP_DEV void epilogue_store(uint32_t taddr, bool valid, __nv_bfloat16* __restrict
 
 __global__ void __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                        const int32_t* __restrict__ groups, const int32_t* __restrict__ n_groups_dev,
-                        int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out,
+                        const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out,
                         int out_ld, int swiglu) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -138,28 +197,8 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
   const int k_blocks = K / gg::BK;
 
   // ---- prologue: group table -> smem, barriers, TMEM
+  load_groups(st, gs, gg::BM, n_blocks);
   if (threadIdx.x == 0) {
-    int ng = *n_groups_dev;
-    if (ng > gg::kMaxGroups) ng = gg::kMaxGroups;
-    st.n_groups = ng;
-  }
-  __syncthreads();
-  const int ng = st.n_groups;
-  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
-    st.g_arow[g] = groups[4 * g + 0];
-    st.g_m[g] = groups[4 * g + 1];
-    st.g_slot[g] = groups[4 * g + 2];
-    st.g_orow[g] = groups[4 * g + 3];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    st.tile_prefix[0] = 0;
-    for (int g = 0; g < ng; ++g) {
-      acc += ((st.g_m[g] + gg::BM - 1) / gg::BM) * n_blocks;
-      st.tile_prefix[g + 1] = acc;
-    }
-    st.total_tiles = acc;
     for (int i = 0; i < gg::kStages; ++i) {
       mbar_init(&st.full[i], 1);
       mbar_init(&st.empty[i], 1);
@@ -300,6 +339,7 @@ struct Gemm2SmemTail {
   int g_m[gg::kMaxGroups];
   int g_slot[gg::kMaxGroups];
   int g_orow[gg::kMaxGroups];
+  int g_tmp[64];
 };
 
 MP_DEV TileCoord decode_tile2(const Gemm2SmemTail& s, int tile, int n_blocks) {
@@ -316,8 +356,7 @@ MP_DEV TileCoord decode_tile2(const Gemm2SmemTail& s, int tile, int n_blocks) {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                            const int32_t* __restrict__ groups, const int32_t* __restrict__ n_groups_dev, int N,
-                            int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out, int out_ld,
+                            const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out, int out_ld,
                             int swiglu) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -334,28 +373,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
   const int n_blocks = N / g2::BN;
   const int k_blocks = K / g2::BK;
 
+  load_groups(st, gs, g2::BM, n_blocks);
   if (threadIdx.x == 0) {
-    int ng = *n_groups_dev;
-    if (ng > gg::kMaxGroups) ng = gg::kMaxGroups;
-    st.n_groups = ng;
-  }
-  __syncthreads();
-  const int ng = st.n_groups;
-  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
-    st.g_arow[g] = groups[4 * g + 0];
-    st.g_m[g] = groups[4 * g + 1];
-    st.g_slot[g] = groups[4 * g + 2];
-    st.g_orow[g] = groups[4 * g + 3];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    st.tile_prefix[0] = 0;
-    for (int g = 0; g < ng; ++g) {
-      acc += ((st.g_m[g] + g2::BM - 1) / g2::BM) * n_blocks;
-      st.tile_prefix[g + 1] = acc;
-    }
-    st.total_tiles = acc;
     for (int i = 0; i < g2::kStages; ++i) {
       mbar_init(&st.full[i], 1);
       mbar_init(&st.empty[i], 1);
@@ -488,8 +507,8 @@ int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
   return MP_OK;
 }
 
-int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const int32_t* groups,
-                        const int32_t* n_groups_dev, int N, int K, int b_slot_stride, int b_offset,
+int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,
+                        int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream, int pair) {
   if (N % gg::BN != 0) return set_error(MP_E_SHAPE, "grouped GEMM N=%d not a multiple of %d", N, gg::BN);
   if (K % gg::BK != 0) return set_error(MP_E_SHAPE, "grouped GEMM K=%d not a multiple of %d", K, gg::BK);
@@ -504,7 +523,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const in
     if (grid <= 0) grid = kNumSMs;
     grid &= ~1;
     grouped_gemm_2sm_kernel<<<grid, gg::kThreads, g2::kSmemBytes, stream>>>(
-        tmA, tmB, groups, n_groups_dev, N, K, b_slot_stride, b_offset, out, out_ld, swiglu);
+        tmA, tmB, gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_2sm_kernel launch");
     return MP_OK;
@@ -517,8 +536,8 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const in
     attr_set = true;
   }
   if (grid <= 0) grid = kNumSMs;
-  grouped_gemm_kernel<<<grid, gg::kThreads, gg::kSmemBytes, stream>>>(tmA, tmB, groups, n_groups_dev, N, K,
-                                                                      b_slot_stride, b_offset, out, out_ld, swiglu);
+  grouped_gemm_kernel<<<grid, gg::kThreads, gg::kSmemBytes, stream>>>(tmA, tmB, gs, N, K, b_slot_stride, b_offset,
+                                                                      out, out_ld, swiglu);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_kernel launch");
   return MP_OK;

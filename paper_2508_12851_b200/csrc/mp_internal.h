@@ -18,27 +18,32 @@ int set_cuda_error(cudaError_t e, const char* what);
 // ---- K1 router
 int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
-                  uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, cudaStream_t stream);
+                  uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
+                  cudaStream_t stream);
 int router_block_tokens();
 __host__ __device__ int router_e_pad(int E_tot);
 int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, float* packed, cudaStream_t stream);
 
-// ---- layout (count exchange result -> offsets, group table)
-int launch_layout(const int32_t* counts_all /*[G][E]*/, const int32_t* route /*[G][E]*/,
-                  const int32_t* slot_of /*[E]*/, const int32_t* blk_counts /*[nb][E]*/, int nb, int G, int E,
-                  int rank, int32_t* my_base /*[E]*/, int32_t* blk_prefix /*[nb][E]*/, int32_t* groups /*[E][4]*/,
-                  int32_t* n_groups, int32_t* recv_rows, cudaStream_t stream);
-
 // ---- K2 permute (+ dispatch through peer pointers)
-int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route_row /*[E] for this origin*/,
-                   const int32_t* my_base, const int32_t* blk_prefix, int T, int d, int E, int k,
-                   __nv_bfloat16* const* recv_ptrs /*[G] device array*/, int32_t* pos_dst, int32_t* pos_row,
-                   cudaStream_t stream);
+int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
+                   const int32_t* blk_counts, int rank, int G, int T, int d, int E, int k,
+                   __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream);
 
 // ---- K3 grouped GEMM
+// Where the GEMM takes its expert groups from (read in the kernel prologue).
+struct GroupSpec {
+  const int32_t* groups = nullptr;    // mode 0: explicit table [n][4] = {a_row, m, slot, out_row}
+  const int32_t* n_groups = nullptr;  //         and its length (device)
+  const int32_t* counts = nullptr;    // mode 1: derived -- exchanged counts C[G][E],
+  const int32_t* route = nullptr;     //         route[G][E] and slot_of[E]: groups are the
+  const int32_t* slot_of = nullptr;   //         experts routed to `rank`, ascending, rows packed
+  int G = 1, E = 0, rank = 0;
+  int single_m = 0;                   // mode 2: one group {0, single_m, slot 0, 0}
+  int mode = 0;
+};
 int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
-int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const int32_t* groups,
-                        const int32_t* n_groups_dev, int N, int K, int b_slot_stride, int b_offset,
+int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,
+                        int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream,
                         int pair = 0);
 

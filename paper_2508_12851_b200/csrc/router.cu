@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(256)
     router_kernel(const __nv_bfloat16* __restrict__ x, const uint4* __restrict__ wp, const float* __restrict__ bias,
                   int T, int d, int E, int has_gate, int k, int score_mode, int renorm, int kc,
                   int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
-                  uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts) {
+                  uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
+                  uint32_t* __restrict__ ticket) {
   extern __shared__ __align__(16) uint8_t rsm[];
   __shared__ float logits[rt::kTokens][rt::kMaxE + 2];
   __shared__ int cnt_s[rt::kMaxE];
@@ -234,16 +235,39 @@ __global__ void __launch_bounds__(256)
   for (int e = tid; e < E; e += blockDim.x) {
     const int c = cnt_s[e];
     if (blk_counts) blk_counts[size_t(blockIdx.x) * E + e] = c;
-    if (c) {
-      if (hist) atomicAdd(&hist[e], uint32_t(c));
-      if (batch_counts) atomicAdd(&batch_counts[e], c);
-    }
+    if (c && hist) atomicAdd(&hist[e], uint32_t(c));
   }
+  if (batch_counts == nullptr || blk_counts == nullptr) return;
+  // The last CTA to finish reduces the per-block counts into this batch's
+  // per-expert counts (integer sums: order-independent), so they are ready when
+  // the kernel completes -- no memset, no second pass.
+  __shared__ int is_last;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  const int nb = gridDim.x;
+  for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
+  __syncthreads();
+  const int per = (int(blockDim.x) / E) * E;  // threads keep a fixed expert
+  if (tid < per) {
+    const int e = tid % E;
+    int sum = 0;
+    for (int i = tid; i < nb * E; i += per) sum += __ldcg(&blk_counts[i]);
+    atomicAdd(&cnt_s[e], sum);
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += blockDim.x) batch_counts[e] = cnt_s[e];
+  if (tid == 0) *ticket = 0u;  // ready for the next launch (stream-ordered)
 }
 
 int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
-                  uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, cudaStream_t stream) {
+                  uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
+                  cudaStream_t stream) {
+  if (batch_counts && !ticket) return set_error(MP_E_ARG, "router: batch counts need a ticket word");
   if (E < 1 || E > rt::kMaxE) return set_error(MP_E_SHAPE, "router: E=%d outside [1, %d]", E, rt::kMaxE);
   if (k < 1 || k > E || k > rt::kMaxK) return set_error(MP_E_SHAPE, "router: top_k=%d invalid for E=%d", k, E);
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "router: d=%d not a multiple of 8", d);
@@ -268,7 +292,7 @@ int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* b
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router)");                            \
   router_kernel<N><<<grid, 32 * warps, smem, stream>>>(x, wp, bias, T, d, E, has_gate ? 1 : 0, k, score_mode, \
                                                        renorm, kc, idx, w, shared_gate, hist, blk_counts,     \
-                                                       batch_counts)
+                                                       batch_counts, ticket)
   if (TE == 2) {
     MP_ROUTER_LAUNCH(2);
   } else if (TE == 4) {

@@ -213,8 +213,8 @@ class B200MoELayer:
     # ------------------------------------------------------------------ forward
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, events=None) -> torch.Tensor:
         """One MoE-layer forward of this GPU's tokens.  `events`: optional list of
-        _lib.NUM_STAGE_EVENTS torch.cuda.Event(enable_timing=True) recorded at the
-        stage boundaries (see include/moeplace_b200.h)."""
+        _lib.NUM_STAGE_EVENTS torch.cuda.Event(enable_timing=True) (None = skip) recorded
+        at the stage boundaries (see include/moeplace_b200.h)."""
         if x.dtype != torch.bfloat16 or x.device != self.device or not x.is_contiguous():
             raise ValueError("x must be a contiguous bf16 tensor on the layer's device")
         if x.dim() != 2 or x.shape[1] != self.shape.d:
@@ -226,9 +226,10 @@ class B200MoELayer:
         if events is None:
             rc = self.lib.mp_layer_forward(self._h, x.data_ptr(), out.data_ptr(), T, self._stream())
         else:
-            if any(ev.cuda_event == 0 for ev in events):
+            if any(ev is not None and ev.cuda_event == 0 for ev in events):
                 raise ValueError("stage events must be created (recorded once) before use")
-            arr = (c_void_p * _lib.NUM_STAGE_EVENTS)(*[c_void_p(ev.cuda_event) for ev in events])
+            arr = (c_void_p * _lib.NUM_STAGE_EVENTS)(*[c_void_p(ev.cuda_event if ev is not None else 0)
+                                                       for ev in events])
             rc = self.lib.mp_layer_forward_timed(self._h, x.data_ptr(), out.data_ptr(), T, self._stream(), arr)
         _lib.check(rc, "mp_layer_forward")
         return out
