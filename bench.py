@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--cpu-tokens", type=int, default=256, help="tokens per CPU-baseline sample")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--stages", action="store_true", help="print the per-stage table on stderr")
+    ap.add_argument("--scenario", default="steady", choices=["steady", "shift"],
+                    help="shift: BASELINE config 5, drifting routing + expert migration vs static placement")
     return ap.parse_args()
 
 
@@ -531,8 +533,195 @@ def main_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- workload-shift scenario
+def main_shift(args):
+    """BASELINE config 5: routing drifts (p -> roll(p, E/2), as the reference acceptance suite's
+    drift, tests/test_acceptance.py:67-68); the migration check mirrors `_migration_check`
+    (sim.py:465-481): window stats -> build_placement -> should_migrate (cost.py:217-248) with a
+    measured remote penalty and measured peer-copy bandwidth; an adopted plan executes as NVLink
+    peer copies on a side stream while traffic keeps the old placement, then routes swap
+    (migration_complete, sim.py:520-525).  Reports phase throughput and local ratio for the
+    static control and the migrated placement."""
+    import torch
+    import torch.distributed as dist
+    from paper_2508_12851_b200 import workload as wl
+    from paper_2508_12851_b200.errors import import_moeplace
+    from paper_2508_12851_b200.layer import B200MoELayer
+    from paper_2508_12851_b200.routing import dispatch_accounting, gpu_expert_sets
+    from paper_2508_12851_b200.shapes import cluster_spec, get_shape, model_spec, slot_caps
+
+    rank, local, world = dist_env()
+    if world < 2:
+        raise SystemExit("the shift scenario needs >= 2 GPUs (with one GPU nothing is remote)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    os.environ["NCCL_DEBUG"] = "WARN"
+    dist.init_process_group("nccl", device_id=dev)
+    mp = import_moeplace()
+    if mp is None:
+        raise SystemExit("the shift scenario needs the reference solver (moeplace)")
+    shape = get_shape(args.config)
+    T, G, seed, E = args.tokens, world, args.seed, shape.E
+    caps = slot_caps(shape, G)
+    cluster0 = cluster_spec(shape, G, caps)
+    model = model_spec(shape)
+    wg = wl.router_weights(E + shape.shared_gate, shape.d, dev, seed)
+    expert_src = lambda e: wl.expert_weights(e, shape.d, shape.f, dev, seed)
+    layer = B200MoELayer(shape, rank=rank, world=world, device=local, max_tokens=T, cap_slots=caps[rank])
+    layer.open_peers()
+    if shape.shared_f:
+        layer.set_shared(*wl.shared_weights(shape.d, shape.shared_f, dev, seed))
+    xs = [wl.tokens(T, shape.d, dev, seed, rank, batch=b) for b in range(N_ROTATE)]
+    out = torch.empty(T, shape.d, device=dev, dtype=torch.bfloat16)
+    stream = torch.cuda.current_stream()
+
+    def all_counts():
+        return layer.gathered_counts()
+
+    def set_phase(shift):
+        layer.set_router(wg[:E], wl.origin_bias(rank, E, seed, shift=shift), wg[E] if shape.shared_gate else None)
+
+    def run(steps):
+        """steps forwards; returns (tokens/s over all GPUs, max-over-ranks seconds)"""
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(steps):
+            layer.forward(xs[i % N_ROTATE], out)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        layer.check()
+        return G * T * steps / (ms.item() * 1e-3), ms.item() * 1e-3
+
+    def placement_from(counts):
+        stats = mp.ActivationStats.from_counts(np.asarray(counts, float)[:, None, :], (E,))
+        return mp.build_placement("ours", cluster0, model, stats, seed), stats
+
+    # ---- phase A: placement fit to phase-A traffic (warm-up histogram)
+    set_phase(0)
+    # warm-up counts with a provisional all-covering placement (uniform round robin)
+    prov = [[e for e in range(E) if e % G == r] for r in range(G)]
+    layer.set_placement_sets(prov, expert_src)
+    layer.reset_counts()
+    run(args.warmup)
+    pa, _ = placement_from(all_counts())
+    sets_a = gpu_expert_sets(pa, 0)
+    layer.set_placement_sets(sets_a, expert_src)
+    layer.reset_counts()
+    tps_a, _ = run(args.steps)
+    acc_a = dispatch_accounting(all_counts(), layer.route, shape.d)
+
+    # ---- phase B with the static placement (the control): drifted routing
+    set_phase(E // 2)
+    layer.reset_counts()
+    tps_b_static, win_s = run(args.steps)
+    counts_b = all_counts()
+    acc_b_static = dispatch_accounting(counts_b, layer.route, shape.d)
+
+    # ---- migration check (sim.py:465-481) with measured costs
+    # remote penalty per token-unit: wire time of one remote invocation (activations out, results
+    # back, comm_time's bandwidth term cost.py:148) at the measured peer bandwidth (probe copy below)
+    bw_probe = measure_peer_copy(layer, world, rank) if world > 1 else 770e9
+    penalty = 2.0 * shape.d * 2 / bw_probe
+    cluster = cluster_spec(shape, G, caps, link_bandwidth=bw_probe, load_bandwidth=bw_probe)
+    candidate, stats_b = placement_from(counts_b)
+    snapshot = mp.CostSnapshot(stats_b, penalty, 0.0, win_s)
+    decision, ledger = mp.should_migrate(pa, candidate, snapshot, cluster, model, "loads-only")
+    sets_b = gpu_expert_sets(candidate, 0)
+    mig = {"decision": ledger["decision"], "cost_current_seconds": ledger["cost_current_seconds"],
+           "cost_candidate_seconds": ledger["cost_candidate_seconds"],
+           "migration_seconds_model": ledger["migration_seconds"], "penalty_seconds_per_token": penalty,
+           "peer_copy_GBps": bw_probe / 1e9}
+    tps_b_mig, acc_b_mig = None, None
+    if decision:
+        slot_maps = [None] * world
+        if world > 1:
+            dist.all_gather_object(slot_maps, layer.slot_of.tolist())
+        else:
+            slot_maps = [layer.slot_of.tolist()]
+        side = torch.cuda.Stream(dev)
+        e0, done = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        side.wait_stream(stream)
+        e0.record(side)
+        adds = layer.migrate_async(sets_a, sets_b, slot_maps, side, done)
+        # traffic keeps flowing on the old placement while the weights move (a fixed number of
+        # forwards on every rank: the layer is SPMD across GPUs)
+        overlap_steps = 3
+        for i in range(overlap_steps):
+            layer.forward(xs[i % N_ROTATE], out)
+        done.synchronize()
+        torch.cuda.synchronize()
+        copy_ms = e0.elapsed_time(done)
+        if world > 1:
+            dist.barrier()
+        layer.finish_migration(sets_b, adds)
+        n_add = torch.tensor([len(adds)], device=dev)
+        t_copy = torch.tensor([copy_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(n_add)
+            dist.all_reduce(t_copy, op=dist.ReduceOp.MAX)
+        mig.update({"slots_copied": int(n_add.item()), "bytes_copied": int(n_add.item()) * shape.expert_bytes,
+                    "copy_ms_max_gpu": t_copy.item(), "forwards_during_copy_rank0": overlap_steps})
+        layer.reset_counts()
+        tps_b_mig, _ = run(args.steps)
+        acc_b_mig = dispatch_accounting(all_counts(), layer.route, shape.d)
+
+    if rank == 0:
+        keep = ("remote_invocations", "remote_bytes", "local_ratio")
+        line = {"scenario": "workload-shift (BASELINE config 5)", "metric": METRIC, "unit": UNIT, "n_gpus": G,
+                "config": {"model": shape.name, "tokens_per_gpu": T, "steps_per_phase": args.steps,
+                           "slot_caps": caps, "drift": f"p -> roll(p, {E // 2})"},
+                "phase_a": {"value": tps_a, **{k: acc_a[k] for k in keep}},
+                "phase_b_static": {"value": tps_b_static, **{k: acc_b_static[k] for k in keep}},
+                "migration": mig,
+                "phase_b_migrated": None if tps_b_mig is None else
+                {"value": tps_b_mig, **{k: acc_b_mig[k] for k in keep}}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    layer.close()
+
+
+def measure_peer_copy(layer, world, rank):
+    """NVLink pull bandwidth: copy one expert slot from the next GPU into a free staging slot."""
+    import torch
+    import torch.distributed as dist
+    peer = (rank + 1) % world
+    slot_maps = [None] * world
+    dist.all_gather_object(slot_maps, layer.slot_of.tolist())
+    src_slot = next(s for s in slot_maps[peer] if s >= 0)
+    dst_slot = layer._free[-1]
+    from paper_2508_12851_b200 import _lib
+    import ctypes
+    ops = (_lib.CopyOp * 1)(_lib.CopyOp(peer, int(src_slot), int(dst_slot)))
+    st = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(2):
+        _lib.check(layer.lib.mp_layer_migrate(layer._h, ops, 1, ctypes.c_void_p(st.cuda_stream), None))
+    a.record(st)
+    reps = 5
+    for _ in range(reps):
+        _lib.check(layer.lib.mp_layer_migrate(layer._h, ops, 1, ctypes.c_void_p(st.cuda_stream), None))
+    b.record(st)
+    torch.cuda.synchronize()
+    sec = a.elapsed_time(b) * 1e-3 / reps
+    bw = torch.tensor([layer.shape.expert_bytes / sec], dtype=torch.float64, device=layer.device)
+    dist.all_reduce(bw, op=dist.ReduceOp.MIN)
+    dist.barrier()
+    return float(bw.item())
+
+
 if __name__ == "__main__":
     a = parse()
+    if a.scenario == "shift" and a.impl != "reference":
+        main_shift(a)
+        raise SystemExit(0)
     if a.impl == "reference":
         # keep the whole --steps K run within minutes: clamp the sample size for the big shapes
         main_reference(a)

@@ -294,8 +294,9 @@ class B200MoELayer:
         for i, (src, e, dst) in enumerate(ops):
             arr[i] = _lib.CopyOp(src, int(peer_slot_of[src][e]), dst)
         with torch.cuda.stream(stream):
-            _lib.check(self.lib.mp_layer_migrate(self._h, arr, len(ops), c_void_p(stream.cuda_stream),
-                                                 c_void_p(event.cuda_event)), "mp_layer_migrate")
+            _lib.check(self.lib.mp_layer_migrate(self._h, arr, len(ops), c_void_p(stream.cuda_stream), None),
+                       "mp_layer_migrate")
+            event.record(stream)  # torch-side record: the CUDA event is created lazily by torch
         for _, dst in adds:
             self._free.remove(dst)
         return adds
