@@ -70,7 +70,7 @@ struct mp_layer {
   // scratch views
   __nv_bfloat16 *h = nullptr, *wg = nullptr, *w13s = nullptr, *w2s = nullptr, *hs = nullptr, *ys = nullptr;
   float *wg_packed = nullptr, *bias = nullptr, *w = nullptr, *sgate = nullptr;
-  int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr,
+  int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr, *blk_prefix = nullptr,
           *batch_counts = nullptr, *route_d = nullptr,
           *slot_of_d = nullptr;
   uint32_t *hist = nullptr, *err = nullptr, *ticket = nullptr;
@@ -150,7 +150,7 @@ int mp_router_topk_hist(const void* x, const void* packed, const float* bias, in
   if (!x || !packed || !idx || !w) return set_error(MP_E_ARG, "mp_router_topk_hist: null pointer");
   return launch_router(static_cast<const __nv_bfloat16*>(x), static_cast<const float*>(packed), bias, T, d,
                        E, has_gate, k, score_mode, renorm,
-                       idx, w, gate_out, hist, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+                       idx, w, gate_out, hist, nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream));
 }
 
 int mp_grouped_gemm(const void* a, int64_t a_rows, const void* b, int64_t b_rows, const int32_t* groups,
@@ -243,6 +243,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       L->pos_dst = cv.take<int32_t>(size_t(T) * k);
       L->pos_row = cv.take<int32_t>(size_t(T) * k);
       L->blk_counts = cv.take<int32_t>(size_t(L->nb_max) * E);
+      L->blk_prefix = cv.take<int32_t>(size_t(L->nb_max) * E);
       L->batch_counts = cv.take<int32_t>(64);
       L->route_d = cv.take<int32_t>(8 * 64);
       L->slot_of_d = cv.take<int32_t>(64);
@@ -473,7 +474,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   MP_TRY(mark());  // 0
   MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
                        D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
-                       L->ticket, st));
+                       L->ticket, L->blk_prefix, st));
   ++launches;
   MP_TRY(mark());  // 1 router (+ per-batch counts)
   const int32_t* counts_all = L->batch_counts;
@@ -484,7 +485,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   }
   MP_TRY(mark());  // 2 count exchange
   MP_TRY(mark());  // 3 (layout: folded into permute / GEMM prologues)
-  MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, L->blk_counts, rank, G,
+  MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, L->blk_prefix, rank, G,
                         T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st));
   ++launches;
   MP_TRY(mark());  // 4 permute + dispatch

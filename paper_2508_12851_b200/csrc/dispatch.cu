@@ -26,7 +26,8 @@ namespace mp {
 //   * my_base[e]: first row of this origin's expert-e rows in the target GPU's
 //     receive buffer = rows of lower experts on that GPU + rows of lower-ranked
 //     sources for e (from the exchanged counts C[G][E] and the route table);
-//   * prefix[e]: rows of expert e in this origin's earlier router blocks.
+//   * prefix[e]: rows of expert e in this origin's earlier router blocks
+//     (scanned once by the router's last CTA into blk_prefix).
 // Phase 1: one thread per (token, slot) pair computes its stable in-block rank.
 // Phase 2: one warp per token loads the x row once (16 B per lane per step) and
 //          stores it to its k destinations, local or peer (NVLink) rows.
@@ -34,7 +35,7 @@ template <int kVecPerLane>
 __global__ void __launch_bounds__(256)
     permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
                    const int32_t* __restrict__ route, const int32_t* __restrict__ counts_all,
-                   const int32_t* __restrict__ blk_counts, int rank, int G, int T, int d, int E, int k,
+                   const int32_t* __restrict__ blk_prefix, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* __restrict__ recv_ptrs, int32_t* __restrict__ pos_dst,
                    int32_t* __restrict__ pos_row) {
   constexpr int kTok = 32;
@@ -52,26 +53,17 @@ __global__ void __launch_bounds__(256)
     C[i / E][i % E] = counts_all[i];
     R[i / E][i % E] = route[i];
   }
-  if (tid < E) base_s[tid] = 0;
   if (tid < np) s_e[tid] = idx[size_t(t0) * k + tid];
   __syncthreads();
-  // rows of this origin's earlier blocks, per expert (integer sums: order-free)
-  const int per = (int(blockDim.x) / E) * E;
-  if (tid < per) {
-    const int e = tid % E;
-    int sum = 0;
-    for (int i = tid; i < b * E; i += per) sum += blk_counts[i];
-    if (sum) atomicAdd(&base_s[e], sum);
-  }
   if (tid < E) {
     const int e = tid, D = R[rank][e];
-    int base = 0;
+    int base = blk_prefix[size_t(b) * E + e];
     for (int e2 = 0; e2 < e; ++e2)
       for (int s = 0; s < G; ++s)
         if (R[s][e2] == D) base += C[s][e2];
     for (int s = 0; s < rank; ++s)
       if (R[s][e] == D) base += C[s][e];
-    atomicAdd(&base_s[e], base);
+    base_s[e] = base;
   }
   __syncthreads();
   if (tid < np) {
@@ -108,7 +100,7 @@ __global__ void __launch_bounds__(256)
 }
 
 int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
-                   const int32_t* blk_counts, int rank, int G, int T, int d, int E, int k,
+                   const int32_t* blk_prefix, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream) {
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "permute: d=%d not a multiple of 8", d);
   if (k > 8) return set_error(MP_E_SHAPE, "permute: top_k=%d > 8", k);
@@ -117,7 +109,7 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   const int grid = (T + 31) / 32;
   const int vpl = (d / 8 + 31) / 32;
 #define MP_PERM_LAUNCH(N)                                                                                       \
-  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route, counts_all, blk_counts, rank, G, T, d, E, k, recv_ptrs, \
+  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route, counts_all, blk_prefix, rank, G, T, d, E, k, recv_ptrs, \
                                               pos_dst, pos_row)
   if (vpl <= 1) MP_PERM_LAUNCH(1);
   else if (vpl <= 2) MP_PERM_LAUNCH(2);

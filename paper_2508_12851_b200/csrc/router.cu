@@ -87,12 +87,12 @@ MP_DEV void cp_async_wait() {
 // the Wg chunk [kc][E_pad] fp32; kStages-deep cp.async ring.
 constexpr int kStages = 4;
 template <int TE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
     router_kernel(const __nv_bfloat16* __restrict__ x, const uint4* __restrict__ wp, const float* __restrict__ bias,
                   int T, int d, int E, int has_gate, int k, int score_mode, int renorm, int kc,
                   int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
                   uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
-                  uint32_t* __restrict__ ticket) {
+                  uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix) {
   extern __shared__ __align__(16) uint8_t rsm[];
   __shared__ float logits[rt::kTokens][rt::kMaxE + 2];
   __shared__ int cnt_s[rt::kMaxE];
@@ -249,24 +249,48 @@ __global__ void __launch_bounds__(256)
   if (!is_last) return;
   __threadfence();
   const int nb = gridDim.x;
-  for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
+  // stage the [nb][E] block-count matrix in the (now idle) dynamic smem ring with
+  // coalesced loads, then per-expert scans run from shared memory
+  int* bc = reinterpret_cast<int*>(rsm);
+  const bool staged = size_t(nb) * E * 4 <= size_t(kStages) * stage_bytes;
+  if (staged)
+    for (int i = tid; i < nb * E; i += blockDim.x) bc[i] = __ldcg(&blk_counts[i]);
   __syncthreads();
-  const int per = (int(blockDim.x) / E) * E;  // threads keep a fixed expert
-  if (tid < per) {
-    const int e = tid % E;
+  __shared__ int seg_sum[64][17];
+  int P = 1;
+  while (P * 2 * E <= int(blockDim.x) && P * 2 <= 16) P *= 2;
+  const int e = tid / P, p = tid - (tid / P) * P;
+  const int seg = (nb + P - 1) / P;
+  const int b0 = min(nb, p * seg), b1 = min(nb, b0 + seg);
+  auto cnt = [&](int blk) { return staged ? bc[blk * E + e] : __ldcg(&blk_counts[size_t(blk) * E + e]); };
+  if (e < E) {
     int sum = 0;
-    for (int i = tid; i < nb * E; i += per) sum += __ldcg(&blk_counts[i]);
-    atomicAdd(&cnt_s[e], sum);
+    for (int blk = b0; blk < b1; ++blk) sum += cnt(blk);
+    seg_sum[e][p] = sum;
   }
   __syncthreads();
-  for (int e = tid; e < E; e += blockDim.x) batch_counts[e] = cnt_s[e];
+  if (e < E) {
+    int run = 0;
+    for (int q = 0; q < p; ++q) run += seg_sum[e][q];
+    if (p == P - 1) {
+      int tot = run;
+      for (int blk = b0; blk < b1; ++blk) tot += cnt(blk);
+      batch_counts[e] = tot;
+    }
+    // exclusive prefix over blocks: blk_prefix[b][e] = sum_{b' < b} blk_counts[b'][e]
+    if (blk_prefix != nullptr)
+      for (int blk = b0; blk < b1; ++blk) {
+        blk_prefix[size_t(blk) * E + e] = run;
+        run += cnt(blk);
+      }
+  }
   if (tid == 0) *ticket = 0u;  // ready for the next launch (stream-ordered)
 }
 
 int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
-                  cudaStream_t stream) {
+                  int32_t* blk_prefix, cudaStream_t stream) {
   if (batch_counts && !ticket) return set_error(MP_E_ARG, "router: batch counts need a ticket word");
   if (E < 1 || E > rt::kMaxE) return set_error(MP_E_SHAPE, "router: E=%d outside [1, %d]", E, rt::kMaxE);
   if (k < 1 || k > E || k > rt::kMaxK) return set_error(MP_E_SHAPE, "router: top_k=%d invalid for E=%d", k, E);
@@ -275,10 +299,10 @@ int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* b
   if (T <= 0) return MP_OK;
   const int E_tot = E + (has_gate ? 1 : 0);
   const int E_pad = router_e_pad(E_tot);
-  int TE = E_pad <= 16 ? 2 : 8;
+  int TE = E_pad <= 16 ? 2 : 4;
   if (const char* env = getenv("MP_ROUTER_TE")) {  // tuning override (2, 4 or 8)
     const int v = atoi(env);
-    if ((v == 2 || v == 4 || v == 8) && E_pad % v == 0 && E_pad / v <= 8) TE = v;
+    if ((v == 2 || v == 4 || v == 8) && E_pad % v == 0 && E_pad / v <= 16) TE = v;
   }
   const int warps = E_pad / TE;
   const int grid = (T + rt::kTokens - 1) / rt::kTokens;
@@ -292,7 +316,7 @@ int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* b
   if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router)");                            \
   router_kernel<N><<<grid, 32 * warps, smem, stream>>>(x, wp, bias, T, d, E, has_gate ? 1 : 0, k, score_mode, \
                                                        renorm, kc, idx, w, shared_gate, hist, blk_counts,     \
-                                                       batch_counts, ticket)
+                                                       batch_counts, ticket, blk_prefix)
   if (TE == 2) {
     MP_ROUTER_LAUNCH(2);
   } else if (TE == 4) {
