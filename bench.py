@@ -235,7 +235,7 @@ def main_b200(args):
     # ---- activation counts of a warm-up batch (GPU router kernel) -> placement
     lib = _lib.load()
     import ctypes
-    packed = torch.empty((shape.E + shape.shared_gate + 7) // 8 * 8 * shape.d, device=dev, dtype=torch.float32)
+    packed = torch.empty((shape.E + shape.shared_gate + 7) // 8 * 8 * shape.d, device=dev, dtype=torch.bfloat16)
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     _lib.check(lib.mp_router_pack(ctypes.c_void_p(wg.data_ptr()), shape.E + shape.shared_gate, shape.d,
                                   ctypes.c_void_p(packed.data_ptr()), st))

@@ -55,10 +55,10 @@ int mp_last_error(char* buf, int buf_len);
  * Stateless kernels (used by the layer, exported for parity tests).
  * --------------------------------------------------------------------- */
 
-/* Repack router weights Wg [E_tot, d] bf16 into the kernel layout
- * [d][E_pad] fp32 (Wg transposed), E_pad = E_tot rounded up to a multiple of
- * 8 (zero columns); `packed` must hold E_pad * d floats.  E_tot = E, or E+1
- * with the shared-expert gate row. */
+/* Copy router weights Wg [E_tot, d] bf16 into the kernel layout [E_pad][d]
+ * bf16, E_pad = E_tot rounded up to a multiple of 8 (zero rows); `packed`
+ * must hold E_pad * d bf16 values; d % 256 == 0.  E_tot = E, or E+1 with the
+ * shared-expert gate row. */
 int mp_router_pack(const void* wg_bf16, int E_tot, int d, void* packed, void* stream);
 
 /* K1 -- replaces ActivationStats.ingest (stats.py:82-96) fed by sampled expert

@@ -33,9 +33,11 @@ and what is not:
                            the stated tolerance for activations.
 
 Numerics contract shared with the CUDA kernels:
-  logits[t,e] = sequential fp32 accumulation over k = 0..d-1 of x[t,k]*Wg[e,k]
-                (bf16 inputs: each product is exact in fp32, so the GPU's FMA
-                chain and this add chain round identically), then + bias[e].
+  logits[t,e] = 32 lane partials (lane l: sequential fp32 accumulation over
+                k in [256 s + 8 l, +8), s ascending) combined by the butterfly
+                tree p[l] += p[l + o], o = 16..1 (bf16 inputs: each product is
+                exact in fp32, so the GPU's FMA chain and this add chain round
+                identically), then + bias[e].
   top-k       = k largest logits, descending, ties -> lower expert id.
   h           = bf16( silu(g) * u ) with g, u the fp32 GEMM accumulators.
   y           = bf16( h @ W2^T ) (fp32 accumulate).
@@ -186,17 +188,34 @@ def slot_assignment(gpu_experts) -> dict:
 
 
 def router_logits(x: np.ndarray, wg: np.ndarray, bias: np.ndarray | None = None) -> np.ndarray:
-    """Sequential fp32 accumulation over k ascending (see the numerics contract)."""
+    """Router logits under the kernel's numerics contract (csrc/router.cu).
+
+    Lane l of 32 owns k in [256 s + 8 l, 256 s + 8 l + 8) for s = 0..d/256-1; its
+    partial is a sequential fp32 accumulation over those k ascending (bf16
+    inputs: products exact, one rounding per add == the GPU's FMA).  The 32
+    partials are combined by the butterfly tree p[l] <- p[l] + p[l + o],
+    o = 16, 8, 4, 2, 1; then + bias[e].
+    """
     x = np.asarray(x, dtype=np.float32)
     wg = np.asarray(wg, dtype=np.float32)
     T, d = x.shape
-    acc = np.zeros((T, wg.shape[0]), dtype=np.float32)
-    wt = np.ascontiguousarray(wg.T)
-    for kk in range(d):
-        acc += x[:, kk:kk + 1] * wt[kk][None, :]   # exact products, one fp32 rounding per add
+    E = wg.shape[0]
+    if d % 256:
+        raise ValueError("router contract needs d % 256 == 0")
+    S = d // 256
+    xr = x.reshape(T, S, 32, 8)
+    wr = wg.reshape(E, S, 32, 8)
+    acc = np.zeros((T, E, 32), dtype=np.float32)
+    for s in range(S):
+        for j in range(8):
+            acc += xr[:, None, s, :, j] * wr[None, :, s, :, j]   # exact products, one fp32 rounding per add
+    p = acc
+    for o in (16, 8, 4, 2, 1):
+        p = p[..., :o] + p[..., o:2 * o]
+    logits = np.ascontiguousarray(p[..., 0])
     if bias is not None:
-        acc[:, :bias.shape[0]] += np.asarray(bias, dtype=np.float32)[None, :]
-    return acc
+        logits[:, :bias.shape[0]] += np.asarray(bias, dtype=np.float32)[None, :]
+    return logits
 
 
 def topk_route(logits: np.ndarray, E: int, k: int, score_mode: int, renorm: int = 0):

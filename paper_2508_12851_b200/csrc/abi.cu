@@ -69,7 +69,8 @@ struct mp_layer {
   uint32_t* flags = nullptr;
   // scratch views
   __nv_bfloat16 *h = nullptr, *wg = nullptr, *w13s = nullptr, *w2s = nullptr, *hs = nullptr, *ys = nullptr;
-  float *wg_packed = nullptr, *bias = nullptr, *w = nullptr, *sgate = nullptr;
+  __nv_bfloat16* wg_packed = nullptr;
+  float *bias = nullptr, *w = nullptr, *sgate = nullptr;
   int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr, *blk_prefix = nullptr,
           *batch_counts = nullptr, *route_d = nullptr,
           *slot_of_d = nullptr;
@@ -140,15 +141,15 @@ int mp_last_error(char* buf, int buf_len) {
 
 int mp_router_pack(const void* wg_bf16, int E_tot, int d, void* packed, void* stream) {
   if (!wg_bf16 || !packed) return set_error(MP_E_ARG, "mp_router_pack: null pointer");
-  return launch_router_pack(static_cast<const __nv_bfloat16*>(wg_bf16), E_tot, d, static_cast<float*>(packed),
-                            static_cast<cudaStream_t>(stream));
+  return launch_router_pack(static_cast<const __nv_bfloat16*>(wg_bf16), E_tot, d,
+                            static_cast<__nv_bfloat16*>(packed), static_cast<cudaStream_t>(stream));
 }
 
 int mp_router_topk_hist(const void* x, const void* packed, const float* bias, int T, int d, int E, int has_gate,
                         int k, int score_mode, int renorm, int32_t* idx, float* w, float* gate_out, uint32_t* hist,
                         void* stream) {
   if (!x || !packed || !idx || !w) return set_error(MP_E_ARG, "mp_router_topk_hist: null pointer");
-  return launch_router(static_cast<const __nv_bfloat16*>(x), static_cast<const float*>(packed), bias, T, d,
+  return launch_router(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(packed), bias, T, d,
                        E, has_gate, k, score_mode, renorm,
                        idx, w, gate_out, hist, nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream));
 }
@@ -235,7 +236,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
     auto plan = [&](Carver& cv) {
       L->h = cv.take<__nv_bfloat16>(size_t(L->recv_cap) * D.f);
       L->wg = cv.take<__nv_bfloat16>(size_t(E_tot) * D.d);
-      L->wg_packed = cv.take<float>(size_t(router_e_pad(E_tot)) * D.d);
+      L->wg_packed = cv.take<__nv_bfloat16>(size_t(router_e_pad(E_tot)) * D.d);
       L->bias = cv.take<float>(E);
       L->w = cv.take<float>(size_t(T) * k);
       L->sgate = D.shared_gate ? cv.take<float>(T) : nullptr;

@@ -12,16 +12,20 @@
 //                 Qwen1.5-MoE / DeepSeek-V2-Lite)
 //   hist[e]    += #tokens whose top-k contains e   (token_count = 1 per token)
 //
-// Bit-exactness contract (checked against oracle/moe_oracle.py): every logit
-// is ONE sequential fp32 FMA chain over k = 0..d-1 ascending, starting at 0.
-// x and Wg are bf16, so every product is exact in fp32 and fma(x,w,acc) ==
-// rn(acc + x*w); the oracle restates this with numpy float32 adds.  Selection
-// compares logits only, so the indices do not depend on the exp implementation.
+// Bit-exactness contract (restated by oracle/moe_oracle.py:router_logits):
+//   * lane l of 32 owns the k-slices [256 s + 8 l, 256 s + 8 l + 8), s = 0..d/256-1;
+//     its partial is ONE sequential fp32 FMA chain over those k ascending, from 0;
+//     x and Wg are bf16, so each product is exact and fma == rn(acc + x*w);
+//   * the 32 partials are combined by the butterfly tree
+//     p[l] <- p[l] + p[l + o] for o = 16, 8, 4, 2, 1 (fp add is commutative, so
+//     a warp reduce-scatter yields exactly this tree), then + bias[e];
+//   * selection compares logits only (independent of the exp implementation).
 //
-// Layout: Wg is repacked once into [d][E_pad] fp32 (Wg^T, E_pad = E_tot
-// rounded up to 8, zero columns), so the TE weights of one k are contiguous.  A CTA owns 32 tokens (one per lane) and all experts (TE per
-// warp); x rows and Wg columns are staged through shared memory in k-chunks by
-// a double-buffered cp.async pipeline.
+// Mapping: a CTA owns 32 tokens (8 warps x 4 tokens).  A warp keeps 4 tokens x
+// 8 experts = 32 accumulators per lane (16 FFMA2 chains) while its lanes walk d;
+// x rows are read straight from HBM (512 B coalesced per token per step), the
+// padded bf16 Wg [E_pad][d] through L1/L2.  One reduce-scatter per 8-expert pass
+// leaves lane l holding logit (token l/8, expert l%8).
 #include <cstdlib>
 
 #include "common.cuh"
@@ -38,26 +42,25 @@ constexpr int kMaxK = 8;
 int router_block_tokens() { return rt::kTokens; }
 __host__ __device__ int router_e_pad(int E_tot) { return (E_tot + 7) / 8 * 8; }
 
-// packed[k][E_pad] fp32 = Wg[e][k] (Wg transposed; zero columns pad E_tot up to E_pad)
+// packed[E_pad][d] bf16 = Wg (zero rows pad E_tot up to a multiple of 8)
 __global__ void router_pack_kernel(const __nv_bfloat16* __restrict__ wg, int E_tot, int E_pad, int d,
-                                   float* __restrict__ packed) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // over d * E_pad
-  if (i >= E_pad * d) return;
-  const int k = i / E_pad, e = i - k * E_pad;
-  packed[i] = e < E_tot ? __bfloat162float(wg[size_t(e) * d + k]) : 0.0f;
+                                   __nv_bfloat16* __restrict__ packed) {
+  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over E_pad * d
+  if (i >= size_t(E_pad) * d) return;
+  packed[i] = i < size_t(E_tot) * d ? wg[i] : __float2bfloat16(0.0f);
 }
 
-int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, float* packed, cudaStream_t stream) {
-  if (d % 8 != 0) return set_error(MP_E_SHAPE, "router d=%d not a multiple of 8", d);
+int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16* packed, cudaStream_t stream) {
+  if (d % 256 != 0) return set_error(MP_E_SHAPE, "router d=%d not a multiple of 256", d);
   const int E_pad = router_e_pad(E_tot);
-  const int n = E_pad * d;
-  router_pack_kernel<<<(n + 255) / 256, 256, 0, stream>>>(wg, E_tot, E_pad, d, packed);
+  const size_t n = size_t(E_pad) * d;
+  router_pack_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(wg, E_tot, E_pad, d, packed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_pack_kernel launch");
 }
 
 // acc = (acc.lo + x*w.lo, acc.hi + x*w.hi): two independent fp32 FMAs (FFMA2),
-// each rounded exactly like fmaf -- the per-logit chain contract is unchanged.
+// each rounded exactly like fmaf -- the per-lane chain contract is unchanged.
 MP_DEV void ffma2(unsigned long long& acc, float x, unsigned long long w) {
   const unsigned long long xx = (unsigned long long)__float_as_uint(x) | ((unsigned long long)__float_as_uint(x) << 32);
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xx), "l"(w));
@@ -69,109 +72,96 @@ MP_DEV unsigned long long pack2(float lo, float hi) {
 // Larger logit wins; equal logits -> lower expert id.
 MP_DEV bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
 
-MP_DEV void cp_async_16(void* smem, const void* gmem, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem), "r"(src_bytes)
-               : "memory");
-}
-MP_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-MP_DEV void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
+#ifndef MP_ROUTER_MIN_BLOCKS
+#define MP_ROUTER_MIN_BLOCKS 1
+#endif
+constexpr int kWarps = 8;      // 8 warps x 4 tokens = rt::kTokens
+constexpr int kTokPerWarp = 4;
+constexpr int kExpPerPass = 8;
 
-// CTA = 32 tokens x (E_pad / TE) warps.  Lane = token, warp = a group of TE
-// consecutive experts: every x element is loaded once per thread and feeds TE
-// independent fp32 chains, two per FFMA2 instruction; the Wg values of one k
-// are warp-uniform (shared-memory broadcast).  Per stage, shared memory holds
-// the x chunk [32][kc+8] bf16 (padded rows: conflict-free 16 B lane loads) and
-// the Wg chunk [kc][E_pad] fp32; kStages-deep cp.async ring.
-constexpr int kStages = 4;
-template <int TE>
-__global__ void __launch_bounds__(512)
-    router_kernel(const __nv_bfloat16* __restrict__ x, const uint4* __restrict__ wp, const float* __restrict__ bias,
-                  int T, int d, int E, int has_gate, int k, int score_mode, int renorm, int kc,
-                  int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
+__global__ void __launch_bounds__(kWarps * 32, MP_ROUTER_MIN_BLOCKS)
+    router_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wp,
+                  const float* __restrict__ bias, int T, int d, int E, int has_gate, int k, int score_mode,
+                  int renorm, int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
                   uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
                   uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix) {
-  extern __shared__ __align__(16) uint8_t rsm[];
-  __shared__ float logits[rt::kTokens][rt::kMaxE + 2];
+  __shared__ float logits[rt::kTokens][rt::kMaxE + 9];
   __shared__ int cnt_s[rt::kMaxE];
+  extern __shared__ int bc[];  // [nb][E] block counts staged by the last CTA (dynamic smem)
 
   const int E_tot = E + has_gate;
   const int E_pad = router_e_pad(E_tot);
   const int t0 = blockIdx.x * rt::kTokens;
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
-  const int pitch = kc + 8;                       // bf16 elements per staged x row
-  const int x_bytes = rt::kTokens * pitch * 2;
-  const int w_bytes = kc * E_pad * 4;
-  const int stage_bytes = x_bytes + w_bytes;
   for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
 
-  unsigned long long acc[TE / 2];
+  // this warp's 4 tokens (rows past T read row 0 and are discarded)
+  const __nv_bfloat16* xr[kTokPerWarp];
 #pragma unroll
-  for (int j = 0; j < TE / 2; ++j) acc[j] = 0ull;
-  const int e0 = warp * TE;
-  const int n_chunks = d / kc;
-
-  auto issue = [&](int c) {
-    uint8_t* base = rsm + (c % kStages) * stage_bytes;
-    const int k0 = c * kc;
-    const int xv = kc / 8;
-    for (int v = tid; v < rt::kTokens * xv; v += blockDim.x) {
-      const int tt = v / xv, c8 = (v - tt * xv) * 8;
-      const bool ok = t0 + tt < T;
-      const __nv_bfloat16* src = ok ? x + size_t(t0 + tt) * d + k0 + c8 : x;
-      cp_async_16(base + (tt * pitch + c8) * 2, src, ok ? 16u : 0u);
-    }
-    const uint4* wsrc = wp + size_t(k0) * E_pad / 4;
-    uint4* wdst = reinterpret_cast<uint4*>(base + x_bytes);
-    for (int v = tid; v < kc * E_pad / 4; v += blockDim.x) cp_async_16(wdst + v, wsrc + v, 16u);
-  };
-
-  // prologue: kStages-1 chunks in flight (one commit group per chunk, empty groups past the end)
-#pragma unroll
-  for (int c = 0; c < kStages - 1; ++c) {
-    if (c < n_chunks) issue(c);
-    cp_async_commit();
+  for (int i = 0; i < kTokPerWarp; ++i) {
+    const int t = t0 + warp * kTokPerWarp + i;
+    xr[i] = x + size_t(t < T ? t : 0) * d + 8 * lane;
   }
-  for (int c = 0; c < n_chunks; ++c) {
-    if (c + kStages - 1 < n_chunks) issue(c + kStages - 1);
-    cp_async_commit();
-    cp_async_wait<kStages - 1>();
-    __syncthreads();
-    const uint8_t* base = rsm + (c % kStages) * stage_bytes;
-    const uint4* xrow = reinterpret_cast<const uint4*>(base + size_t(lane) * pitch * 2);
-    const float* ws = reinterpret_cast<const float*>(base + x_bytes) + e0;
+  const int S = d / 256;
+
+  for (int e0 = 0; e0 < E_pad; e0 += kExpPerPass) {
+    unsigned long long acc[kTokPerWarp][kExpPerPass / 2];
+#pragma unroll
+    for (int i = 0; i < kTokPerWarp; ++i)
+#pragma unroll
+      for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
+    const __nv_bfloat16* wr = wp + size_t(e0) * d + 8 * lane;
 #pragma unroll 2
-    for (int kk = 0; kk < kc; kk += 8) {
-      const uint4 xv = xrow[kk >> 3];
-      const float xs[8] = {bf16_lo(xv.x), bf16_hi(xv.x), bf16_lo(xv.y), bf16_hi(xv.y),
-                           bf16_lo(xv.z), bf16_hi(xv.z), bf16_lo(xv.w), bf16_hi(xv.w)};
+    for (int s = 0; s < S; ++s) {
+      uint4 xv[kTokPerWarp], wv[kExpPerPass];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {   // strictly ascending k
-        const float* wr = ws + size_t(kk + q) * E_pad;
-        if constexpr (TE == 2) {
-          const float2 w = *reinterpret_cast<const float2*>(wr);
-          ffma2(acc[0], xs[q], pack2(w.x, w.y));
-        } else {
+      for (int i = 0; i < kTokPerWarp; ++i) xv[i] = ld_nc_v4(xr[i] + 256 * s);
 #pragma unroll
-          for (int j = 0; j < TE / 4; ++j) {
-            const float4 w = reinterpret_cast<const float4*>(wr)[j];
-            ffma2(acc[2 * j], xs[q], pack2(w.x, w.y));
-            ffma2(acc[2 * j + 1], xs[q], pack2(w.z, w.w));
-          }
+      for (int j = 0; j < kExpPerPass; ++j)
+        wv[j] = __ldg(reinterpret_cast<const uint4*>(wr + size_t(j) * d + 256 * s));
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // strictly ascending k inside the lane's slice
+        float xs[kTokPerWarp];
+#pragma unroll
+        for (int i = 0; i < kTokPerWarp; ++i) {
+          const uint32_t u = (&xv[i].x)[q >> 1];
+          xs[i] = (q & 1) ? bf16_hi(u) : bf16_lo(u);
+        }
+#pragma unroll
+        for (int j = 0; j < kExpPerPass / 2; ++j) {
+          const uint32_t u0 = (&wv[2 * j].x)[q >> 1], u1 = (&wv[2 * j + 1].x)[q >> 1];
+          const unsigned long long w2 =
+              (q & 1) ? pack2(bf16_hi(u0), bf16_hi(u1)) : pack2(bf16_lo(u0), bf16_lo(u1));
+#pragma unroll
+          for (int i = 0; i < kTokPerWarp; ++i) ffma2(acc[i][j], xs[i], w2);
         }
       }
     }
-    __syncthreads();
-  }
+    // butterfly reduce-scatter over the 32 lane partials of 32 values
+    // (value v = token v/8, expert v%8); afterwards lane l holds value l
+    float v[32];
 #pragma unroll
-  for (int j = 0; j < TE; ++j) {
-    const int e = e0 + j;
+    for (int i = 0; i < kTokPerWarp; ++i)
+#pragma unroll
+      for (int j = 0; j < kExpPerPass / 2; ++j) {
+        v[i * 8 + 2 * j] = __uint_as_float(uint32_t(acc[i][j]));
+        v[i * 8 + 2 * j + 1] = __uint_as_float(uint32_t(acc[i][j] >> 32));
+      }
+#pragma unroll
+    for (int o = 16, n = 32; o >= 1; o >>= 1, n >>= 1) {
+      const bool upper = (lane & o) != 0;
+#pragma unroll
+      for (int i = 0; i < n / 2; ++i) {
+        const float send = upper ? v[i] : v[i + n / 2];
+        const float keep = upper ? v[i + n / 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    const int tt = warp * kTokPerWarp + (lane >> 3), e = e0 + (lane & 7);
     if (e < E_tot) {
-      float v = __uint_as_float(uint32_t(acc[j >> 1] >> ((j & 1) * 32)));
-      if (bias != nullptr && e < E) v = __fadd_rn(v, bias[e]);
-      logits[lane][e] = v;
+      float val = v[0];
+      if (bias != nullptr && e < E) val = __fadd_rn(val, bias[e]);
+      logits[tt][e] = val;
     }
   }
   __syncthreads();
@@ -249,10 +239,9 @@ __global__ void __launch_bounds__(512)
   if (!is_last) return;
   __threadfence();
   const int nb = gridDim.x;
-  // stage the [nb][E] block-count matrix in the (now idle) dynamic smem ring with
-  // coalesced loads, then per-expert scans run from shared memory
-  int* bc = reinterpret_cast<int*>(rsm);
-  const bool staged = size_t(nb) * E * 4 <= size_t(kStages) * stage_bytes;
+  // stage the [nb][E] block-count matrix in shared memory with coalesced loads
+  // (when it fits), then per-expert scans run from there
+  const bool staged = true;
   if (staged)
     for (int i = tid; i < nb * E; i += blockDim.x) bc[i] = __ldcg(&blk_counts[i]);
   __syncthreads();
@@ -287,45 +276,29 @@ __global__ void __launch_bounds__(512)
   if (tid == 0) *ticket = 0u;  // ready for the next launch (stream-ordered)
 }
 
-int launch_router(const __nv_bfloat16* x, const float* wg_packed, const float* bias, int T, int d, int E,
+int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
                   int32_t* blk_prefix, cudaStream_t stream) {
   if (batch_counts && !ticket) return set_error(MP_E_ARG, "router: batch counts need a ticket word");
   if (E < 1 || E > rt::kMaxE) return set_error(MP_E_SHAPE, "router: E=%d outside [1, %d]", E, rt::kMaxE);
   if (k < 1 || k > E || k > rt::kMaxK) return set_error(MP_E_SHAPE, "router: top_k=%d invalid for E=%d", k, E);
-  if (d % 8 != 0) return set_error(MP_E_SHAPE, "router: d=%d not a multiple of 8", d);
+  if (d % 256 != 0) return set_error(MP_E_SHAPE, "router: d=%d not a multiple of 256", d);
   if (score_mode != 0 && score_mode != 1) return set_error(MP_E_ARG, "router: score_mode %d", score_mode);
   if (T <= 0) return MP_OK;
-  const int E_tot = E + (has_gate ? 1 : 0);
-  const int E_pad = router_e_pad(E_tot);
-  int TE = E_pad <= 16 ? 2 : 4;
-  if (const char* env = getenv("MP_ROUTER_TE")) {  // tuning override (2, 4 or 8)
-    const int v = atoi(env);
-    if ((v == 2 || v == 4 || v == 8) && E_pad % v == 0 && E_pad / v <= 16) TE = v;
-  }
-  const int warps = E_pad / TE;
   const int grid = (T + rt::kTokens - 1) / rt::kTokens;
-  const uint4* wp = reinterpret_cast<const uint4*>(wg_packed);
-  int kc = E_pad <= 16 ? 256 : 128;
-  while (d % kc) kc >>= 1;
-  const size_t smem = size_t(kStages) * (rt::kTokens * (kc + 8) * 2 + size_t(kc) * E_pad * 4);
-  cudaError_t e;
-#define MP_ROUTER_LAUNCH(N)                                                                                    \
-  e = cudaFuncSetAttribute(router_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));        \
-  if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(router)");                            \
-  router_kernel<N><<<grid, 32 * warps, smem, stream>>>(x, wp, bias, T, d, E, has_gate ? 1 : 0, k, score_mode, \
-                                                       renorm, kc, idx, w, shared_gate, hist, blk_counts,     \
-                                                       batch_counts, ticket, blk_prefix)
-  if (TE == 2) {
-    MP_ROUTER_LAUNCH(2);
-  } else if (TE == 4) {
-    MP_ROUTER_LAUNCH(4);
-  } else {
-    MP_ROUTER_LAUNCH(8);
+  const size_t smem = blk_counts && batch_counts ? size_t(grid) * E * 4 : 0;
+  if (smem > 200 * 1024) return set_error(MP_E_SHAPE, "router: %d blocks x %d experts too large", grid, E);
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    cudaError_t ea = cudaFuncSetAttribute(router_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (ea != cudaSuccess) return set_cuda_error(ea, "cudaFuncSetAttribute(router)");
+    smem_set = smem;
   }
-#undef MP_ROUTER_LAUNCH
-  e = cudaGetLastError();
+  router_kernel<<<grid, kWarps * 32, smem, stream>>>(x, wg_packed, bias, T, d, E, has_gate ? 1 : 0, k, score_mode, renorm,
+                                                  idx, w, shared_gate, hist, blk_counts, batch_counts, ticket,
+                                                  blk_prefix);
+  cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_kernel launch");
 }
 

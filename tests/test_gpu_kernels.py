@@ -121,7 +121,7 @@ def test_router_bit_exact(E, k, mode, gate, d, T):
 
     xt = torch.from_numpy(x).cuda().bfloat16()
     wgt = torch.from_numpy(wg).cuda().bfloat16()
-    packed = torch.empty((E + gate + 7) // 8 * 8 * d, device="cuda", dtype=torch.float32)
+    packed = torch.empty((E + gate + 7) // 8 * 8 * d, device="cuda", dtype=torch.bfloat16)
     L.check(lib.mp_router_pack(_vp(wgt), E + gate, d, _vp(packed), _stream()))
     bt = torch.from_numpy(bias).cuda()
     idx = torch.empty(T, k, dtype=torch.int32, device="cuda")

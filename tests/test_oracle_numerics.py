@@ -13,18 +13,27 @@ def test_bf16_round_matches_torch():
     np.testing.assert_array_equal(orc.bf16_round(a), ref)
 
 
-def test_router_logits_are_a_sequential_fp32_chain():
-    """The accumulation contract: acc_{k+1} = fl(acc_k + x_k * w_k), k ascending."""
+def test_router_logits_contract():
+    """32 lane chains over 8-wide k slices strided by 256, then the butterfly tree."""
     rng = np.random.default_rng(1)
-    x = orc.bf16_round(rng.standard_normal((3, 64)).astype(np.float32))
-    w = orc.bf16_round(rng.standard_normal((5, 64)).astype(np.float32))
+    d = 512
+    x = orc.bf16_round(rng.standard_normal((3, d)).astype(np.float32))
+    w = orc.bf16_round(rng.standard_normal((5, d)).astype(np.float32))
     got = orc.router_logits(x, w)
     for t in range(3):
         for e in range(5):
-            acc = np.float32(0)
-            for k in range(64):
-                acc = np.float32(acc + np.float32(x[t, k] * w[e, k]))
-            assert got[t, e] == acc
+            p = []
+            for lane in range(32):
+                acc = np.float32(0)
+                for s in range(d // 256):
+                    for j in range(8):
+                        k = 256 * s + 8 * lane + j
+                        acc = np.float32(acc + np.float32(x[t, k] * w[e, k]))
+                p.append(acc)
+            for o in (16, 8, 4, 2, 1):
+                p = [np.float32(p[i] + p[i + o]) for i in range(o)]
+            assert got[t, e] == p[0]
+    np.testing.assert_allclose(got, x @ w.T, rtol=1e-4, atol=1e-3)
 
 
 def test_topk_ties_go_to_lower_id():

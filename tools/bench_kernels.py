@@ -53,7 +53,7 @@ def main():
     if not args.only or args.only == "router":
         x = wl.tokens(T, d, dev)
         wg = wl.router_weights(E_tot, d, dev)
-        packed = torch.empty((E_tot + 7) // 8 * 8 * d, device=dev, dtype=torch.float32)
+        packed = torch.empty((E_tot + 7) // 8 * 8 * d, device=dev, dtype=torch.bfloat16)
         _lib.check(lib.mp_router_pack(vp(wg), E_tot, d, vp(packed), st))
         bias = wl.origin_bias(0, E).to(dev)
         idx = torch.empty(T, k, dtype=torch.int32, device=dev)
