@@ -74,7 +74,7 @@ struct mp_layer {
   int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr, *blk_prefix = nullptr,
           *batch_counts = nullptr, *route_d = nullptr,
           *slot_of_d = nullptr;
-  uint32_t *hist = nullptr, *err = nullptr, *ticket = nullptr;
+  uint32_t *hist = nullptr, *err = nullptr, *ticket = nullptr, *sync_state = nullptr;
   void** ptr_arrays = nullptr;  // device: recv[8], y[8], flags[8], counts0[8], counts1[8]
 
   uint8_t* peer_window[8] = {};
@@ -88,7 +88,6 @@ struct mp_layer {
   const void* tm_x_ptr = nullptr;
   int tm_x_rows = -1;
 
-  uint32_t epoch = 0;
   uint64_t fwd_count = 0;
   int last_launches = 0;
 };
@@ -251,6 +250,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       L->hist = cv.take<uint32_t>(64);
       L->err = cv.take<uint32_t>(4);
       L->ticket = cv.take<uint32_t>(4);
+      L->sync_state = cv.take<uint32_t>(4);
       L->ptr_arrays = cv.take<void*>(5 * 8);
       if (D.shared_f > 0) {
         L->w13s = cv.take<__nv_bfloat16>(size_t(2) * D.shared_f * D.d);
@@ -450,11 +450,10 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   if (!L->peers_open) return set_error(MP_E_PEER, "mp_layer_forward: peers not opened (G=%d)", L->G);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int G = L->G, E = D.E, k = D.top_k, rank = L->rank;
-  const int par = int(L->fwd_count & 1);
   auto** recv_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 0 * 8);
   auto** y_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 1 * 8);
   auto** flag_ptrs = reinterpret_cast<uint32_t**>(L->ptr_arrays + 2 * 8);
-  auto** count_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + (3 + par) * 8);
+  auto** count_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + 3 * 8);  // [parity][peer]
   int launches = 0;
   int ev_i = 0;
   auto mark = [&]() -> int {
@@ -479,14 +478,17 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   ++launches;
   MP_TRY(mark());  // 1 router (+ per-batch counts)
   const int32_t* counts_all = L->batch_counts;
+  const uint32_t* parity = nullptr;
   if (G > 1) {
-    MP_TRY(launch_publish_barrier(flag_ptrs, count_ptrs, L->batch_counts, E, G, rank, ++L->epoch, L->err, st));
+    MP_TRY(launch_publish_barrier(flag_ptrs, count_ptrs, L->batch_counts, E, G, rank, L->sync_state, L->err, st));
     ++launches;
-    counts_all = L->counts + size_t(par) * G * E;
+    counts_all = L->counts;
+    parity = L->sync_state + 2;
   }
   MP_TRY(mark());  // 2 count exchange
   MP_TRY(mark());  // 3 (layout: folded into permute / GEMM prologues)
-  MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, L->blk_prefix, rank, G,
+  MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, parity, L->blk_prefix,
+                        rank, G,
                         T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st));
   ++launches;
   MP_TRY(mark());  // 4 permute + dispatch
@@ -503,7 +505,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   }
   MP_TRY(mark());  // 5 shared expert
   if (G > 1) {
-    MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, ++L->epoch, L->err, st));
+    MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, L->sync_state, L->err, st));
     ++launches;
   }
   MP_TRY(mark());  // 6 dispatch barrier
@@ -511,6 +513,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     GroupSpec gs;
     gs.mode = 1;
     gs.counts = counts_all;
+    gs.parity = parity;
     gs.route = L->route_d;
     gs.slot_of = L->slot_of_d;
     gs.G = G;
@@ -528,7 +531,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   }
   MP_TRY(mark());  // 8 GEMM2
   if (G > 1) {
-    MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, ++L->epoch, L->err, st));
+    MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, L->sync_state, L->err, st));
     ++launches;
   }
   MP_TRY(mark());  // 9 return barrier
@@ -560,8 +563,9 @@ int mp_layer_read_counts(mp_layer* L, int32_t* host_counts, void* stream) {
   if (G == 1) {
     MP_CUDA(cudaMemcpy(host_counts, L->batch_counts, size_t(E) * 4, cudaMemcpyDeviceToHost));
   } else {
-    const int par = int((L->fwd_count + 1) & 1);  // parity of the last completed forward
-    MP_CUDA(cudaMemcpy(host_counts, L->counts + size_t(par) * G * E, size_t(G) * E * 4, cudaMemcpyDeviceToHost));
+    uint32_t par = 0;  // parity of the last completed forward (device state)
+    MP_CUDA(cudaMemcpy(&par, L->sync_state + 2, 4, cudaMemcpyDeviceToHost));
+    MP_CUDA(cudaMemcpy(host_counts, L->counts + size_t(par & 1) * G * E, size_t(G) * E * 4, cudaMemcpyDeviceToHost));
   }
   return MP_OK;
 }

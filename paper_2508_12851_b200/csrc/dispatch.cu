@@ -35,7 +35,8 @@ template <int kVecPerLane>
 __global__ void __launch_bounds__(256)
     permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
                    const int32_t* __restrict__ route, const int32_t* __restrict__ counts_all,
-                   const int32_t* __restrict__ blk_prefix, int rank, int G, int T, int d, int E, int k,
+                   const uint32_t* __restrict__ parity, const int32_t* __restrict__ blk_prefix, int rank, int G,
+                   int T, int d, int E, int k,
                    __nv_bfloat16* const* __restrict__ recv_ptrs, int32_t* __restrict__ pos_dst,
                    int32_t* __restrict__ pos_row) {
   constexpr int kTok = 32;
@@ -49,6 +50,7 @@ __global__ void __launch_bounds__(256)
   const int nt = min(kTok, T - t0);
   const int np = nt * k;
   const int tid = threadIdx.x;
+  if (parity != nullptr) counts_all += size_t(*parity) * G * E;
   for (int i = tid; i < G * E; i += blockDim.x) {
     C[i / E][i % E] = counts_all[i];
     R[i / E][i % E] = route[i];
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(256)
 }
 
 int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
-                   const int32_t* blk_prefix, int rank, int G, int T, int d, int E, int k,
+                   const uint32_t* parity, const int32_t* blk_prefix, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream) {
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "permute: d=%d not a multiple of 8", d);
   if (k > 8) return set_error(MP_E_SHAPE, "permute: top_k=%d > 8", k);
@@ -109,7 +111,8 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   const int grid = (T + 31) / 32;
   const int vpl = (d / 8 + 31) / 32;
 #define MP_PERM_LAUNCH(N)                                                                                       \
-  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route, counts_all, blk_prefix, rank, G, T, d, E, k, recv_ptrs, \
+  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route, counts_all, parity, blk_prefix, rank, G, T, d, E, k,  \
+                                              recv_ptrs,                                                   \
                                               pos_dst, pos_row)
   if (vpl <= 1) MP_PERM_LAUNCH(1);
   else if (vpl <= 2) MP_PERM_LAUNCH(2);

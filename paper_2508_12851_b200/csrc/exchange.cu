@@ -18,18 +18,31 @@ namespace mp {
 
 constexpr uint64_t kBarrierTimeoutNs = 30ull * 1000ull * 1000ull * 1000ull;
 
+// Barrier state lives on the device (graph-replayable): state[0] = barrier
+// epoch, state[1] = forwards seen by the count exchange, state[2] = count-table
+// parity of the current forward (read by the permute kernel and the GEMM
+// prologue).  Stream order serialises the single-CTA barrier kernels.
 __global__ void __launch_bounds__(256)
     publish_barrier_kernel(uint32_t* const* __restrict__ flag_ptrs, int32_t* const* __restrict__ count_ptrs,
-                           const int32_t* __restrict__ my_counts, int E, int G, int rank, uint32_t epoch,
-                           uint32_t* __restrict__ error_word) {
+                           const int32_t* __restrict__ my_counts, int E, int G, int rank,
+                           uint32_t* __restrict__ state, uint32_t* __restrict__ error_word) {
+  __shared__ uint32_t s_epoch, s_par, s_fwd;
   const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_epoch = state[0] + 1;
+    s_fwd = state[1];
+    s_par = s_fwd & 1u;
+  }
   // everything this stream wrote before (permute rows, expert outputs) must be
   // visible system-wide before the flag goes up
   __threadfence_system();
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
   if (count_ptrs != nullptr) {
+    int32_t* const* half = count_ptrs + 8 * s_par;  // [parity][peer]
     for (int i = tid; i < G * E; i += blockDim.x) {
       const int p = i / E, e = i - p * E;
-      count_ptrs[p][rank * E + e] = my_counts[e];
+      half[p][rank * E + e] = my_counts[e];
     }
   }
   __threadfence_system();
@@ -47,11 +60,18 @@ __global__ void __launch_bounds__(256)
     }
   }
   __syncthreads();
+  if (tid == 0) {
+    state[0] = epoch;
+    if (count_ptrs != nullptr) {
+      state[1] = s_fwd + 1;
+      state[2] = s_par;
+    }
+  }
 }
 
 int launch_publish_barrier(uint32_t* const* flag_ptrs, int32_t* const* count_ptrs, const int32_t* my_counts, int E,
-                           int G, int rank, uint32_t epoch, uint32_t* error_word, cudaStream_t stream) {
-  publish_barrier_kernel<<<1, 256, 0, stream>>>(flag_ptrs, count_ptrs, my_counts, E, G, rank, epoch, error_word);
+                           int G, int rank, uint32_t* state, uint32_t* error_word, cudaStream_t stream) {
+  publish_barrier_kernel<<<1, 256, 0, stream>>>(flag_ptrs, count_ptrs, my_counts, E, G, rank, state, error_word);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "publish_barrier_kernel launch");
 }

@@ -68,9 +68,10 @@ MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
   const int tid = threadIdx.x;
   if (gs.mode == 1) {
     if (tid < gs.E) {
+      const int32_t* counts = gs.counts + (gs.parity ? size_t(*gs.parity) * gs.G * gs.E : 0);
       int m = 0;
       for (int s = 0; s < gs.G; ++s)
-        if (gs.route[s * gs.E + tid] == gs.rank) m += gs.counts[s * gs.E + tid];
+        if (gs.route[s * gs.E + tid] == gs.rank) m += counts[s * gs.E + tid];
       st.g_tmp[tid] = m;
     }
     __syncthreads();

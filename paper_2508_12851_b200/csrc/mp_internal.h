@@ -26,7 +26,7 @@ int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16*
 
 // ---- K2 permute (+ dispatch through peer pointers)
 int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
-                   const int32_t* blk_prefix, int rank, int G, int T, int d, int E, int k,
+                   const uint32_t* parity, const int32_t* blk_prefix, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream);
 
 // ---- K3 grouped GEMM
@@ -34,7 +34,8 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
 struct GroupSpec {
   const int32_t* groups = nullptr;    // mode 0: explicit table [n][4] = {a_row, m, slot, out_row}
   const int32_t* n_groups = nullptr;  //         and its length (device)
-  const int32_t* counts = nullptr;    // mode 1: derived -- exchanged counts C[G][E],
+  const int32_t* counts = nullptr;    // mode 1: derived -- exchanged counts C[G][E] (+ parity half
+  const uint32_t* parity = nullptr;   //         *parity * G * E when non-null),
   const int32_t* route = nullptr;     //         route[G][E] and slot_of[E]: groups are the
   const int32_t* slot_of = nullptr;   //         experts routed to `rank`, ascending, rows packed
   int G = 1, E = 0, rank = 0;
@@ -54,8 +55,8 @@ int launch_combine(__nv_bfloat16* const* y_ptrs /*[G] device array*/, const int3
 
 // ---- exchange / barrier over NVLink peer memory
 int launch_publish_barrier(uint32_t* const* flag_ptrs /*[G] device array, each -> flags[G]*/,
-                           int32_t* const* count_ptrs /*[G] device array, each -> table[G][E] or null*/,
-                           const int32_t* my_counts, int E, int G, int rank, uint32_t epoch,
+                           int32_t* const* count_ptrs /*[2][8] device array -> table halves, or null*/,
+                           const int32_t* my_counts, int E, int G, int rank, uint32_t* state /*[3] device*/,
                            uint32_t* error_word, cudaStream_t stream);
 
 }  // namespace mp

@@ -368,3 +368,55 @@ class HostPipeline:
     def drain(self) -> None:
         self.s_out.synchronize()
         self.compute.synchronize()
+
+
+def capture_graph(fn, warmup: int = 1):
+    """Capture fn() (a sequence of layer forwards on static buffers) into a CUDA graph.
+
+    The forward is graph-safe: no host synchronisation, barrier epochs and
+    count-table parity live on the device, every tensor map is bound to a
+    static buffer.  Warm-up calls run eagerly first (attribute setup).
+    """
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    return g
+
+
+class MoEStack:
+    """Several MoE layers applied in sequence -- ModelSpec.num_layers > 1.
+
+    The reference walks a request through its layers strictly in order
+    (sim.py:500-505); each layer has its own placement, expert weights and
+    activation statistics (one B200MoELayer per layer).  Non-MoE compute
+    between layers is outside the path (modelled as a constant).
+    """
+
+    def __init__(self, layers: list[B200MoELayer]):
+        if not layers:
+            raise ValueError("a stack needs at least one layer")
+        self.layers = layers
+        d = layers[0].shape.d
+        if any(l.shape.d != d for l in layers):
+            raise ValueError("all layers of a stack share the hidden width")
+        self._bufs = {}
+
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        key = (x.shape[0], x.device)
+        if key not in self._bufs:
+            self._bufs[key] = [torch.empty_like(x), torch.empty_like(x)]
+        bufs = self._bufs[key]
+        cur = x
+        for i, layer in enumerate(self.layers):
+            dst = out if (i == len(self.layers) - 1 and out is not None) else bufs[i & 1]
+            cur = layer.forward(cur, dst)
+        return cur
+
+    __call__ = forward
+
+    def capture(self, x: torch.Tensor, out: torch.Tensor, warmup: int = 1):
+        """CUDA graph of the whole stack on static x / out buffers (replay with g.replay())."""
+        return capture_graph(lambda: self.forward(x, out), warmup)

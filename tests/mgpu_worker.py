@@ -73,9 +73,22 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed):
 
     route1 = route_table([frozenset(s) for s in sets], E, lat, bw, shape.d)
     assert np.array_equal(layer.route, route1)
-    check(route1, "placement A")
+    out_a = check(route1, "placement A").clone()
     # repeated forwards reuse the parity-double-buffered count tables
     check(route1, "placement A again")
+    # CUDA-graph replay across GPUs (device-side barrier epochs / count parity)
+    from paper_2508_12851_b200.layer import capture_graph
+    gout = torch.empty_like(x)
+    g = capture_graph(lambda: layer.forward(x, gout))
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    layer.check()
+    dist.barrier()
+    assert torch.equal(gout, out_a), "graph replay differs from eager forward"
+    assert np.array_equal(layer.read_counts(), orc.moe_layer_forward(
+        shape, xs, wg[:E], biases, route1, experts, shared, wg[E] if shape.shared_gate else None).counts)
+    del g
 
     # ---- migration A -> B: gather every GPU's slot map, pull added experts over NVLink
     slot_maps = [None] * G
