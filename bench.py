@@ -627,7 +627,8 @@ def main_shift(args):
     # remote penalty per token-unit: wire time of one remote invocation (activations out, results
     # back, comm_time's bandwidth term cost.py:148) at the measured peer bandwidth (probe copy below)
     bw_probe = measure_peer_copy(layer, world, rank) if world > 1 else 770e9
-    penalty = 2.0 * shape.d * 2 / bw_probe
+    from paper_2508_12851_b200.calibrate import remote_penalty_seconds
+    penalty = remote_penalty_seconds(shape.d, bw_probe)
     cluster = cluster_spec(shape, G, caps, link_bandwidth=bw_probe, load_bandwidth=bw_probe)
     candidate, stats_b = placement_from(counts_b)
     snapshot = mp.CostSnapshot(stats_b, penalty, 0.0, win_s)

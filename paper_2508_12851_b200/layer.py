@@ -267,6 +267,11 @@ class B200MoELayer:
         counts = self.gathered_counts(group).astype(float)
         return mp.ActivationStats.from_counts(counts[:, None, :], (self.shape.E,))
 
+    def trace_records(self, T: int, layer: int = 0, t: float = 0.0) -> list[dict]:
+        """The last forward's routing of this origin as reference trace records (cli.py:91-135)."""
+        from .trace import trace_records
+        return trace_records(self.idx[:T].cpu().numpy(), self.rank, layer, t)
+
     def reset_counts(self) -> None:
         self.hist.zero_()
 
