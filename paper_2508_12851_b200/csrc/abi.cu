@@ -84,7 +84,7 @@ struct mp_layer {
   CUtensorMap tm_recv, tm_w13, tm_h, tm_w2, tm_w13s, tm_hs, tm_w2s, tm_x;
   // B maps with 128-row boxes for the CTA-pair GEMM (each CTA loads half of N)
   CUtensorMap tm_w13_p, tm_w2_p, tm_w13s_p, tm_w2s_p;
-  int pair_routed = 0, pair_shared = 1;
+  int pair_routed = 0, pair_shared = 1, gemm_order = 0;
   const void* tm_x_ptr = nullptr;
   int tm_x_rows = -1;
 
@@ -303,6 +303,10 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   // CTA pairs (256-row tiles) when the average expert group is large
   L->pair_routed = int64_t(D.world) * D.max_tokens * D.top_k >= int64_t(512) * D.E ? 1 : 0;
   if (const char* env = getenv("MP_GEMM_PAIR")) L->pair_routed = L->pair_shared = atoi(env) ? 1 : 0;
+  // tile order (0 = group-major) -- n-block-major interleaves weight-bound small groups with
+  // compute-bound large ones but loses the L2 reuse of each group's token tiles (measured slower)
+  L->gemm_order = 0;
+  if (const char* env = getenv("MP_GEMM_ORDER")) L->gemm_order = atoi(env) ? 1 : 0;
   if (D.shared_f > 0) {
     if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
       return fail(r);
@@ -519,6 +523,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     gs.G = G;
     gs.E = E;
     gs.rank = rank;
+    gs.order = L->gemm_order;
     const int pr = L->pair_routed;
     MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
                                0, st, pr));

@@ -48,7 +48,10 @@ struct GemmSmemTail {
   uint32_t tmem_base;
   int n_groups;
   int total_tiles;
+  int order;      // 0: (group, n, m) -- 1: (n, group, m)
+  int total_mb;   // sum of m-blocks over groups
   int tile_prefix[gg::kMaxGroups + 1];
+  int mb_prefix[gg::kMaxGroups + 1];
   int g_arow[gg::kMaxGroups];
   int g_m[gg::kMaxGroups];
   int g_slot[gg::kMaxGroups];
@@ -110,27 +113,48 @@ MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
   }
   __syncthreads();
   if (tid == 0) {
-    int acc = 0;
+    int acc = 0, mb = 0;
     st.tile_prefix[0] = 0;
+    st.mb_prefix[0] = 0;
     for (int g = 0; g < st.n_groups; ++g) {
-      acc += ((st.g_m[g] + bm - 1) / bm) * n_blocks;
+      const int m_blocks = (st.g_m[g] + bm - 1) / bm;
+      acc += m_blocks * n_blocks;
+      mb += m_blocks;
       st.tile_prefix[g + 1] = acc;
+      st.mb_prefix[g + 1] = mb;
     }
     st.total_tiles = acc;
+    st.total_mb = mb;
+    st.order = gs.order;
   }
 }
 
-MP_DEV TileCoord decode_tile(const GemmSmemTail& s, int tile, int n_blocks) {
+// tile -> (group, n-block, m-block).  order 0 walks one group at a time (its
+// weight tiles are reused across its m-blocks while hot in L2); order 1 walks
+// n-blocks across all groups, so weight-bound small groups run concurrently
+// with compute-bound large ones.
+template <class Tail>
+MP_DEV TileCoord decode_any(const Tail& s, int tile, int n_blocks, int bm) {
+  TileCoord c;
+  if (s.order == 1) {
+    c.n_blk = tile / s.total_mb;
+    const int r = tile - c.n_blk * s.total_mb;
+    int g = 0;
+    while (s.mb_prefix[g + 1] <= r) ++g;
+    c.g = g;
+    c.m_blk = r - s.mb_prefix[g];
+    return c;
+  }
   int g = 0;
   while (s.tile_prefix[g + 1] <= tile) ++g;
   const int local = tile - s.tile_prefix[g];
-  const int m_blocks = (s.g_m[g] + gg::BM - 1) / gg::BM;
-  TileCoord c;
+  const int m_blocks = (s.g_m[g] + bm - 1) / bm;
   c.g = g;
   c.n_blk = local / m_blocks;
   c.m_blk = local - c.n_blk * m_blocks;
   return c;
 }
+
 
 // Epilogue of one 128-row x 256-column accumulator: this thread owns one row
 // (TMEM lane), reads 32 columns per tcgen05.ld, applies SwiGLU (GEMM1: columns
@@ -227,7 +251,7 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const TileCoord c = decode_tile(st, tile, n_blocks);
+        const TileCoord c = decode_any(st, tile, n_blocks, gg::BM);
         const int a_row = st.g_arow[c.g] + c.m_blk * gg::BM;
         const int b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * gg::BN;
         for (int kb = 0; kb < k_blocks; ++kb) {
@@ -282,7 +306,7 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const TileCoord c = decode_tile(st, tile, n_blocks);
+      const TileCoord c = decode_any(st, tile, n_blocks, gg::BM);
       const int row = c.m_blk * gg::BM + q * 32 + lane;
       const bool valid = row < st.g_m[c.g];
       const size_t orow = size_t(st.g_orow[c.g] + row);
@@ -335,7 +359,10 @@ struct Gemm2SmemTail {
   uint32_t tmem_base;
   int n_groups;
   int total_tiles;
+  int order;      // 0: (group, n, m) -- 1: (n, group, m)
+  int total_mb;   // sum of m-blocks over groups
   int tile_prefix[gg::kMaxGroups + 1];
+  int mb_prefix[gg::kMaxGroups + 1];
   int g_arow[gg::kMaxGroups];
   int g_m[gg::kMaxGroups];
   int g_slot[gg::kMaxGroups];
@@ -343,17 +370,6 @@ struct Gemm2SmemTail {
   int g_tmp[64];
 };
 
-MP_DEV TileCoord decode_tile2(const Gemm2SmemTail& s, int tile, int n_blocks) {
-  int g = 0;
-  while (s.tile_prefix[g + 1] <= tile) ++g;
-  const int local = tile - s.tile_prefix[g];
-  const int m_pairs = (s.g_m[g] + g2::BM - 1) / g2::BM;
-  TileCoord c;
-  c.g = g;
-  c.n_blk = local / m_pairs;
-  c.m_blk = local - c.n_blk * m_pairs;
-  return c;
-}
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -404,7 +420,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster_id; tile < total; tile += n_clusters) {
-        const TileCoord c = decode_tile2(st, tile, n_blocks);
+        const TileCoord c = decode_any(st, tile, n_blocks, g2::BM);
         const int a_row = st.g_arow[c.g] + c.m_blk * g2::BM + int(rank) * 128;
         const int b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * g2::BN + int(rank) * 128;
         for (int kb = 0; kb < k_blocks; ++kb) {
@@ -456,7 +472,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = cluster_id; tile < total; tile += n_clusters) {
-      const TileCoord c = decode_tile2(st, tile, n_blocks);
+      const TileCoord c = decode_any(st, tile, n_blocks, g2::BM);
       const int row = c.m_blk * g2::BM + int(rank) * 128 + q * 32 + lane;
       const bool valid = row < st.g_m[c.g];
       const size_t orow = size_t(st.g_orow[c.g] + row);
