@@ -123,10 +123,10 @@ def main():
 
     # case 2: DeepSeek-like routing (64 experts, top-6, shared experts), one GPU holding few experts
     shape = LayerShape("ds_small", d=256, f=256, E=64, k=6, score_mode=1, shared_f=512)
-    per = 64 // G
-    sets = [sorted(set(range(g * per, (g + 1) * per)) | {(g * per + per) % 64}) for g in range(G)]
-    sets2 = [sorted(set(range(g * per, (g + 1) * per)) | {(g * per + per + 1) % 64, (g * per + 2 * per + 5) % 64})
-             for g in range(G)]
+    per = -(-64 // G)
+    own = [set(range(g * per, min(64, (g + 1) * per))) for g in range(G)]
+    sets = [sorted(own[g] | {(g * per + per) % 64}) for g in range(G)]
+    sets2 = [sorted(own[g] | {(g * per + per + 1) % 64, (g * per + 2 * per + 5) % 64}) for g in range(G)]
     run_case(shape, G, rank, sets, sets2, [150] * G, seed=2)
 
     # case 3: Qwen-like (softmax-top4 + sigmoid-gated shared expert)

@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("G", [2, 3, 4])
 def test_multi_gpu_layer_matches_oracle(G):
     if torch.cuda.device_count() < G:
         pytest.skip(f"needs {G} GPUs, have {torch.cuda.device_count()}")
