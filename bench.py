@@ -71,6 +71,25 @@ def load_peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+def init_dist_quiet(dev):
+    """NCCL process group; keep stdout to the single JSON line (the NCCL version banner is
+    printed on the first communicator creation, so fd 1 is silenced until then)."""
+    import torch.distributed as dist
+    os.environ["NCCL_DEBUG"] = "WARN"
+    sys.stdout.flush()
+    saved = os.dup(1)
+    devnull = os.open(os.devnull, os.O_WRONLY)
+    os.dup2(devnull, 1)
+    try:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
+        os.close(devnull)
+
+
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
@@ -222,8 +241,7 @@ def main_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the single JSON line
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist_quiet(dev)
     shape = get_shape(args.config)
     T, G, seed = args.tokens, world, args.seed
 
@@ -555,8 +573,7 @@ def main_shift(args):
         raise SystemExit("the shift scenario needs >= 2 GPUs (with one GPU nothing is remote)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    os.environ["NCCL_DEBUG"] = "WARN"
-    dist.init_process_group("nccl", device_id=dev)
+    init_dist_quiet(dev)
     mp = import_moeplace()
     if mp is None:
         raise SystemExit("the shift scenario needs the reference solver (moeplace)")

@@ -119,7 +119,9 @@ typedef struct mp_layer_ptrs {
   int32_t* pos_row;  /* [max_tokens][k] row in the target's receive buffer       */
   void* recv;        /* [recv_cap][d] bf16 rows received for local experts       */
   void* h;           /* [recv_cap][f] bf16 SwiGLU activations                    */
-  void* y;           /* [recv_cap][d] bf16 expert outputs                        */
+  void* ret;         /* [max_tokens][k][d] bf16 this origin's expert outputs, in (token, slot)
+                        order, written back by the (local or peer) GEMM2 epilogues      */
+  int32_t* recv_src; /* [recv_cap] (origin rank << 24 | pair index) of each received row */
   uint32_t* hist;    /* [E] cumulative activation histogram (this origin)        */
   int32_t* counts;   /* [2][G][E] exchanged batch counts C[src][e] (parity halves) */
   float* shared_gate;/* [max_tokens] or NULL                                     */
@@ -150,8 +152,9 @@ int mp_layer_prepare_router(mp_layer* layer, void* stream);
 /* One MoE-layer forward of T tokens originating on this GPU -- replaces
  * `_dispatch_layer` (sim.py:441-463).  x, out: [T, d] bf16 device.  SPMD: all
  * G ranks must call it with their own T.  Kernels: router+histogram, count
- * exchange, layout, permute+dispatch (NVLink stores), shared expert, barrier,
- * grouped SwiGLU GEMMs (tcgen05), barrier, combine+return (NVLink loads). */
+ * exchange, permute+dispatch (NVLink stores), shared expert, barrier, grouped
+ * SwiGLU GEMMs (tcgen05; GEMM2's epilogue stores each row back to its origin
+ * GPU over NVLink), barrier, combine (local). */
 int mp_layer_forward(mp_layer* layer, const void* x, void* out, int T, void* stream);
 
 /* Same forward, recording MP_NUM_STAGE_EVENTS cudaEvent_t (created by the

@@ -54,7 +54,8 @@ class LayerPtrs(Structure):
     _fields_ = [
         ("w13_pool", c_void_p), ("w2_pool", c_void_p), ("wg", c_void_p), ("bias", c_void_p),
         ("w13_shared", c_void_p), ("w2_shared", c_void_p), ("idx", c_void_p), ("w", c_void_p),
-        ("pos_dst", c_void_p), ("pos_row", c_void_p), ("recv", c_void_p), ("h", c_void_p), ("y", c_void_p),
+        ("pos_dst", c_void_p), ("pos_row", c_void_p), ("recv", c_void_p), ("h", c_void_p), ("ret", c_void_p),
+        ("recv_src", c_void_p),
         ("hist", c_void_p), ("counts", c_void_p),
         ("shared_gate", c_void_p), ("recv_cap", c_int64), ("slot_bytes", c_int64),
     ]

@@ -61,10 +61,11 @@ struct mp_layer {
   size_t window_bytes = 0;
   uint8_t* scratch = nullptr;
   size_t scratch_bytes = 0;
-  size_t off_recv = 0, off_y = 0, off_counts = 0, off_flags = 0;
+  size_t off_recv = 0, off_ret = 0, off_src = 0, off_counts = 0, off_flags = 0;
 
   // pool / window views
-  __nv_bfloat16 *w13 = nullptr, *w2 = nullptr, *recv = nullptr, *y = nullptr;
+  __nv_bfloat16 *w13 = nullptr, *w2 = nullptr, *recv = nullptr, *ret = nullptr;
+  int32_t* recv_src = nullptr;
   int32_t* counts = nullptr;
   uint32_t* flags = nullptr;
   // scratch views
@@ -75,7 +76,7 @@ struct mp_layer {
           *batch_counts = nullptr, *route_d = nullptr,
           *slot_of_d = nullptr;
   uint32_t *hist = nullptr, *err = nullptr, *ticket = nullptr, *sync_state = nullptr;
-  void** ptr_arrays = nullptr;  // device: recv[8], y[8], flags[8], counts0[8], counts1[8]
+  void** ptr_arrays = nullptr;  // device: recv[8], ret[8], flags[8], counts0[8], counts1[8], recv_src[8]
 
   uint8_t* peer_window[8] = {};
   uint8_t* peer_pool[8] = {};
@@ -209,8 +210,10 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
     size_t off = 0;
     L->off_recv = off;
     off = align_up(off + size_t(L->recv_cap) * D.d * 2, 1024);
-    L->off_y = off;
-    off = align_up(off + size_t(L->recv_cap) * D.d * 2, 1024);
+    L->off_ret = off;
+    off = align_up(off + size_t(D.max_tokens) * D.top_k * D.d * 2, 1024);
+    L->off_src = off;
+    off = align_up(off + size_t(L->recv_cap) * 4, 1024);
     L->off_counts = off;
     off = align_up(off + size_t(2) * 8 * 64 * 4, 256);
     L->off_flags = off;
@@ -221,7 +224,8 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
     return fail(set_error(MP_E_CAPACITY, "cannot allocate the exchange window (%zu bytes): %s", L->window_bytes,
                           cudaGetErrorString(e)));
   L->recv = reinterpret_cast<__nv_bfloat16*>(L->window + L->off_recv);
-  L->y = reinterpret_cast<__nv_bfloat16*>(L->window + L->off_y);
+  L->ret = reinterpret_cast<__nv_bfloat16*>(L->window + L->off_ret);
+  L->recv_src = reinterpret_cast<int32_t*>(L->window + L->off_src);
   L->counts = reinterpret_cast<int32_t*>(L->window + L->off_counts);
   L->flags = reinterpret_cast<uint32_t*>(L->window + L->off_flags);
   if ((e = cudaMemset(L->window + L->off_counts, 0, L->window_bytes - L->off_counts)) != cudaSuccess)
@@ -251,7 +255,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       L->err = cv.take<uint32_t>(4);
       L->ticket = cv.take<uint32_t>(4);
       L->sync_state = cv.take<uint32_t>(4);
-      L->ptr_arrays = cv.take<void*>(5 * 8);
+      L->ptr_arrays = cv.take<void*>(6 * 8);
       if (D.shared_f > 0) {
         L->w13s = cv.take<__nv_bfloat16>(size_t(2) * D.shared_f * D.d);
         L->w2s = cv.take<__nv_bfloat16>(size_t(D.d) * D.shared_f);
@@ -273,9 +277,10 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
 
   // ---- own pointer arrays (peers filled by mp_layer_open_peers)
   {
-    void* host[5 * 8] = {};
+    void* host[6 * 8] = {};
     host[0 * 8 + L->rank] = L->recv;
-    host[1 * 8 + L->rank] = L->y;
+    host[1 * 8 + L->rank] = L->ret;
+    host[5 * 8 + L->rank] = L->recv_src;
     host[2 * 8 + L->rank] = L->flags;
     host[3 * 8 + L->rank] = L->counts;
     host[4 * 8 + L->rank] = L->counts + L->G * D.E;
@@ -353,7 +358,8 @@ int mp_layer_get_ptrs(mp_layer* L, mp_layer_ptrs* o) {
   o->pos_row = L->pos_row;
   o->recv = L->recv;
   o->h = L->h;
-  o->y = L->y;
+  o->ret = L->ret;
+  o->recv_src = L->recv_src;
   o->hist = L->hist;
   o->counts = L->counts;
   o->shared_gate = L->sgate;
@@ -378,7 +384,7 @@ int mp_layer_open_peers(mp_layer* L, const void* all_handles) {
   if (!L || !all_handles) return set_error(MP_E_ARG, "mp_layer_open_peers: null pointer");
   MP_CUDA(cudaSetDevice(L->desc.device));
   const uint8_t* h = static_cast<const uint8_t*>(all_handles);
-  void* host[5 * 8] = {};
+  void* host[6 * 8] = {};
   for (int p = 0; p < L->G; ++p) {
     uint8_t* win;
     if (p == L->rank) {
@@ -402,7 +408,8 @@ int mp_layer_open_peers(mp_layer* L, const void* all_handles) {
       win = L->peer_window[p];
     }
     host[0 * 8 + p] = win + L->off_recv;
-    host[1 * 8 + p] = win + L->off_y;
+    host[1 * 8 + p] = win + L->off_ret;
+    host[5 * 8 + p] = win + L->off_src;
     host[2 * 8 + p] = win + L->off_flags;
     host[3 * 8 + p] = win + L->off_counts;
     host[4 * 8 + p] = win + L->off_counts + size_t(L->G) * L->desc.E * 4;
@@ -455,7 +462,8 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int G = L->G, E = D.E, k = D.top_k, rank = L->rank;
   auto** recv_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 0 * 8);
-  auto** y_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 1 * 8);
+  auto** ret_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 1 * 8);
+  auto** src_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + 5 * 8);
   auto** flag_ptrs = reinterpret_cast<uint32_t**>(L->ptr_arrays + 2 * 8);
   auto** count_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + 3 * 8);  // [parity][peer]
   int launches = 0;
@@ -492,7 +500,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   MP_TRY(mark());  // 2 count exchange
   MP_TRY(mark());  // 3 (layout: folded into permute / GEMM prologues)
   MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, parity, L->blk_prefix,
-                        rank, G,
+                        src_ptrs, rank, G,
                         T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st));
   ++launches;
   MP_TRY(mark());  // 4 permute + dispatch
@@ -528,8 +536,9 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
                                0, st, pr));
     MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
-    MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->y, D.d, 0, 0,
-                               st, pr));
+    // GEMM2 epilogue returns every output row to its origin GPU (NVLink stores)
+    MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0, 0,
+                               st, pr, L->recv_src, ret_ptrs));
     launches += 2;
   } else {
     MP_TRY(mark());
@@ -540,7 +549,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     ++launches;
   }
   MP_TRY(mark());  // 9 return barrier
-  MP_TRY(launch_combine(y_ptrs, L->pos_dst, L->pos_row, L->w, T, D.d, k, D.shared_f > 0 ? L->ys : nullptr,
+  MP_TRY(launch_combine(L->ret, L->w, T, D.d, k, D.shared_f > 0 ? L->ys : nullptr,
                         D.shared_gate ? L->sgate : nullptr, static_cast<__nv_bfloat16*>(out), st));
   ++launches;
   MP_TRY(mark());  // 10 combine + return

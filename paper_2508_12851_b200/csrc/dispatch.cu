@@ -1,4 +1,4 @@
-// K2 permute+dispatch and K5 combine+return.
+// K2 permute+dispatch and K5 combine.
 //
 // Reference anchors:
 //   * target rule  `_choose_target` (reference pkg/src/moeplace/sim.py:433-439):
@@ -6,8 +6,9 @@
 //   * per-target grouping in `_dispatch_layer` (sim.py:446-457): here every
 //     (token, slot) pair is stably counting-sorted by (target GPU, expert);
 //   * remote payload accounting 2*tokens*d*bpe (sim.py:454, domain.py:193-194):
-//     the rows written to a peer's receive buffer here are exactly the
-//     reference's "remote invocations" at token granularity.
+//     the rows written to a peer's receive buffer here, and returned by the
+//     peer's GEMM2 epilogue, are exactly the reference's "remote invocations"
+//     at token granularity (payload out + result back).
 //
 // Receive-buffer layout on GPU D (identical formula on every rank, so no
 // per-row metadata crosses NVLink): rows grouped by expert id ascending; inside
@@ -35,8 +36,8 @@ template <int kVecPerLane>
 __global__ void __launch_bounds__(256)
     permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
                    const int32_t* __restrict__ route, const int32_t* __restrict__ counts_all,
-                   const uint32_t* __restrict__ parity, const int32_t* __restrict__ blk_prefix, int rank, int G,
-                   int T, int d, int E, int k,
+                   const uint32_t* __restrict__ parity, const int32_t* __restrict__ blk_prefix,
+                   int32_t* const* __restrict__ src_ptrs, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* __restrict__ recv_ptrs, int32_t* __restrict__ pos_dst,
                    int32_t* __restrict__ pos_row) {
   constexpr int kTok = 32;
@@ -78,6 +79,8 @@ __global__ void __launch_bounds__(256)
     s_row[tid] = row;
     pos_dst[size_t(t0) * k + tid] = dst;
     pos_row[size_t(t0) * k + tid] = row;
+    // where this row's expert output must return: (origin rank, pair index)
+    src_ptrs[dst][row] = int32_t((uint32_t(rank) << 24) | uint32_t(t0 * k + tid));
   }
   __syncthreads();
   const int warp = warp_id(), lane = lane_id();
@@ -102,7 +105,8 @@ __global__ void __launch_bounds__(256)
 }
 
 int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
-                   const uint32_t* parity, const int32_t* blk_prefix, int rank, int G, int T, int d, int E, int k,
+                   const uint32_t* parity, const int32_t* blk_prefix, int32_t* const* src_ptrs, int rank, int G,
+                   int T, int d, int E, int k,
                    __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream) {
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "permute: d=%d not a multiple of 8", d);
   if (k > 8) return set_error(MP_E_SHAPE, "permute: top_k=%d > 8", k);
@@ -111,7 +115,8 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   const int grid = (T + 31) / 32;
   const int vpl = (d / 8 + 31) / 32;
 #define MP_PERM_LAUNCH(N)                                                                                       \
-  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route, counts_all, parity, blk_prefix, rank, G, T, d, E, k,  \
+  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route, counts_all, parity, blk_prefix, src_ptrs, rank, G, T, d, \
+                                              E, k,                                                        \
                                               recv_ptrs,                                                   \
                                               pos_dst, pos_row)
   if (vpl <= 1) MP_PERM_LAUNCH(1);
@@ -126,33 +131,30 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "permute_kernel launch");
 }
 
-// ------------------------------------------------------------------ K5 combine + return
-// One warp per token.  out[t] = bf16( sum_{j<k} w[t,j] * y_{dst_j}[row_j] (+ g[t] * ysh[t]) )
-// accumulated in fp32 in ascending j (deterministic).  y rows that live on a
-// peer GPU are read straight over NVLink (the "return all-to-all").
+// ------------------------------------------------------------------ K5 combine
+// One warp per token.  The k expert outputs of token t were written back into
+// this GPU's return buffer by the (local or remote) GEMM2 epilogues, at rows
+// t*k .. t*k+k-1, so the combine is a local, fully coalesced read:
+// out[t] = bf16( sum_{j<k} w[t,j] * ret[t*k+j] (+ g[t] * ysh[t]) ), fp32, ascending j.
 template <int K>
 __global__ void __launch_bounds__(256)
-    combine_kernel(__nv_bfloat16* const* __restrict__ y_ptrs, const int32_t* __restrict__ pos_dst,
-                   const int32_t* __restrict__ pos_row, const float* __restrict__ w, int T, int d,
+    combine_kernel(const __nv_bfloat16* __restrict__ ret, const float* __restrict__ w, int T, int d,
                    const __nv_bfloat16* __restrict__ shared_y, const float* __restrict__ shared_gate,
                    __nv_bfloat16* __restrict__ out) {
   const int t = blockIdx.x * 8 + warp_id();
   if (t >= T) return;
   const int lane = lane_id();
-  const __nv_bfloat16* src[K];
+  const __nv_bfloat16* src = ret + size_t(t) * K * d;
   float wj[K];
 #pragma unroll
-  for (int j = 0; j < K; ++j) {
-    src[j] = y_ptrs[pos_dst[size_t(t) * K + j]] + size_t(pos_row[size_t(t) * K + j]) * d;
-    wj[j] = w[size_t(t) * K + j];
-  }
+  for (int j = 0; j < K; ++j) wj[j] = w[size_t(t) * K + j];
   const float g = shared_gate ? shared_gate[t] : 1.0f;
   const int nvec = d / 8;
 #pragma unroll 4
   for (int c = lane; c < nvec; c += 32) {
     uint4 v[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) v[j] = ld_v4(src[j] + 8 * c);
+    for (int j = 0; j < K; ++j) v[j] = ld_nc_v4(src + size_t(j) * d + 8 * c);
     float acc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.f;
@@ -183,16 +185,15 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-int launch_combine(__nv_bfloat16* const* y_ptrs, const int32_t* pos_dst, const int32_t* pos_row, const float* w,
-                   int T, int d, int k, const __nv_bfloat16* shared_y, const float* shared_gate,
-                   __nv_bfloat16* out, cudaStream_t stream) {
+int launch_combine(const __nv_bfloat16* ret, const float* w, int T, int d, int k, const __nv_bfloat16* shared_y,
+                   const float* shared_gate, __nv_bfloat16* out, cudaStream_t stream) {
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "combine: d=%d not a multiple of 8", d);
   if (k < 1 || k > 8) return set_error(MP_E_SHAPE, "combine: top_k=%d outside [1, 8]", k);
   if (T <= 0) return MP_OK;
   const int grid = (T + 7) / 8;
   switch (k) {
 #define MP_COMBINE_CASE(N) \
-  case N: combine_kernel<N><<<grid, 256, 0, stream>>>(y_ptrs, pos_dst, pos_row, w, T, d, shared_y, shared_gate, out); break;
+  case N: combine_kernel<N><<<grid, 256, 0, stream>>>(ret, w, T, d, shared_y, shared_gate, out); break;
     MP_COMBINE_CASE(1) MP_COMBINE_CASE(2) MP_COMBINE_CASE(3) MP_COMBINE_CASE(4)
     MP_COMBINE_CASE(5) MP_COMBINE_CASE(6) MP_COMBINE_CASE(7) MP_COMBINE_CASE(8)
 #undef MP_COMBINE_CASE

@@ -156,13 +156,24 @@ MP_DEV TileCoord decode_any(const Tail& s, int tile, int n_blocks, int bm) {
 }
 
 
+// Output row of the epilogue.  Plain mode: out + orow * out_ld.  Scatter mode
+// (GEMM2 of the layer): the row goes straight back to its origin GPU's return
+// buffer, at the origin's (token, slot) pair index -- recorded per receive row
+// by the permute kernel as (source rank << 24 | pair) -- so the return transfer
+// rides NVLink inside the GEMM, tile by tile.
+MP_DEV __nv_bfloat16* out_row_ptr(__nv_bfloat16* out, size_t orow, int out_ld, const int32_t* scatter_src,
+                                   __nv_bfloat16* const* scatter_ptrs, bool valid) {
+  if (scatter_src == nullptr || !valid) return out + orow * size_t(out_ld);
+  const uint32_t info = uint32_t(__ldg(scatter_src + orow));
+  return scatter_ptrs[info >> 24] + size_t(info & 0xFFFFFFu) * size_t(out_ld);
+}
+
 // Epilogue of one 128-row x 256-column accumulator: this thread owns one row
 // (TMEM lane), reads 32 columns per tcgen05.ld, applies SwiGLU (GEMM1: columns
 // [0,128) gate, [128,256) up) and writes bf16.
-MP_DEV void epilogue_store(uint32_t taddr, bool valid, __nv_bfloat16* __restrict__ out, size_t orow, int out_ld,
-                           int n_blk, int swiglu) {
+MP_DEV void epilogue_store(uint32_t taddr, bool valid, __nv_bfloat16* __restrict__ rowp, int n_blk, int swiglu) {
   if (swiglu) {
-    __nv_bfloat16* dst = out + orow * size_t(out_ld) + size_t(n_blk) * (gg::BN / 2);
+    __nv_bfloat16* dst = rowp + size_t(n_blk) * (gg::BN / 2);
 #pragma unroll 1
     for (int cc = 0; cc < gg::BN / 2; cc += 32) {
       uint32_t gv[32], uv[32];
@@ -186,7 +197,7 @@ MP_DEV void epilogue_store(uint32_t taddr, bool valid, __nv_bfloat16* __restrict
       }
     }
   } else {
-    __nv_bfloat16* dst = out + orow * size_t(out_ld) + size_t(n_blk) * gg::BN;
+    __nv_bfloat16* dst = rowp + size_t(n_blk) * gg::BN;
 #pragma unroll 1
     for (int cc = 0; cc < gg::BN; cc += 32) {
       uint32_t v[32];
@@ -209,7 +220,8 @@ MP_DEV void epilogue_store(uint32_t taddr, bool valid, __nv_bfloat16* __restrict
 __global__ void __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out,
-                        int out_ld, int swiglu) {
+                        int out_ld, int swiglu, const int32_t* __restrict__ scatter_src,
+                        __nv_bfloat16* const* __restrict__ scatter_ptrs) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -313,7 +325,8 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
       mbar_wait(&st.tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * gg::BN);
-      epilogue_store(taddr, valid, out, orow, out_ld, c.n_blk, swiglu);
+      epilogue_store(taddr, valid, out_row_ptr(out, orow, out_ld, scatter_src, scatter_ptrs, valid), c.n_blk,
+                     swiglu);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&st.tempty[acc]);
@@ -374,7 +387,8 @@ struct Gemm2SmemTail {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                             const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out, int out_ld,
-                            int swiglu) {
+                            int swiglu, const int32_t* __restrict__ scatter_src,
+                            __nv_bfloat16* const* __restrict__ scatter_ptrs) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -479,7 +493,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
       mbar_wait(&st.tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * g2::BN);
-      epilogue_store(taddr, valid, out, orow, out_ld, c.n_blk, swiglu);
+      epilogue_store(taddr, valid, out_row_ptr(out, orow, out_ld, scatter_src, scatter_ptrs, valid), c.n_blk,
+                     swiglu);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&st.tempty[acc], 0);
@@ -526,7 +541,8 @@ int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
 
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,
                         int b_slot_stride, int b_offset,
-                        __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream, int pair) {
+                        __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream, int pair,
+                        const int32_t* scatter_src, __nv_bfloat16* const* scatter_ptrs) {
   if (N % gg::BN != 0) return set_error(MP_E_SHAPE, "grouped GEMM N=%d not a multiple of %d", N, gg::BN);
   if (K % gg::BK != 0) return set_error(MP_E_SHAPE, "grouped GEMM K=%d not a multiple of %d", K, gg::BK);
   if (pair) {  // the B map must have 128-row boxes (each CTA loads half of N)
@@ -540,7 +556,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
     if (grid <= 0) grid = kNumSMs;
     grid &= ~1;
     grouped_gemm_2sm_kernel<<<grid, gg::kThreads, g2::kSmemBytes, stream>>>(
-        tmA, tmB, gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu);
+        tmA, tmB, gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_2sm_kernel launch");
     return MP_OK;
@@ -554,7 +570,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
   }
   if (grid <= 0) grid = kNumSMs;
   grouped_gemm_kernel<<<grid, gg::kThreads, gg::kSmemBytes, stream>>>(tmA, tmB, gs, N, K, b_slot_stride, b_offset,
-                                                                      out, out_ld, swiglu);
+                                                                      out, out_ld, swiglu, scatter_src, scatter_ptrs);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_kernel launch");
   return MP_OK;

@@ -26,7 +26,7 @@ int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16*
 
 // ---- K2 permute (+ dispatch through peer pointers)
 int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
-                   const uint32_t* parity, const int32_t* blk_prefix, int rank, int G, int T, int d, int E, int k,
+                   const uint32_t* parity, const int32_t* blk_prefix, int32_t* const* src_ptrs, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream);
 
 // ---- K3 grouped GEMM
@@ -47,12 +47,13 @@ int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,
                         int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream,
-                        int pair = 0);
+                        int pair = 0, const int32_t* scatter_src = nullptr,
+                        __nv_bfloat16* const* scatter_ptrs = nullptr);
 
-// ---- K5 combine (+ return through peer pointers)
-int launch_combine(__nv_bfloat16* const* y_ptrs /*[G] device array*/, const int32_t* pos_dst,
-                   const int32_t* pos_row, const float* w, int T, int d, int k, const __nv_bfloat16* shared_y,
-                   const float* shared_gate, __nv_bfloat16* out, cudaStream_t stream);
+// ---- K5 combine (the expert outputs are already back in this GPU's return buffer)
+int launch_combine(const __nv_bfloat16* ret /*[T][k][d]*/, const float* w, int T, int d, int k,
+                   const __nv_bfloat16* shared_y, const float* shared_gate, __nv_bfloat16* out,
+                   cudaStream_t stream);
 
 // ---- exchange / barrier over NVLink peer memory
 int launch_publish_barrier(uint32_t* const* flag_ptrs /*[G] device array, each -> flags[G]*/,

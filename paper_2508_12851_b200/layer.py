@@ -89,7 +89,8 @@ class B200MoELayer:
         self.pos_dst = _view(p.pos_dst, (T, k), torch.int32, dev)
         self.pos_row = _view(p.pos_row, (T, k), torch.int32, dev)
         self.recv = _view(p.recv, (p.recv_cap, d), torch.bfloat16, dev)
-        self.y = _view(p.y, (p.recv_cap, d), torch.bfloat16, dev)
+        self.ret = _view(p.ret, (T * k, d), torch.bfloat16, dev)          # expert outputs, (token, slot) order
+        self.recv_src = _view(p.recv_src, (p.recv_cap,), torch.int32, dev)
         self.hist = _view(p.hist, (E,), torch.int32, dev)
         self.w13_shared = _view(p.w13_shared, (2 * shape.shared_f, d), torch.bfloat16, dev) if shape.shared_f else None
         self.w2_shared = _view(p.w2_shared, (d, shape.shared_f), torch.bfloat16, dev) if shape.shared_f else None
