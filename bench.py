@@ -241,6 +241,8 @@ def main_b200(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
+        from paper_2508_12851_b200.numa import bind_to_gpu_node
+        bind_to_gpu_node(local)  # host buffers of the e2e path stay on the GPU's NUMA node
         init_dist_quiet(dev)
     shape = get_shape(args.config)
     T, G, seed = args.tokens, world, args.seed
