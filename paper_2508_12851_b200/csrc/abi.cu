@@ -86,6 +86,10 @@ struct mp_layer {
   // B maps with 128-row boxes for the CTA-pair GEMM (each CTA loads half of N)
   CUtensorMap tm_w13_p, tm_w2_p, tm_w13s_p, tm_w2s_p;
   int pair_routed = 0, pair_shared = 1, gemm_order = 0;
+  // small-group split: groups below split_m rows run on a side stream over small_grid SMs
+  int split_m = 0, small_grid = 24, pair_big = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const void* tm_x_ptr = nullptr;
   int tm_x_rows = -1;
 
@@ -311,6 +315,19 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   // tile order (0 = group-major) -- n-block-major interleaves weight-bound small groups with
   // compute-bound large ones but loses the L2 reuse of each group's token tiles (measured slower)
   L->gemm_order = 0;
+  // many small expert groups (Qwen / DeepSeek): weight-bound small groups run concurrently
+  // with the compute-bound large ones on a disjoint set of SMs
+  L->split_m = D.E >= 16 ? 256 : 0;
+  if (const char* env = getenv("MP_GEMM_SPLIT_M")) L->split_m = atoi(env);
+  if (const char* env = getenv("MP_GEMM_SMALL_GRID")) L->small_grid = std::max(2, atoi(env)) & ~1;
+  if (const char* env = getenv("MP_GEMM_PAIR_BIG")) L->pair_big = atoi(env);
+  if (L->split_m > 0) {
+    if ((e = cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking)) != cudaSuccess)
+      return fail(set_cuda_error(e, "cudaStreamCreate(side)"));
+    if ((e = cudaEventCreateWithFlags(&L->ev_fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&L->ev_join, cudaEventDisableTiming)) != cudaSuccess)
+      return fail(set_cuda_error(e, "cudaEventCreate(split)"));
+  }
   if (const char* env = getenv("MP_GEMM_ORDER")) L->gemm_order = atoi(env) ? 1 : 0;
   if (D.shared_f > 0) {
     if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
@@ -336,6 +353,9 @@ int mp_layer_destroy(mp_layer* L) {
     if (L->peer_window[p]) cudaIpcCloseMemHandle(L->peer_window[p]);
     if (L->peer_pool[p]) cudaIpcCloseMemHandle(L->peer_pool[p]);
   }
+  if (L->ev_fork) cudaEventDestroy(L->ev_fork);
+  if (L->ev_join) cudaEventDestroy(L->ev_join);
+  if (L->side) cudaStreamDestroy(L->side);
   if (L->scratch) cudaFree(L->scratch);
   if (L->window) cudaFree(L->window);
   if (L->pool) cudaFree(L->pool);
@@ -532,13 +552,31 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     gs.E = E;
     gs.rank = rank;
     gs.order = L->gemm_order;
-    const int pr = L->pair_routed;
+    int pr = L->pair_routed;
+    if (L->split_m > 0) {
+      // fork: small groups (weight-bound) on the side stream over small_grid SMs, large
+      // groups (compute-bound) on the main stream over the rest, then join
+      GroupSpec gsmall = gs;
+      gsmall.m_hi = L->split_m;
+      gs.m_lo = L->split_m;
+      MP_CUDA(cudaEventRecord(L->ev_fork, st));
+      MP_CUDA(cudaStreamWaitEvent(L->side, L->ev_fork, 0));
+      MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, gsmall, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
+                                 L->small_grid, L->side, 0));
+      MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, gsmall, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
+                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs));
+      MP_CUDA(cudaEventRecord(L->ev_join, L->side));
+      launches += 2;
+    }
+    const int big_grid = L->split_m > 0 ? kNumSMs - L->small_grid : 0;
+    if (L->split_m >= 512 && L->pair_big) pr = 1;  // large groups only: 256-row CTA-pair tiles
     MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                               0, st, pr));
+                               big_grid, st, pr));
     MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
     // GEMM2 epilogue returns every output row to its origin GPU (NVLink stores)
-    MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0, 0,
-                               st, pr, L->recv_src, ret_ptrs));
+    MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
+                               big_grid, st, pr, L->recv_src, ret_ptrs));
+    if (L->split_m > 0) MP_CUDA(cudaStreamWaitEvent(st, L->ev_join, 0));
     launches += 2;
   } else {
     MP_TRY(mark());

@@ -82,7 +82,7 @@ MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
       int ng = 0, row = 0;
       for (int e = 0; e < gs.E; ++e) {
         const int m = st.g_tmp[e];
-        if (m > 0) {
+        if (m > 0 && m >= gs.m_lo && m < gs.m_hi) {
           st.g_arow[ng] = row;
           st.g_m[ng] = m;
           st.g_slot[ng] = gs.slot_of[e];

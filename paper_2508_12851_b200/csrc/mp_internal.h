@@ -42,6 +42,7 @@ struct GroupSpec {
   int single_m = 0;                   // mode 2: one group {0, single_m, slot 0, 0}
   int mode = 0;
   int order = 0;                      // tile order: 0 group-major, 1 n-block-major
+  int m_lo = 0, m_hi = 1 << 30;       // mode 1: only groups with m_lo <= m < m_hi
 };
 int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,
