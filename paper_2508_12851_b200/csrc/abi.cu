@@ -87,7 +87,7 @@ struct mp_layer {
   CUtensorMap tm_w13_p, tm_w2_p, tm_w13s_p, tm_w2s_p;
   int pair_routed = 0, pair_shared = 1, gemm_order = 0;
   // small-group split: groups below split_m rows run on a side stream over small_grid SMs
-  int split_m = 0, small_grid = 24, pair_big = 0;
+  int split_m = 0, small_grid = 24;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const void* tm_x_ptr = nullptr;
@@ -311,7 +311,6 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   }
   // CTA pairs (256-row tiles) when the average expert group is large
   L->pair_routed = int64_t(D.world) * D.max_tokens * D.top_k >= int64_t(512) * D.E ? 1 : 0;
-  if (const char* env = getenv("MP_GEMM_PAIR")) L->pair_routed = L->pair_shared = atoi(env) ? 1 : 0;
   // tile order (0 = group-major) -- n-block-major interleaves weight-bound small groups with
   // compute-bound large ones but loses the L2 reuse of each group's token tiles (measured slower)
   L->gemm_order = 0;
@@ -320,7 +319,9 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   L->split_m = D.E >= 16 ? 256 : 0;
   if (const char* env = getenv("MP_GEMM_SPLIT_M")) L->split_m = atoi(env);
   if (const char* env = getenv("MP_GEMM_SMALL_GRID")) L->small_grid = std::max(2, atoi(env)) & ~1;
-  if (const char* env = getenv("MP_GEMM_PAIR_BIG")) L->pair_big = atoi(env);
+  // with the small groups split off, the remaining (>= split_m rows) groups run on CTA pairs
+  if (L->split_m >= 256) L->pair_routed = 1;
+  if (const char* env = getenv("MP_GEMM_PAIR")) L->pair_routed = L->pair_shared = atoi(env) ? 1 : 0;
   if (L->split_m > 0) {
     if ((e = cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking)) != cudaSuccess)
       return fail(set_cuda_error(e, "cudaStreamCreate(side)"));
@@ -552,7 +553,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     gs.E = E;
     gs.rank = rank;
     gs.order = L->gemm_order;
-    int pr = L->pair_routed;
+    const int pr = L->pair_routed;
     if (L->split_m > 0) {
       // fork: small groups (weight-bound) on the side stream over small_grid SMs, large
       // groups (compute-bound) on the main stream over the rest, then join
@@ -569,7 +570,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       launches += 2;
     }
     const int big_grid = L->split_m > 0 ? kNumSMs - L->small_grid : 0;
-    if (L->split_m >= 512 && L->pair_big) pr = 1;  // large groups only: 256-row CTA-pair tiles
+
     MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
                                big_grid, st, pr));
     MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
