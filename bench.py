@@ -175,7 +175,7 @@ def build_placement_sets(shape, G, counts, strategy, seed):
     return gpu_expert_sets(placement, 0), caps, f"moeplace.build_placement({strategy!r})"
 
 
-def uniform_sets(shape, G, caps):
+def uniform_sets(shape, G):
     """place_uniform's round-robin partition (reference placement.py:407-422), for the naive comparison."""
     sets = [[] for _ in range(G)]
     for e in range(shape.E):
@@ -194,7 +194,7 @@ def cpu_layer_sample(shape, T_cpu, seed, weights_cpu, wg_np, bias_np):
     orc.moe_layer_forward(shape, [x], wg_np[:shape.E], [bias_np], route, weights_cpu["experts"], shared, wsg)
 
 
-def cpu_weights(shape, seed, wg_gpu=None, expert_src=None):
+def cpu_weights(shape, seed, expert_src):
     """fp32 host copies of the expert weights (the same values the GPU holds)."""
     import torch
     from paper_2508_12851_b200 import workload as wl
@@ -399,7 +399,7 @@ def main_b200(args):
 
     # naive placement accounting on the same counts (counts do not depend on placement)
     lat, bw = uniform_links(G)
-    naive_route = route_table([frozenset(s) for s in uniform_sets(shape, G, caps)], shape.E, lat, bw, shape.d)
+    naive_route = route_table([frozenset(s) for s in uniform_sets(shape, G)], shape.E, lat, bw, shape.d)
     acc_naive = dispatch_accounting(counts_last, naive_route, shape.d)
 
     # ---- roofline of the dominant kernel: grouped_gemm_kernel (GEMM1 SwiGLU + GEMM2), every GPU;
@@ -428,7 +428,7 @@ def main_b200(args):
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        wcpu = cpu_weights(shape, seed, wg, expert_src)
+        wcpu = cpu_weights(shape, seed, expert_src)
         wg_np = wg.float().cpu().numpy()
         rate, reps, el, thr = time_cpu_baseline(shape, seed, args.cpu_tokens, args.cpu_seconds, wcpu, wg_np,
                                                 bias.numpy())

@@ -8,7 +8,7 @@ exception types (reference pkg/src/moeplace/domain.py:32-37, cost.py:34-35).
 from __future__ import annotations
 
 import ctypes
-from ctypes import POINTER, Structure, c_int, c_int32, c_int64, c_uint32, c_float, c_void_p, c_char_p
+from ctypes import POINTER, Structure, c_char_p, c_int, c_int32, c_int64, c_void_p
 from pathlib import Path
 
 from .errors import DimensionMismatch, InfeasibleError, UnplacedExpertError

@@ -93,7 +93,6 @@ struct mp_layer {
   const void* tm_x_ptr = nullptr;
   int tm_x_rows = -1;
 
-  uint64_t fwd_count = 0;
   int last_launches = 0;
 };
 
@@ -593,7 +592,6 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   ++launches;
   MP_TRY(mark());  // 10 combine + return
   L->last_launches = launches;
-  ++L->fwd_count;
   return MP_OK;
 }
 

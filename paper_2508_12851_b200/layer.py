@@ -30,7 +30,7 @@ import torch
 from . import _lib
 from .errors import InfeasibleError
 from .migration import plan_pulls
-from .routing import dispatch_accounting, gpu_expert_sets, route_table_for, server_expert_sets, route_table
+from .routing import dispatch_accounting, gpu_expert_sets, route_table, route_table_for
 from .shapes import LayerShape
 
 

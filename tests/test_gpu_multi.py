@@ -1,6 +1,5 @@
 """Multi-GPU parity (G = 2 / 4): one torchrun process per GPU running tests/mgpu_worker.py."""
 
-import os
 import socket
 import subprocess
 import sys
