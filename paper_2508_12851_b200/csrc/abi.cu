@@ -29,6 +29,16 @@ int set_error(int code, const char* fmt, ...) {
   return code;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    // measured: within noise on Mixtral, slower with the concurrent small-group chain
+    // (Qwen / DeepSeek) -- opt in with MP_PDL=1
+    const char* env = getenv("MP_PDL");
+    return env != nullptr && atoi(env) != 0;
+  }();
+  return on;
+}
+
 int set_cuda_error(cudaError_t e, const char* what) {
   return set_error(MP_E_CUDA, "%s: %s (%d)", what, cudaGetErrorString(e), int(e));
 }
@@ -561,21 +571,23 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       gs.m_lo = L->split_m;
       MP_CUDA(cudaEventRecord(L->ev_fork, st));
       MP_CUDA(cudaStreamWaitEvent(L->side, L->ev_fork, 0));
+      // (no PDL on the split chains: early-scheduled CTAs would contend for the other chain's SMs)
       MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, gsmall, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                                 L->small_grid, L->side, 0));
+                                 L->small_grid, L->side, 0, nullptr, nullptr, false));
       MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, gsmall, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs));
+                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs, false));
       MP_CUDA(cudaEventRecord(L->ev_join, L->side));
       launches += 2;
     }
     const int big_grid = L->split_m > 0 ? kNumSMs - L->small_grid : 0;
 
+    const bool pdl = L->split_m == 0;
     MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                               big_grid, st, pr));
+                               big_grid, st, pr, nullptr, nullptr, pdl));
     MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
     // GEMM2 epilogue returns every output row to its origin GPU (NVLink stores)
     MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                               big_grid, st, pr, L->recv_src, ret_ptrs));
+                               big_grid, st, pr, L->recv_src, ret_ptrs, pdl));
     if (L->split_m > 0) MP_CUDA(cudaStreamWaitEvent(st, L->ev_join, 0));
     launches += 2;
   } else {

@@ -251,6 +251,11 @@ MP_DEV void st_v4(void* p, uint4 v) {
                : "memory");
 }
 
+// Programmatic dependent launch: let the next kernel in the stream be scheduled
+// now / wait until the previous kernel's memory is visible.
+MP_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+MP_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 MP_DEV int warp_id() { return threadIdx.x >> 5; }
 MP_DEV int lane_id() { return threadIdx.x & 31; }
 

@@ -51,6 +51,8 @@ __global__ void __launch_bounds__(256)
   const int nt = min(kTok, T - t0);
   const int np = nt * k;
   const int tid = threadIdx.x;
+  griddep_launch_dependents();
+  griddep_wait();
   if (parity != nullptr) counts_all += size_t(*parity) * G * E;
   for (int i = tid; i < G * E; i += blockDim.x) {
     C[i / E][i % E] = counts_all[i];
@@ -114,11 +116,10 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   if (T <= 0) return MP_OK;
   const int grid = (T + 31) / 32;
   const int vpl = (d / 8 + 31) / 32;
-#define MP_PERM_LAUNCH(N)                                                                                       \
-  permute_kernel<N><<<grid, 256, 0, stream>>>(x, idx, route, counts_all, parity, blk_prefix, src_ptrs, rank, G, T, d, \
-                                              E, k,                                                        \
-                                              recv_ptrs,                                                   \
-                                              pos_dst, pos_row)
+  cudaError_t e;
+#define MP_PERM_LAUNCH(N)                                                                                    \
+  e = launch_pdl(permute_kernel<N>, dim3(grid), dim3(256), 0, stream, x, idx, route, counts_all, parity, blk_prefix, \
+                 src_ptrs, rank, G, T, d, E, k, recv_ptrs, pos_dst, pos_row)
   if (vpl <= 1) MP_PERM_LAUNCH(1);
   else if (vpl <= 2) MP_PERM_LAUNCH(2);
   else if (vpl <= 4) MP_PERM_LAUNCH(4);
@@ -127,7 +128,7 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   else if (vpl <= 32) MP_PERM_LAUNCH(32);
   else return set_error(MP_E_SHAPE, "permute: d=%d too large", d);
 #undef MP_PERM_LAUNCH
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "permute_kernel launch");
 }
 
@@ -141,6 +142,8 @@ __global__ void __launch_bounds__(256)
     combine_kernel(const __nv_bfloat16* __restrict__ ret, const float* __restrict__ w, int T, int d,
                    const __nv_bfloat16* __restrict__ shared_y, const float* __restrict__ shared_gate,
                    __nv_bfloat16* __restrict__ out) {
+  griddep_launch_dependents();
+  griddep_wait();
   const int t = blockIdx.x * 8 + warp_id();
   if (t >= T) return;
   const int lane = lane_id();
@@ -191,14 +194,15 @@ int launch_combine(const __nv_bfloat16* ret, const float* w, int T, int d, int k
   if (k < 1 || k > 8) return set_error(MP_E_SHAPE, "combine: top_k=%d outside [1, 8]", k);
   if (T <= 0) return MP_OK;
   const int grid = (T + 7) / 8;
+  cudaError_t e = cudaSuccess;
   switch (k) {
 #define MP_COMBINE_CASE(N) \
-  case N: combine_kernel<N><<<grid, 256, 0, stream>>>(ret, w, T, d, shared_y, shared_gate, out); break;
+  case N: e = launch_pdl(combine_kernel<N>, dim3(grid), dim3(256), 0, stream, ret, w, T, d, shared_y, shared_gate, out); break;
     MP_COMBINE_CASE(1) MP_COMBINE_CASE(2) MP_COMBINE_CASE(3) MP_COMBINE_CASE(4)
     MP_COMBINE_CASE(5) MP_COMBINE_CASE(6) MP_COMBINE_CASE(7) MP_COMBINE_CASE(8)
 #undef MP_COMBINE_CASE
   }
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "combine_kernel launch");
 }
 

@@ -28,6 +28,8 @@ __global__ void __launch_bounds__(256)
                            uint32_t* __restrict__ state, uint32_t* __restrict__ error_word) {
   __shared__ uint32_t s_epoch, s_par, s_fwd;
   const int tid = threadIdx.x;
+  griddep_launch_dependents();
+  griddep_wait();
   if (tid == 0) {
     s_epoch = state[0] + 1;
     s_fwd = state[1];
@@ -71,8 +73,9 @@ __global__ void __launch_bounds__(256)
 
 int launch_publish_barrier(uint32_t* const* flag_ptrs, int32_t* const* count_ptrs, const int32_t* my_counts, int E,
                            int G, int rank, uint32_t* state, uint32_t* error_word, cudaStream_t stream) {
-  publish_barrier_kernel<<<1, 256, 0, stream>>>(flag_ptrs, count_ptrs, my_counts, E, G, rank, state, error_word);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(publish_barrier_kernel, dim3(1), dim3(256), 0, stream, flag_ptrs, count_ptrs, my_counts, E,
+                             G, rank, state, error_word);
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "publish_barrier_kernel launch");
 }
 

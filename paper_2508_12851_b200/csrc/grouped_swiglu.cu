@@ -233,8 +233,9 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
   const int n_blocks = N / gg::BN;
   const int k_blocks = K / gg::BK;
 
-  // ---- prologue: group table -> smem, barriers, TMEM
-  load_groups(st, gs, gg::BM, n_blocks);
+  // ---- prologue: barriers, TMEM and descriptor prefetch overlap the previous
+  // kernel's tail (PDL); the group table needs its results, so it comes after
+  griddep_launch_dependents();
   if (threadIdx.x == 0) {
     for (int i = 0; i < gg::kStages; ++i) {
       mbar_init(&st.full[i], 1);
@@ -251,6 +252,8 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
     tma_prefetch_desc(&tmB);
   }
   if (warp == 2) tmem_alloc<gg::kTmemCols>(&st.tmem_base);
+  griddep_wait();
+  load_groups(st, gs, gg::BM, n_blocks);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -404,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
   const int n_blocks = N / g2::BN;
   const int k_blocks = K / g2::BK;
 
-  load_groups(st, gs, g2::BM, n_blocks);
+  griddep_launch_dependents();
   if (threadIdx.x == 0) {
     for (int i = 0; i < g2::kStages; ++i) {
       mbar_init(&st.full[i], 1);
@@ -421,6 +424,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
     tma_prefetch_desc(&tmB);
   }
   if (warp == 2) tmem_alloc_2sm<gg::kTmemCols>(&st.tmem_base);
+  griddep_wait();
+  load_groups(st, gs, g2::BM, n_blocks);
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // the peer's barriers are initialised before any remote arrive / TMA
@@ -542,7 +547,7 @@ int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,
                         int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream, int pair,
-                        const int32_t* scatter_src, __nv_bfloat16* const* scatter_ptrs) {
+                        const int32_t* scatter_src, __nv_bfloat16* const* scatter_ptrs, bool pdl) {
   if (N % gg::BN != 0) return set_error(MP_E_SHAPE, "grouped GEMM N=%d not a multiple of %d", N, gg::BN);
   if (K % gg::BK != 0) return set_error(MP_E_SHAPE, "grouped GEMM K=%d not a multiple of %d", K, gg::BK);
   if (pair) {  // the B map must have 128-row boxes (each CTA loads half of N)
@@ -555,9 +560,10 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
     }
     if (grid <= 0) grid = kNumSMs;
     grid &= ~1;
-    grouped_gemm_2sm_kernel<<<grid, gg::kThreads, g2::kSmemBytes, stream>>>(
-        tmA, tmB, gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl_if(pdl, grouped_gemm_2sm_kernel, dim3(grid), dim3(gg::kThreads), g2::kSmemBytes, stream, tmA,
+                               tmB, gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src,
+                               scatter_ptrs);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_2sm_kernel launch");
     return MP_OK;
   }
@@ -569,9 +575,9 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
     attr_set = true;
   }
   if (grid <= 0) grid = kNumSMs;
-  grouped_gemm_kernel<<<grid, gg::kThreads, gg::kSmemBytes, stream>>>(tmA, tmB, gs, N, K, b_slot_stride, b_offset,
-                                                                      out, out_ld, swiglu, scatter_src, scatter_ptrs);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl_if(pdl, grouped_gemm_kernel, dim3(grid), dim3(gg::kThreads), gg::kSmemBytes, stream, tmA, tmB,
+                             gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_kernel launch");
   return MP_OK;
 }

@@ -11,6 +11,31 @@
 
 namespace mp {
 
+// Kernel launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its predecessor drains; every kernel calls griddep_wait()
+// before touching memory its predecessor produces.  Off by default; MP_PDL=1 enables.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  return launch_pdl_if(true, kernel, grid, block, smem, stream, static_cast<Args&&>(args)...);
+}
+
 // Error state (thread-local, read through mp_last_error).
 int set_error(int code, const char* fmt, ...);
 int set_cuda_error(cudaError_t e, const char* what);
@@ -49,7 +74,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
                         int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream,
                         int pair = 0, const int32_t* scatter_src = nullptr,
-                        __nv_bfloat16* const* scatter_ptrs = nullptr);
+                        __nv_bfloat16* const* scatter_ptrs = nullptr, bool pdl = true);
 
 // ---- K5 combine (the expert outputs are already back in this GPU's return buffer)
 int launch_combine(const __nv_bfloat16* ret /*[T][k][d]*/, const float* w, int T, int d, int k,

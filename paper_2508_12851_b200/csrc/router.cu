@@ -89,6 +89,8 @@ __global__ void __launch_bounds__(kWarps * 32, MP_ROUTER_MIN_BLOCKS)
   __shared__ int cnt_s[rt::kMaxE];
   extern __shared__ int bc[];  // [nb][E] block counts staged by the last CTA (dynamic smem)
 
+  griddep_launch_dependents();
+  griddep_wait();
   const int E_tot = E + has_gate;
   const int E_pad = router_e_pad(E_tot);
   const int t0 = blockIdx.x * rt::kTokens;
@@ -295,10 +297,10 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
     if (ea != cudaSuccess) return set_cuda_error(ea, "cudaFuncSetAttribute(router)");
     smem_set = smem;
   }
-  router_kernel<<<grid, kWarps * 32, smem, stream>>>(x, wg_packed, bias, T, d, E, has_gate ? 1 : 0, k, score_mode, renorm,
-                                                  idx, w, shared_gate, hist, blk_counts, batch_counts, ticket,
-                                                  blk_prefix);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(router_kernel, dim3(grid), dim3(kWarps * 32), smem, stream, x, wg_packed, bias, T, d, E,
+                             has_gate ? 1 : 0, k, score_mode, renorm, idx, w, shared_gate, hist, blk_counts,
+                             batch_counts, ticket, blk_prefix);
+  if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_kernel launch");
 }
 
