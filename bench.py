@@ -145,6 +145,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def stage_roofline(shape, T, rows, stage_ms, hbm_gbs):
+    """Algorithmic HBM bytes of the memory-bound stages over their diagnostic-pass
+    time (event-bounded, so launch gaps are included: a lower bound on the kernel's own rate)."""
+    d, k = shape.d, shape.k
+    algo = {
+        "router": T * d * 2 + T * k * 8,                           # x once + idx/w out
+        "permute_dispatch": T * d * 2 + T * k * d * 2 + T * k * 8,  # x once, k row copies, positions
+        "combine_return": T * k * d * 2 + T * k * 4 + T * d * 2 + (T * d * 2 if shape.shared_f else 0),
+    }
+    out = {}
+    for name, b in algo.items():
+        ms = stage_ms.get(name, 0.0)
+        gbs = b / (ms * 1e-3) / 1e9 if ms > 0 else None
+        out[name] = {"bytes": b, "ms": ms, "GB/s": gbs, "frac_hbm": gbs / hbm_gbs if gbs else None}
+    return out
+
+
 # ----------------------------------------------------------------------------- placement
 def build_placement_sets(shape, G, counts, strategy, seed):
     """Per-GPU expert lists from the reference placement solver (build_placement,
@@ -466,6 +483,8 @@ def main_b200(args):
             "recv_rows_per_gpu": rows_list,
         },
         "stages_ms": {name: float(v) for name, v in zip(_lib.STAGES, stage_t.tolist()) if name != "unused"},
+        "stage_roofline": stage_roofline(shape, T, rows_list[hot], dict(zip(_lib.STAGES, stage_t.tolist())),
+                                         float(peaks.get("hbm_gbs"))),
         "stages_note": "per-stage means from a diagnostic pass with events at every boundary (max over ranks); "
                        "the timed region records only the K3 boundaries",
         "roofline": {"bound": "tensor", "kernel": f"grouped_gemm_kernel (GEMM1+SwiGLU, GEMM2), rank {hot} "
