@@ -334,7 +334,7 @@ def main_b200(args):
         return rows
 
     g0, g1, g2 = _lib.GEMM_START, _lib.GEMM1_END, _lib.GEMM_END
-    evs = make_events(K, {0, g0, g1, g2, NS - 1})
+    evs = make_events(K, {0, g0, g1, g2, _lib.MAIN_STAGE_EVENTS - 1})
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
@@ -351,7 +351,7 @@ def main_b200(args):
     clocks = sampler.stop()
     layer.check()
     t_ms = start.elapsed_time(end)
-    step_ms = [evs[i][0].elapsed_time(evs[i][NS - 1]) for i in range(K)]
+    step_ms = [evs[i][0].elapsed_time(evs[i][_lib.MAIN_STAGE_EVENTS - 1]) for i in range(K)]
     gemm1_ms = np.array([evs[i][g0].elapsed_time(evs[i][g1]) for i in range(K)])
     gemm2_ms = np.array([evs[i][g1].elapsed_time(evs[i][g2]) for i in range(K)])
 
@@ -364,8 +364,15 @@ def main_b200(args):
         layer.forward(xs[i % N_ROTATE], out, events=dev_[i])
     torch.cuda.synchronize()
     barrier()
-    stage_ms = np.array([[dev_[i][j].elapsed_time(dev_[i][j + 1]) for j in range(NS - 1)] for i in range(n_diag)])
+    NM = _lib.MAIN_STAGE_EVENTS
+    stage_ms = np.array([[dev_[i][j].elapsed_time(dev_[i][j + 1]) for j in range(NM - 1)] for i in range(n_diag)])
+    side_ms = None
+    if layer.exec_plan()["split_m"] > 0:
+        # the small-group chain on the side stream: its span and its offset from GEMM start
+        side_ms = [float(np.mean([dev_[i][NM].elapsed_time(dev_[i][NM + 1]) for i in range(n_diag)])),
+                   float(np.mean([dev_[i][_lib.GEMM_START].elapsed_time(dev_[i][NM + 1]) for i in range(n_diag)]))]
     launches = layer.last_launches() * K
+    exec_plan = layer.exec_plan()
     acc_ours = layer.dispatch_accounting()
     counts_last = layer.read_counts()
     recv_rows = int(np.sum([counts_last[s, e] for s in range(G) for e in range(shape.E) if layer.route[s, e] == rank]))
@@ -422,9 +429,13 @@ def main_b200(args):
     # ---- roofline of the dominant kernel: grouped_gemm_kernel (GEMM1 SwiGLU + GEMM2), every GPU;
     # the headline figure is the GPU with the most routed rows (it sets the step time)
     peaks, peaks_src = load_peaks()
-    per_rank_tf = [2.0 * r * 3 * shape.d * shape.f / (ms * 1e-3) / 1e12 if ms > 0 else 0.0 for r, ms in per_rank]
+    # algorithmic: 6*d*f per routed (token, expert) pair, plus 6*d*f_shared per token when the
+    # shared expert rides in the same launches (fused plan)
+    shared_flops = 2.0 * T * 3 * shape.d * shape.shared_f if exec_plan["fuse_shared"] else 0.0
+    per_rank_tf = [(2.0 * r * 3 * shape.d * shape.f + shared_flops) / (ms * 1e-3) / 1e12 if ms > 0 else 0.0
+                   for r, ms in per_rank]
     hot = int(np.argmax(rows_list))
-    flops = 2.0 * rows_list[hot] * 3 * shape.d * shape.f  # algorithmic: 6*d*f per routed (token, expert) pair
+    flops = 2.0 * rows_list[hot] * 3 * shape.d * shape.f + shared_flops
     achieved_tflops = per_rank_tf[hot]
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
     traffic = None
@@ -473,7 +484,7 @@ def main_b200(args):
         "config": {"workload": f"{shape.name} MoE layer, {T} tokens/GPU, placement {solver}",
                    "model": shape.name, "d": shape.d, "ffn": shape.f, "experts": shape.E, "top_k": shape.k,
                    "shared_ffn": shape.shared_f, "tokens_per_gpu": T, "global_batch": G * T,
-                   "slot_caps": caps, "parallelism": f"ep{G}+dp{G}",
+                   "slot_caps": caps, "parallelism": f"ep{G}+dp{G}", "k3_plan": exec_plan,
                    "l2": f"{N_ROTATE} rotating input batches ({N_ROTATE * T * shape.d * 2 / 2**20:.0f} MiB) + "
                          f"{sum(len(s) for s in sets) * shape.expert_bytes / 2**30:.2f} GiB resident expert weights "
                          "streamed per step exceed the 126 MB L2"},
@@ -485,10 +496,14 @@ def main_b200(args):
         "stages_ms": {name: float(v) for name, v in zip(_lib.STAGES, stage_t.tolist()) if name != "unused"},
         "stage_roofline": stage_roofline(shape, T, rows_list[hot], dict(zip(_lib.STAGES, stage_t.tolist())),
                                          float(peaks.get("hbm_gbs"))),
-        "stages_note": "per-stage means from a diagnostic pass with events at every boundary (max over ranks); "
+        "side_chain_ms": side_ms,
+        "stages_note": "side_chain_ms = [span of the small-group chain on the side stream, GEMM start -> its end]; "
+                       "per-stage means from a diagnostic pass with events at every boundary (max over ranks); "
                        "the timed region records only the K3 boundaries",
         "roofline": {"bound": "tensor", "kernel": f"grouped_gemm_kernel (GEMM1+SwiGLU, GEMM2), rank {hot} "
-                                                  "(most routed rows)",
+                                                  "(most routed rows)"
+                                                  + ("; shared expert fused into the same launches"
+                                                     if exec_plan["fuse_shared"] else ""),
                      "achieved_per_rank": per_rank_tf,
                      "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved_tflops / peak if peak else None, "traffic": traffic,

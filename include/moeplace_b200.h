@@ -162,12 +162,22 @@ int mp_layer_forward(mp_layer* layer, const void* x, void* out, int T, void* str
  * stage boundaries:
  *   0 start | 1 router | 2 count exchange | 3 (unused) | 4 permute+dispatch |
  *   5 shared expert | 6 dispatch barrier | 7 GEMM1 SwiGLU | 8 GEMM2 |
- *   9 return barrier | 10 combine+return                                      */
-#define MP_NUM_STAGE_EVENTS 11
+ *   9 return barrier | 10 combine+return
+ * and, on the side stream when the small-group chain runs (MP_CFG_SPLIT_M):
+ *   11 side chain start | 12 side chain end                                   */
+#define MP_NUM_STAGE_EVENTS 13
 int mp_layer_forward_timed(mp_layer* layer, const void* x, void* out, int T, void* stream, void* const* events);
 
 /* Number of kernels the last mp_layer_forward launched. */
 int mp_layer_last_launches(mp_layer* layer);
+
+/* Execution plan chosen at creation (from the shape; MP_* environment knobs
+ * override), for reporting: */
+#define MP_CFG_PAIR_ROUTED 0   /* routed experts on CTA-pair (256-row) tiles   */
+#define MP_CFG_SPLIT_M 1       /* groups below this many rows: side-stream chain */
+#define MP_CFG_SMALL_GRID 2    /* SMs given to that side chain                   */
+#define MP_CFG_FUSE_SHARED 3   /* shared expert fused into the routed launches   */
+int mp_layer_config(mp_layer* layer, int key);
 
 /* Host copy of the last forward's exchanged count table C[src][e] (G*E int32;
  * synchronises the stream).  C feeds the reference accounting: remote pairs

@@ -26,10 +26,12 @@ MP_E_PEER = -6
 
 MP_SCORE_TOPK_SOFTMAX = 0
 MP_SCORE_SOFTMAX_TOPK = 1
-NUM_STAGE_EVENTS = 11
+NUM_STAGE_EVENTS = 13
+MAIN_STAGE_EVENTS = 11  # 11, 12: side-chain start / end (side stream, split plan only)
 STAGES = ("router", "count_exchange", "unused", "permute_dispatch", "shared_expert", "dispatch_barrier",
           "gemm1_swiglu", "gemm2", "return_barrier", "combine_return")
 GEMM_START, GEMM1_END, GEMM_END = 6, 7, 8
+CFG_KEYS = {"pair_routed": 0, "split_m": 1, "small_grid": 2, "fuse_shared": 3}
 
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
@@ -37,7 +39,7 @@ EXPORTED_SYMBOLS = (
     "mp_layer_create", "mp_layer_destroy", "mp_layer_get_ptrs", "mp_layer_export_handles",
     "mp_layer_open_peers", "mp_layer_set_routes", "mp_layer_prepare_router", "mp_layer_forward",
     "mp_layer_forward_timed",
-    "mp_layer_last_launches", "mp_layer_read_counts", "mp_layer_check", "mp_layer_migrate",
+    "mp_layer_last_launches", "mp_layer_config", "mp_layer_read_counts", "mp_layer_check", "mp_layer_migrate",
 )
 
 
@@ -99,6 +101,7 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         "mp_layer_forward": ([V, V, V, I, V], I),
         "mp_layer_forward_timed": ([V, V, V, I, V, POINTER(c_void_p)], I),
         "mp_layer_last_launches": ([V], I),
+        "mp_layer_config": ([V, I], I),
         "mp_layer_read_counts": ([V, V, V], I),
         "mp_layer_check": ([V, V], I),
         "mp_layer_migrate": ([V, POINTER(CopyOp), I, V, V], I),

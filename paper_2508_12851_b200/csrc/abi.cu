@@ -96,8 +96,13 @@ struct mp_layer {
   // B maps with 128-row boxes for the CTA-pair GEMM (each CTA loads half of N)
   CUtensorMap tm_w13_p, tm_w2_p, tm_w13s_p, tm_w2s_p;
   int pair_routed = 0, pair_shared = 1, gemm_order = 0;
+  // shared expert fused into the routed CTA-pair launches (one GEMM1 and one GEMM2
+  // launch cover both problems; no per-launch tails / wave quantisation of its own)
+  int fuse_shared = 0, fuse_sched = 2;
+  // L2 prefetch distance (k-blocks) of the weight-bound small-group chain
+  int small_prefetch = 0;  // measured: no gain (the chain is MMA-bound on padded 128-row tiles)
   // small-group split: groups below split_m rows run on a side stream over small_grid SMs
-  int split_m = 0, small_grid = 24;
+  int split_m = 0, small_grid = 20;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const void* tm_x_ptr = nullptr;
@@ -339,6 +344,10 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       return fail(set_cuda_error(e, "cudaEventCreate(split)"));
   }
   if (const char* env = getenv("MP_GEMM_ORDER")) L->gemm_order = atoi(env) ? 1 : 0;
+  L->fuse_shared = (D.shared_f > 0 && D.n_slots > 0 && L->pair_routed && L->pair_shared) ? 1 : 0;
+  if (const char* env = getenv("MP_FUSE_SHARED")) L->fuse_shared = L->fuse_shared && atoi(env) != 0;
+  if (const char* env = getenv("MP_FUSE_SCHED")) L->fuse_sched = atoi(env);
+  if (const char* env = getenv("MP_SMALL_PREFETCH")) L->small_prefetch = std::max(0, atoi(env));
   if (D.shared_f > 0) {
     if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
       return fail(r);
@@ -534,7 +543,8 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
                         T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st));
   ++launches;
   MP_TRY(mark());  // 4 permute + dispatch
-  if (D.shared_f > 0 && T > 0) {
+  const bool fused = L->fuse_shared && D.shared_f > 0 && T > 0;
+  if (D.shared_f > 0 && T > 0 && !fused) {
     GroupSpec gsh;
     gsh.mode = 2;
     gsh.single_m = T;
@@ -571,23 +581,45 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       gs.m_lo = L->split_m;
       MP_CUDA(cudaEventRecord(L->ev_fork, st));
       MP_CUDA(cudaStreamWaitEvent(L->side, L->ev_fork, 0));
+      if (events && events[11]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[11]), L->side));
       // (no PDL on the split chains: early-scheduled CTAs would contend for the other chain's SMs)
       MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, gsmall, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                                 L->small_grid, L->side, 0, nullptr, nullptr, false));
+                                 L->small_grid, L->side, 0, nullptr, nullptr, false, nullptr, L->small_prefetch));
       MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, gsmall, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs, false));
+                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs, false, nullptr,
+                                 L->small_prefetch));
+      if (events && events[12]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[12]), L->side));
       MP_CUDA(cudaEventRecord(L->ev_join, L->side));
       launches += 2;
     }
     const int big_grid = L->split_m > 0 ? kNumSMs - L->small_grid : 0;
 
     const bool pdl = L->split_m == 0;
+    // fused shared expert: its GEMM1 / GEMM2 tiles ride in the routed launches
+    AuxProblem aux1, aux2;
+    if (fused) {
+      aux1.tmA = L->tm_x;
+      aux1.tmB = L->tm_w13s_p;
+      aux1.out = L->hs;
+      aux1.out_ld = D.shared_f;
+      aux1.m = T;
+      aux1.N = 2 * D.shared_f;
+      aux1.K = D.d;
+      aux2.tmA = L->tm_hs;
+      aux2.tmB = L->tm_w2s_p;
+      aux2.out = L->ys;
+      aux2.out_ld = D.d;
+      aux2.m = T;
+      aux2.N = D.d;
+      aux2.K = D.shared_f;
+      aux1.sched = aux2.sched = L->fuse_sched;
+    }
     MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                               big_grid, st, pr, nullptr, nullptr, pdl));
+                               big_grid, st, pr, nullptr, nullptr, pdl, fused ? &aux1 : nullptr));
     MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
     // GEMM2 epilogue returns every output row to its origin GPU (NVLink stores)
     MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                               big_grid, st, pr, L->recv_src, ret_ptrs, pdl));
+                               big_grid, st, pr, L->recv_src, ret_ptrs, pdl, fused ? &aux2 : nullptr));
     if (L->split_m > 0) MP_CUDA(cudaStreamWaitEvent(st, L->ev_join, 0));
     launches += 2;
   } else {
@@ -617,6 +649,17 @@ int mp_layer_forward_timed(mp_layer* L, const void* x, void* out, int T, void* s
 }
 
 int mp_layer_last_launches(mp_layer* L) { return L ? L->last_launches : 0; }
+
+int mp_layer_config(mp_layer* L, int key) {
+  if (!L) return set_error(MP_E_ARG, "mp_layer_config: null layer");
+  switch (key) {
+    case MP_CFG_PAIR_ROUTED: return L->pair_routed;
+    case MP_CFG_SPLIT_M: return L->split_m;
+    case MP_CFG_SMALL_GRID: return L->split_m > 0 ? L->small_grid : 0;
+    case MP_CFG_FUSE_SHARED: return L->fuse_shared;
+    default: return set_error(MP_E_ARG, "mp_layer_config: key %d", key);
+  }
+}
 
 int mp_layer_read_counts(mp_layer* L, int32_t* host_counts, void* stream) {
   if (!L || !host_counts) return set_error(MP_E_ARG, "mp_layer_read_counts: null pointer");

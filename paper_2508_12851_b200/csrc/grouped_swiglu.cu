@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out,
                         int out_ld, int swiglu, const int32_t* __restrict__ scatter_src,
-                        __nv_bfloat16* const* __restrict__ scatter_ptrs) {
+                        __nv_bfloat16* const* __restrict__ scatter_ptrs, int l2_prefetch) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -265,11 +265,29 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
       // ================= TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      // L2 prefetch cursor `l2_prefetch` k-blocks ahead of the loads in this CTA's
+      // (tile, k-block) sequence: weight-bound small groups are latency-bound on
+      // the smem ring alone
+      int pt = blockIdx.x, pkb = 0, pb_row = 0;
+      auto prefetch_next = [&]() {
+        if (pt >= total) return;
+        if (pkb == 0) {
+          const TileCoord pc = decode_any(st, pt, n_blocks, gg::BM);
+          pb_row = st.g_slot[pc.g] * b_slot_stride + b_offset + pc.n_blk * gg::BN;
+        }
+        tma_prefetch_l2_2d(&tmB, pkb * gg::BK, pb_row);
+        if (++pkb == k_blocks) {
+          pkb = 0;
+          pt += gridDim.x;
+        }
+      };
+      for (int i = 0; i < l2_prefetch; ++i) prefetch_next();
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
         const TileCoord c = decode_any(st, tile, n_blocks, gg::BM);
         const int a_row = st.g_arow[c.g] + c.m_blk * gg::BM;
         const int b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * gg::BN;
         for (int kb = 0; kb < k_blocks; ++kb) {
+          if (l2_prefetch > 0) prefetch_next();
           mbar_wait(&st.empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&st.full[stage], gg::kStageBytes);
           tma_load_2d(smA + stage * gg::kABytes, &tmA, &st.full[stage], kb * gg::BK, a_row);
@@ -387,11 +405,135 @@ struct Gemm2SmemTail {
 };
 
 
+// One unit of pair work: where its A / B rows come from, how many k-blocks it
+// runs and where its 128 x 256 half-tile of output goes.
+struct PairJob {
+  const CUtensorMap* ma;
+  const CUtensorMap* mb;
+  int a_row, b_row;   // first row of the 256-row tile (A) and of its 256 N rows (B)
+  int k_blocks;
+  int n_blk;
+  int m_row0, m_rows;  // tile's first row inside its group, and the group's row count
+  bool aux;
+  int g;               // routed group (aux: -1)
+};
+
+// Static schedule of one cluster: aux tiles round-robin (tile t -> cluster
+// t mod C), then routed tiles in up to two strided segments.
+//   sched 0  k-block-balanced contiguous ranges (closed form)
+//   sched 1  round-robin over the concatenated [aux | routed] list
+//   sched 2  round-robin (reversed cluster order), then the last routed tiles
+//            only to the clusters that drew one aux tile fewer
+// Without an aux problem every mode is the plain round-robin.
+struct PairSched {
+  int A, aux_mb, aux_kb;
+  int s1_begin, s1_end, s1_step;
+  int s2_begin, s2_end, s2_step;
+};
+
+MP_DEV PairSched make_sched(const AuxProblem& aux, int R, int k_blocks, int cluster_id, int C) {
+  PairSched ps;
+  ps.aux_mb = aux.m > 0 ? (aux.m + g2::BM - 1) / g2::BM : 0;
+  ps.A = ps.aux_mb * (aux.N / g2::BN);
+  ps.aux_kb = aux.K / g2::BK;
+  ps.s2_begin = ps.s2_end = 0;
+  ps.s2_step = 1;
+  const int A = ps.A;
+  if (A == 0) {
+    ps.s1_begin = cluster_id;
+    ps.s1_end = R;
+    ps.s1_step = C;
+    return ps;
+  }
+  const int q = A / C, rem = A - (A / C) * C;
+  if (aux.sched == 1) {
+    ps.s1_begin = ((cluster_id - A) % C + C) % C;
+    ps.s1_end = R;
+    ps.s1_step = C;
+    return ps;
+  }
+  if (aux.sched == 2) {
+    // clusters c >= rem drew q aux tiles, the others q + 1: give the former
+    // about ca/cr routed tiles more each, from the end of the list
+    const int extra = rem > 0 ? (ps.aux_kb + k_blocks / 2) / k_blocks : 0;
+    const int X = min(R, (C - rem) * extra);
+    const int R1 = R - X;
+    ps.s1_begin = C - 1 - cluster_id;
+    ps.s1_end = R1;
+    ps.s1_step = C;
+    if (cluster_id >= rem && X > 0) {
+      ps.s2_begin = R1 + (cluster_id - rem);
+      ps.s2_end = R;
+      ps.s2_step = C - rem;
+    }
+    return ps;
+  }
+  // sched 0: F(c) = c * total - C * ca * (#aux tiles of clusters < c), in (k-blocks x C)
+  const long long ca = ps.aux_kb, cr = k_blocks, total = ca * A + cr * R;
+  long long run = 0;
+  auto start_of = [&](int c, long long& best) -> int {
+    if (c >= C) return R;
+    const long long F = c * total - C * ca * ((long long)c * q + min(c, rem));
+    best = F > best ? F : best;
+    long long t = (best + C * cr / 2) / (C * cr);
+    return int(t < 0 ? 0 : (t > R ? R : t));
+  };
+  int b = 0;
+  for (int c = 1; c <= cluster_id; ++c) b = start_of(c, run);
+  ps.s1_begin = cluster_id == 0 ? 0 : b;
+  long long run2 = run;
+  ps.s1_end = start_of(cluster_id + 1, run2);
+  if (ps.s1_end < ps.s1_begin) ps.s1_end = ps.s1_begin;
+  ps.s1_step = 1;
+  return ps;
+}
+
+template <class Fn>
+MP_DEV void for_each_pair_job(const PairSched& ps, const Gemm2SmemTail& st, const AuxProblem& aux,
+                              const CUtensorMap* tmA, const CUtensorMap* tmB, int n_blocks, int k_blocks,
+                              int b_slot_stride, int b_offset, int cluster_id, int C, Fn&& fn) {
+  for (int t = cluster_id; t < ps.A; t += C) {
+    PairJob j;
+    j.aux = true;
+    j.g = -1;
+    j.n_blk = t / ps.aux_mb;
+    const int m_blk = t - j.n_blk * ps.aux_mb;
+    j.ma = &aux.tmA;
+    j.mb = &aux.tmB;
+    j.m_row0 = m_blk * g2::BM;
+    j.m_rows = aux.m;
+    j.a_row = j.m_row0;
+    j.b_row = j.n_blk * g2::BN;
+    j.k_blocks = ps.aux_kb;
+    fn(j);
+  }
+  for (int seg = 0; seg < 2; ++seg) {
+    const int t0 = seg ? ps.s2_begin : ps.s1_begin, t1 = seg ? ps.s2_end : ps.s1_end;
+    const int dt = seg ? ps.s2_step : ps.s1_step;
+    for (int t = t0; t < t1; t += dt) {
+    const TileCoord c = decode_any(st, t, n_blocks, g2::BM);
+    PairJob j;
+    j.aux = false;
+    j.g = c.g;
+    j.n_blk = c.n_blk;
+    j.ma = tmA;
+    j.mb = tmB;
+    j.m_row0 = c.m_blk * g2::BM;
+    j.m_rows = st.g_m[c.g];
+    j.a_row = st.g_arow[c.g] + j.m_row0;
+    j.b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * g2::BN;
+    j.k_blocks = k_blocks;
+    fn(j);
+    }
+  }
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                            const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out, int out_ld,
-                            int swiglu, const int32_t* __restrict__ scatter_src,
-                            __nv_bfloat16* const* __restrict__ scatter_ptrs) {
+                            const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset,
+                            __nv_bfloat16* __restrict__ out, int out_ld, int swiglu,
+                            const int32_t* __restrict__ scatter_src, __nv_bfloat16* const* __restrict__ scatter_ptrs,
+                            const __grid_constant__ AuxProblem aux) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -422,6 +564,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (aux.m > 0) {
+      tma_prefetch_desc(&aux.tmA);
+      tma_prefetch_desc(&aux.tmB);
+    }
   }
   if (warp == 2) tmem_alloc_2sm<gg::kTmemCols>(&st.tmem_base);
   griddep_wait();
@@ -431,28 +577,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
   cluster_sync();  // the peer's barriers are initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = st.tmem_base;
-  const int total = st.total_tiles;
+  const PairSched ps = make_sched(aux, st.total_tiles, k_blocks, cluster_id, n_clusters);
+  auto each_job = [&](auto&& fn) {
+    for_each_pair_job(ps, st, aux, &tmA, &tmB, n_blocks, k_blocks, b_slot_stride, b_offset, cluster_id, n_clusters,
+                      fn);
+  };
 
   if (warp == 0) {
     if (lane == 0) {
       // ================= TMA producer (both CTAs load their halves)
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster_id; tile < total; tile += n_clusters) {
-        const TileCoord c = decode_any(st, tile, n_blocks, g2::BM);
-        const int a_row = st.g_arow[c.g] + c.m_blk * g2::BM + int(rank) * 128;
-        const int b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * g2::BN + int(rank) * 128;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+      each_job([&](const PairJob& j) {
+        const int a_row = j.a_row + int(rank) * 128;
+        const int b_row = j.b_row + int(rank) * 128;
+        for (int kb = 0; kb < j.k_blocks; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&st.full[stage], 2 * g2::kStageBytes);
-          tma_load_2d_2sm(smA + stage * g2::kABytes, &tmA, &st.full[stage], kb * g2::BK, a_row);
-          tma_load_2d_2sm(smB + stage * g2::kBBytes, &tmB, &st.full[stage], kb * g2::BK, b_row);
+          tma_load_2d_2sm(smA + stage * g2::kABytes, j.ma, &st.full[stage], kb * g2::BK, a_row);
+          tma_load_2d_2sm(smB + stage * g2::kBBytes, j.mb, &st.full[stage], kb * g2::BK, b_row);
           if (++stage == g2::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-      }
+      });
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
@@ -462,11 +611,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = cluster_id; tile < total; tile += n_clusters) {
+      each_job([&](const PairJob& j) {
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * g2::BN);
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = 0; kb < j.k_blocks; ++kb) {
           mbar_wait(&st.full[stage], phase);
           tc_fence_after();
           const uint64_t adesc = make_sdesc_sw128(smem_u32(smA + stage * g2::kABytes));
@@ -483,29 +632,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
         umma_commit_2sm_mc(&st.tfull[acc], 0x3);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-      }
+      });
     }
   } else if (warp >= 4) {
     // ================= epilogue (both CTAs: own 128 rows of the pair tile)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = cluster_id; tile < total; tile += n_clusters) {
-      const TileCoord c = decode_any(st, tile, n_blocks, g2::BM);
-      const int row = c.m_blk * g2::BM + int(rank) * 128 + q * 32 + lane;
-      const bool valid = row < st.g_m[c.g];
-      const size_t orow = size_t(st.g_orow[c.g] + row);
+    each_job([&](const PairJob& j) {
+      const int row = j.m_row0 + int(rank) * 128 + q * 32 + lane;
+      const bool valid = row < j.m_rows;
+      __nv_bfloat16* rowp =
+          j.aux ? aux.out + size_t(row) * aux.out_ld
+                : out_row_ptr(out, size_t(st.g_orow[j.g] + row), out_ld, scatter_src, scatter_ptrs, valid);
       mbar_wait(&st.tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * g2::BN);
-      epilogue_store(taddr, valid, out_row_ptr(out, orow, out_ld, scatter_src, scatter_ptrs, valid), c.n_blk,
-                     swiglu);
+      epilogue_store(taddr, valid, rowp, j.n_blk, swiglu);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&st.tempty[acc], 0);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    }
+    });
   }
 
   tc_fence_before();
@@ -547,9 +696,18 @@ int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,
                         int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream, int pair,
-                        const int32_t* scatter_src, __nv_bfloat16* const* scatter_ptrs, bool pdl) {
+                        const int32_t* scatter_src, __nv_bfloat16* const* scatter_ptrs, bool pdl,
+                        const AuxProblem* aux, int l2_prefetch) {
   if (N % gg::BN != 0) return set_error(MP_E_SHAPE, "grouped GEMM N=%d not a multiple of %d", N, gg::BN);
   if (K % gg::BK != 0) return set_error(MP_E_SHAPE, "grouped GEMM K=%d not a multiple of %d", K, gg::BK);
+  AuxProblem no_aux;
+  if (aux && aux->m > 0) {
+    if (!pair) return set_error(MP_E_ARG, "grouped GEMM: a fused aux problem needs the CTA-pair kernel");
+    if (aux->N % g2::BN != 0 || aux->K % g2::BK != 0 || aux->K <= 0)
+      return set_error(MP_E_SHAPE, "grouped GEMM aux problem N=%d K=%d", aux->N, aux->K);
+    if (swiglu && aux->out_ld < aux->N / 2) return set_error(MP_E_SHAPE, "aux out_ld %d", aux->out_ld);
+  }
+  const AuxProblem& ax = (aux && aux->m > 0) ? *aux : no_aux;
   if (pair) {  // the B map must have 128-row boxes (each CTA loads half of N)
     static bool attr2 = false;
     if (!attr2) {
@@ -562,7 +720,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
     grid &= ~1;
     cudaError_t e = launch_pdl_if(pdl, grouped_gemm_2sm_kernel, dim3(grid), dim3(gg::kThreads), g2::kSmemBytes, stream, tmA,
                                tmB, gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src,
-                               scatter_ptrs);
+                               scatter_ptrs, ax);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_2sm_kernel launch");
     return MP_OK;
@@ -576,7 +734,8 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
   }
   if (grid <= 0) grid = kNumSMs;
   cudaError_t e = launch_pdl_if(pdl, grouped_gemm_kernel, dim3(grid), dim3(gg::kThreads), gg::kSmemBytes, stream, tmA, tmB,
-                             gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs);
+                             gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs,
+                             l2_prefetch);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_kernel launch");
   return MP_OK;

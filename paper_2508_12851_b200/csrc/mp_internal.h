@@ -69,12 +69,24 @@ struct GroupSpec {
   int order = 0;                      // tile order: 0 group-major, 1 n-block-major
   int m_lo = 0, m_hi = 1 << 30;       // mode 1: only groups with m_lo <= m < m_hi
 };
+// A second, dense problem fused into the same CTA-pair launch (the shared
+// expert): its tiles are scheduled first, round-robin over the clusters, and
+// the routed tiles fill each cluster up to an equal share of k-blocks.
+struct alignas(64) AuxProblem {
+  CUtensorMap tmA;                // A rows [m, K] (box 128 rows)
+  CUtensorMap tmB;                // B rows [N, K] (box 128 rows)
+  __nv_bfloat16* out = nullptr;   // [m, out_ld]
+  int out_ld = 0;
+  int m = 0, N = 0, K = 0;        // m == 0: no aux problem
+  int sched = 0;                  // tile schedule (grouped_swiglu.cu: make_sched)
+};
 int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,
                         int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream,
                         int pair = 0, const int32_t* scatter_src = nullptr,
-                        __nv_bfloat16* const* scatter_ptrs = nullptr, bool pdl = true);
+                        __nv_bfloat16* const* scatter_ptrs = nullptr, bool pdl = true,
+                        const AuxProblem* aux = nullptr, int l2_prefetch = 0);
 
 // ---- K5 combine (the expert outputs are already back in this GPU's return buffer)
 int launch_combine(const __nv_bfloat16* ret /*[T][k][d]*/, const float* w, int T, int d, int k,

@@ -26,6 +26,7 @@
 // x rows are read straight from HBM (512 B coalesced per token per step), the
 // padded bf16 Wg [E_pad][d] through L1/L2.  One reduce-scatter per 8-expert pass
 // leaves lane l holding logit (token l/8, expert l%8).
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -75,11 +76,20 @@ MP_DEV bool better(float a, int ia, float b, int ib) { return a > b || (a == b &
 #ifndef MP_ROUTER_MIN_BLOCKS
 #define MP_ROUTER_MIN_BLOCKS 1
 #endif
-constexpr int kWarps = 8;      // 8 warps x 4 tokens = rt::kTokens
+constexpr int kQuads = 8;      // 8 token quads x 4 tokens = rt::kTokens
+constexpr int kMaxWarps = 16;  // 2 warps per quad when there are >= 2 expert passes
 constexpr int kTokPerWarp = 4;
 constexpr int kExpPerPass = 8;
 
-__global__ void __launch_bounds__(kWarps * 32, MP_ROUTER_MIN_BLOCKS)
+// kWarpsT = 8: one warp per quad, 255-register budget, two k-steps of loads in
+// flight per warp (Mixtral: one expert pass; x read once, straight from HBM
+// after an L2 bulk prefetch of the CTA's rows).  kWarpsT = 16: two warps per
+// quad on alternate passes, 128 registers -- twice the warps to hide latency
+// when there are >= 2 passes (E_pad >= 16); with kXSmem the CTA's 32 x rows
+// (contiguous, 32 d bf16) are bulk-copied into shared memory once and every
+// pass reads them from there.
+template <int kWarpsT, bool kXSmem>
+__global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
     router_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wp,
                   const float* __restrict__ bias, int T, int d, int E, int has_gate, int k, int score_mode,
                   int renorm, int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
@@ -87,37 +97,63 @@ __global__ void __launch_bounds__(kWarps * 32, MP_ROUTER_MIN_BLOCKS)
                   uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix) {
   __shared__ float logits[rt::kTokens][rt::kMaxE + 9];
   __shared__ int cnt_s[rt::kMaxE];
-  extern __shared__ int bc[];  // [nb][E] block counts staged by the last CTA (dynamic smem)
+  __shared__ uint64_t xbar;
+  // kXSmem: the CTA's x rows [32][d]; afterwards (last CTA) the [nb][E] block counts
+  extern __shared__ __align__(128) uint8_t dsm[];
+  int* bc = reinterpret_cast<int*>(dsm);
 
-  griddep_launch_dependents();
-  griddep_wait();
   const int E_tot = E + has_gate;
   const int E_pad = router_e_pad(E_tot);
   const int t0 = blockIdx.x * rt::kTokens;
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  const int n_tok = min(rt::kTokens, T - t0);
   for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
+  if (kXSmem && tid == 0) {
+    mbar_init(&xbar, 1);
+    fence_barrier_init();
+  }
+  griddep_launch_dependents();
+  __syncthreads();
+  griddep_wait();
+  const __nv_bfloat16* xblk = x + size_t(t0) * d;  // n_tok contiguous rows
+  if (tid == 0) {
+    const uint32_t bytes = uint32_t(n_tok) * d * 2;
+    if (kXSmem) {
+      mbar_arrive_expect_tx(&xbar, bytes);
+      for (uint32_t off = 0; off < bytes; off += 32768u)
+        bulk_load(dsm + off, reinterpret_cast<const uint8_t*>(xblk) + off, min(32768u, bytes - off), &xbar);
+    } else {
+      for (uint32_t off = 0; off < bytes; off += 32768u)
+        bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(xblk) + off, min(32768u, bytes - off));
+    }
+  }
 
-  // this warp's 4 tokens (rows past T read row 0 and are discarded)
+  // this warp's 4 tokens (rows past T are never loaded and are discarded); with
+  // 16 warps, warp w and w + 8 share a quad and take alternate expert passes
+  const int quad = warp % kQuads, n_pg = (blockDim.x >> 5) / kQuads;
   const __nv_bfloat16* xr[kTokPerWarp];
 #pragma unroll
   for (int i = 0; i < kTokPerWarp; ++i) {
-    const int t = t0 + warp * kTokPerWarp + i;
-    xr[i] = x + size_t(t < T ? t : 0) * d + 8 * lane;
+    const int r = quad * kTokPerWarp + i;
+    xr[i] = kXSmem ? reinterpret_cast<const __nv_bfloat16*>(dsm) + size_t(r) * d + 8 * lane
+                   : x + size_t(t0 + (r < n_tok ? r : 0)) * d + 8 * lane;
   }
+  if (kXSmem) mbar_wait(&xbar, 0);
   const int S = d / 256;
 
-  for (int e0 = 0; e0 < E_pad; e0 += kExpPerPass) {
+  for (int e0 = kExpPerPass * (warp / kQuads); e0 < E_pad; e0 += kExpPerPass * n_pg) {
     unsigned long long acc[kTokPerWarp][kExpPerPass / 2];
 #pragma unroll
     for (int i = 0; i < kTokPerWarp; ++i)
 #pragma unroll
       for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
     const __nv_bfloat16* wr = wp + size_t(e0) * d + 8 * lane;
-#pragma unroll 2
+#pragma unroll(kWarpsT == kQuads ? 2 : 1)
     for (int s = 0; s < S; ++s) {
       uint4 xv[kTokPerWarp], wv[kExpPerPass];
 #pragma unroll
-      for (int i = 0; i < kTokPerWarp; ++i) xv[i] = ld_nc_v4(xr[i] + 256 * s);
+      for (int i = 0; i < kTokPerWarp; ++i)
+        xv[i] = kXSmem ? *reinterpret_cast<const uint4*>(xr[i] + 256 * s) : ld_nc_v4(xr[i] + 256 * s);
 #pragma unroll
       for (int j = 0; j < kExpPerPass; ++j)
         wv[j] = __ldg(reinterpret_cast<const uint4*>(wr + size_t(j) * d + 256 * s));
@@ -159,7 +195,7 @@ __global__ void __launch_bounds__(kWarps * 32, MP_ROUTER_MIN_BLOCKS)
         v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
       }
     }
-    const int tt = warp * kTokPerWarp + (lane >> 3), e = e0 + (lane & 7);
+    const int tt = quad * kTokPerWarp + (lane >> 3), e = e0 + (lane & 7);
     if (e < E_tot) {
       float val = v[0];
       if (bias != nullptr && e < E) val = __fadd_rn(val, bias[e]);
@@ -288,18 +324,30 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   if (d % 256 != 0) return set_error(MP_E_SHAPE, "router: d=%d not a multiple of 256", d);
   if (score_mode != 0 && score_mode != 1) return set_error(MP_E_ARG, "router: score_mode %d", score_mode);
   if (T <= 0) return MP_OK;
+  if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return set_error(MP_E_ARG, "router: x not 16-byte aligned");
   const int grid = (T + rt::kTokens - 1) / rt::kTokens;
-  const size_t smem = blk_counts && batch_counts ? size_t(grid) * E * 4 : 0;
-  if (smem > 200 * 1024) return set_error(MP_E_SHAPE, "router: %d blocks x %d experts too large", grid, E);
-  static size_t smem_set = 0;
-  if (smem > 48 * 1024 && smem > smem_set) {
-    cudaError_t ea = cudaFuncSetAttribute(router_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const size_t bc_bytes = blk_counts && batch_counts ? size_t(grid) * E * 4 : 0;
+  if (bc_bytes > 200 * 1024) return set_error(MP_E_SHAPE, "router: %d blocks x %d experts too large", grid, E);
+  static const int wide_env = [] {
+    const char* v = getenv("MP_ROUTER_WIDE");
+    return v ? atoi(v) : -1;
+  }();
+  const bool wide = wide_env >= 0 ? wide_env != 0 : router_e_pad(E + (has_gate ? 1 : 0)) >= 2 * kExpPerPass;
+  const size_t x_bytes = size_t(rt::kTokens) * d * 2;
+  const bool xsmem = wide && x_bytes <= 160 * 1024;
+  auto kern = xsmem ? router_kernel<kMaxWarps, true>
+                    : (wide ? router_kernel<kMaxWarps, false> : router_kernel<kQuads, false>);
+  const int variant = xsmem ? 2 : (wide ? 1 : 0);
+  const size_t smem = std::max(bc_bytes, xsmem ? x_bytes : size_t(0));
+  static size_t smem_set[3] = {0, 0, 0};
+  if (smem > 48 * 1024 && smem > smem_set[variant]) {
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (ea != cudaSuccess) return set_cuda_error(ea, "cudaFuncSetAttribute(router)");
-    smem_set = smem;
+    smem_set[variant] = smem;
   }
-  cudaError_t e = launch_pdl(router_kernel, dim3(grid), dim3(kWarps * 32), smem, stream, x, wg_packed, bias, T, d, E,
-                             has_gate ? 1 : 0, k, score_mode, renorm, idx, w, shared_gate, hist, blk_counts,
-                             batch_counts, ticket, blk_prefix);
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3((wide ? kMaxWarps : kQuads) * 32), smem, stream, x, wg_packed,
+                             bias, T, d, E, has_gate ? 1 : 0, k, score_mode, renorm, idx, w, shared_gate, hist,
+                             blk_counts, batch_counts, ticket, blk_prefix);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_kernel launch");
 }

@@ -240,6 +240,10 @@ class B200MoELayer:
     def last_launches(self) -> int:
         return int(self.lib.mp_layer_last_launches(self._h))
 
+    def exec_plan(self) -> dict:
+        """Execution plan the C ABI chose for this layer (mp_layer_config)."""
+        return {k: int(self.lib.mp_layer_config(self._h, v)) for k, v in _lib.CFG_KEYS.items()}
+
     def check(self) -> None:
         _lib.check(self.lib.mp_layer_check(self._h, self._stream()), "mp_layer_check")
 

@@ -51,7 +51,9 @@ def main():
     res = {}
     E_tot = E + shape.shared_gate
     if not args.only or args.only == "router":
-        x = wl.tokens(T, d, dev)
+        # 16 rotating batches (> L2) so every call reads its x cold from HBM, as inside a layer step
+        xs_ = [wl.tokens(T, d, dev, batch=b) for b in range(16)]
+        x = xs_[0]
         wg = wl.router_weights(E_tot, d, dev)
         packed = torch.empty((E_tot + 7) // 8 * 8 * d, device=dev, dtype=torch.bfloat16)
         _lib.check(lib.mp_router_pack(vp(wg), E_tot, d, vp(packed), st))
@@ -60,7 +62,12 @@ def main():
         w = torch.empty(T, k, dtype=torch.float32, device=dev)
         g = torch.empty(T, dtype=torch.float32, device=dev)
         hist = torch.zeros(E, dtype=torch.int32, device=dev)
-        call = lambda: _lib.check(lib.mp_router_topk_hist(vp(x), vp(packed), vp(bias), T, d, E, shape.shared_gate, k,
+        rot = [0]
+
+        def nxt():
+            rot[0] = (rot[0] + 1) % len(xs_)
+            return xs_[rot[0]]
+        call = lambda: _lib.check(lib.mp_router_topk_hist(vp(nxt()), vp(packed), vp(bias), T, d, E, shape.shared_gate, k,
                                                           shape.score_mode, 0, vp(idx), vp(w), vp(g), vp(hist), st))
         us = timeit(call, args.iters)
         byts = T * d * 2 + T * k * 8
