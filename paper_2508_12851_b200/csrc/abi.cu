@@ -99,8 +99,6 @@ struct mp_layer {
   // shared expert fused into the routed CTA-pair launches (one GEMM1 and one GEMM2
   // launch cover both problems; no per-launch tails / wave quantisation of its own)
   int fuse_shared = 0, fuse_sched = 2;
-  // L2 prefetch distance (k-blocks) of the weight-bound small-group chain
-  int small_prefetch = 0;  // measured: no gain (the chain is MMA-bound on padded 128-row tiles)
   // small-group split: groups below split_m rows run on a side stream over small_grid SMs
   int split_m = 0, small_grid = 20;
   cudaStream_t side = nullptr;
@@ -347,7 +345,6 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   L->fuse_shared = (D.shared_f > 0 && D.n_slots > 0 && L->pair_routed && L->pair_shared) ? 1 : 0;
   if (const char* env = getenv("MP_FUSE_SHARED")) L->fuse_shared = L->fuse_shared && atoi(env) != 0;
   if (const char* env = getenv("MP_FUSE_SCHED")) L->fuse_sched = atoi(env);
-  if (const char* env = getenv("MP_SMALL_PREFETCH")) L->small_prefetch = std::max(0, atoi(env));
   if (D.shared_f > 0) {
     if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
       return fail(r);
@@ -584,10 +581,9 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       if (events && events[11]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[11]), L->side));
       // (no PDL on the split chains: early-scheduled CTAs would contend for the other chain's SMs)
       MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, gsmall, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                                 L->small_grid, L->side, 0, nullptr, nullptr, false, nullptr, L->small_prefetch));
+                                 L->small_grid, L->side, 0, nullptr, nullptr, false));
       MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, gsmall, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs, false, nullptr,
-                                 L->small_prefetch));
+                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs, false));
       if (events && events[12]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[12]), L->side));
       MP_CUDA(cudaEventRecord(L->ev_join, L->side));
       launches += 2;

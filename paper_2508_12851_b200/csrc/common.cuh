@@ -101,14 +101,6 @@ MP_DEV void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes)
                : "memory");
 }
-// Prefetch a 2-D box of a tensor map into L2 (no shared memory, no completion):
-// keeps HBM busy further ahead than the shared-memory ring can.
-MP_DEV void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
 // 2-D tile load global -> shared, completion signalled on `bar` (tx bytes).
 // c0 = innermost (element) coordinate, c1 = row coordinate.
 MP_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {

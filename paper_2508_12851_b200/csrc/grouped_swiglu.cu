@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out,
                         int out_ld, int swiglu, const int32_t* __restrict__ scatter_src,
-                        __nv_bfloat16* const* __restrict__ scatter_ptrs, int l2_prefetch) {
+                        __nv_bfloat16* const* __restrict__ scatter_ptrs) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -265,29 +265,11 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
       // ================= TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      // L2 prefetch cursor `l2_prefetch` k-blocks ahead of the loads in this CTA's
-      // (tile, k-block) sequence: weight-bound small groups are latency-bound on
-      // the smem ring alone
-      int pt = blockIdx.x, pkb = 0, pb_row = 0;
-      auto prefetch_next = [&]() {
-        if (pt >= total) return;
-        if (pkb == 0) {
-          const TileCoord pc = decode_any(st, pt, n_blocks, gg::BM);
-          pb_row = st.g_slot[pc.g] * b_slot_stride + b_offset + pc.n_blk * gg::BN;
-        }
-        tma_prefetch_l2_2d(&tmB, pkb * gg::BK, pb_row);
-        if (++pkb == k_blocks) {
-          pkb = 0;
-          pt += gridDim.x;
-        }
-      };
-      for (int i = 0; i < l2_prefetch; ++i) prefetch_next();
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
         const TileCoord c = decode_any(st, tile, n_blocks, gg::BM);
         const int a_row = st.g_arow[c.g] + c.m_blk * gg::BM;
         const int b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * gg::BN;
         for (int kb = 0; kb < k_blocks; ++kb) {
-          if (l2_prefetch > 0) prefetch_next();
           mbar_wait(&st.empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&st.full[stage], gg::kStageBytes);
           tma_load_2d(smA + stage * gg::kABytes, &tmA, &st.full[stage], kb * gg::BK, a_row);
@@ -697,7 +679,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
                         int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream, int pair,
                         const int32_t* scatter_src, __nv_bfloat16* const* scatter_ptrs, bool pdl,
-                        const AuxProblem* aux, int l2_prefetch) {
+                        const AuxProblem* aux) {
   if (N % gg::BN != 0) return set_error(MP_E_SHAPE, "grouped GEMM N=%d not a multiple of %d", N, gg::BN);
   if (K % gg::BK != 0) return set_error(MP_E_SHAPE, "grouped GEMM K=%d not a multiple of %d", K, gg::BK);
   AuxProblem no_aux;
@@ -734,8 +716,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
   }
   if (grid <= 0) grid = kNumSMs;
   cudaError_t e = launch_pdl_if(pdl, grouped_gemm_kernel, dim3(grid), dim3(gg::kThreads), gg::kSmemBytes, stream, tmA, tmB,
-                             gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs,
-                             l2_prefetch);
+                             gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_kernel launch");
   return MP_OK;

@@ -86,7 +86,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream,
                         int pair = 0, const int32_t* scatter_src = nullptr,
                         __nv_bfloat16* const* scatter_ptrs = nullptr, bool pdl = true,
-                        const AuxProblem* aux = nullptr, int l2_prefetch = 0);
+                        const AuxProblem* aux = nullptr);
 
 // ---- K5 combine (the expert outputs are already back in this GPU's return buffer)
 int launch_combine(const __nv_bfloat16* ret /*[T][k][d]*/, const float* w, int T, int d, int k,
