@@ -185,8 +185,8 @@ MP_DEV void epilogue_store(uint32_t taddr, bool valid, __nv_bfloat16* __restrict
       for (int i = 0; i < 16; ++i) {
         float g0 = __uint_as_float(gv[2 * i]), g1 = __uint_as_float(gv[2 * i + 1]);
         float u0 = __uint_as_float(uv[2 * i]), u1 = __uint_as_float(uv[2 * i + 1]);
-        float h0 = g0 / (1.0f + __expf(-g0)) * u0;
-        float h1 = g1 / (1.0f + __expf(-g1)) * u1;
+        float h0 = __fdividef(g0, 1.0f + __expf(-g0)) * u0;
+        float h1 = __fdividef(g1, 1.0f + __expf(-g1)) * u1;
         packed[i] = pack_bf16x2(h0, h1);
       }
       if (valid) {
