@@ -151,18 +151,20 @@ int mp_layer_prepare_router(mp_layer* layer, void* stream);
 
 /* One MoE-layer forward of T tokens originating on this GPU -- replaces
  * `_dispatch_layer` (sim.py:441-463).  x, out: [T, d] bf16 device.  SPMD: all
- * G ranks must call it with their own T.  Kernels: router+histogram, count
- * exchange, permute+dispatch (NVLink stores), shared expert, barrier, grouped
- * SwiGLU GEMMs (tcgen05; GEMM2's epilogue stores each row back to its origin
- * GPU over NVLink), barrier, combine (local). */
+ * G ranks must call it with their own T (T = 0 allowed).  Kernels: router +
+ * histogram (its tail publishes the counts to every peer), permute + dispatch
+ * (NVLink stores), grouped SwiGLU GEMMs on tcgen05 (shared expert fused in;
+ * GEMM2's epilogue stores each row back to its origin GPU over NVLink),
+ * combine (local).  The cross-GPU ordering is a flag protocol inside those
+ * kernels; there is no separate barrier launch. */
 int mp_layer_forward(mp_layer* layer, const void* x, void* out, int T, void* stream);
 
 /* Same forward, recording MP_NUM_STAGE_EVENTS cudaEvent_t (created by the
  * caller with timing enabled; NULL entries are skipped) on `stream` at the
  * stage boundaries:
- *   0 start | 1 router | 2 count exchange | 3 (unused) | 4 permute+dispatch |
- *   5 shared expert | 6 dispatch barrier | 7 GEMM1 SwiGLU | 8 GEMM2 |
- *   9 return barrier | 10 combine+return
+ *   0 start | 1 router (+ count exchange) | 2, 3 (folded) | 4 permute+dispatch |
+ *   5 shared expert (empty when fused into K3) | 6 (folded) | 7 GEMM1 SwiGLU |
+ *   8 GEMM2 | 9 (folded) | 10 combine+return
  * and, on the side stream when the small-group chain runs (MP_CFG_SPLIT_M):
  *   11 side chain start | 12 side chain end                                   */
 #define MP_NUM_STAGE_EVENTS 13

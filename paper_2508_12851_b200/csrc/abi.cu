@@ -86,6 +86,7 @@ struct mp_layer {
           *batch_counts = nullptr, *route_d = nullptr,
           *slot_of_d = nullptr;
   uint32_t *hist = nullptr, *err = nullptr, *ticket = nullptr, *sync_state = nullptr;
+  uint32_t *perm_ticket = nullptr, *ret_ticket = nullptr;  // arrival counters of the raising kernels
   void** ptr_arrays = nullptr;  // device: recv[8], ret[8], flags[8], counts0[8], counts1[8], recv_src[8]
 
   uint8_t* peer_window[8] = {};
@@ -270,6 +271,8 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       L->hist = cv.take<uint32_t>(64);
       L->err = cv.take<uint32_t>(4);
       L->ticket = cv.take<uint32_t>(4);
+      L->perm_ticket = cv.take<uint32_t>(4);
+      L->ret_ticket = cv.take<uint32_t>(4);
       L->sync_state = cv.take<uint32_t>(4);
       L->ptr_arrays = cv.take<void*>(6 * 8);
       if (D.shared_f > 0) {
@@ -519,26 +522,49 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     L->tm_x_rows = T;
   }
 
-  MP_TRY(mark());  // 0
-  MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
-                       D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
-                       L->ticket, L->blk_prefix, st));
-  ++launches;
-  MP_TRY(mark());  // 1 router (+ per-batch counts)
-  const int32_t* counts_all = L->batch_counts;
-  const uint32_t* parity = nullptr;
+  // NVLink flag protocol (G > 1), folded into the kernels: router tail raises A
+  // (counts published), permute waits A and its tail raises B (rows sent), GEMM1
+  // producers wait B, the GEMM2 tails raise C (rows returned), combine waits C
+  PeerSync ps0;
   if (G > 1) {
-    MP_TRY(launch_publish_barrier(flag_ptrs, count_ptrs, L->batch_counts, E, G, rank, L->sync_state, L->err, st));
-    ++launches;
-    counts_all = L->counts;
-    parity = L->sync_state + 2;
+    ps0.flag_ptrs = flag_ptrs;
+    ps0.count_ptrs = count_ptrs;
+    ps0.state = L->sync_state;
+    ps0.err = L->err;
+    ps0.G = G;
+    ps0.rank = rank;
   }
-  MP_TRY(mark());  // 2 count exchange
+  PeerSync ps_wait = ps0, ps_perm = ps0, ps_ret = ps0;
+  ps_wait.wait = 1;
+  ps_perm.wait = 1;
+  ps_perm.ticket = L->perm_ticket;
+  ps_perm.total = 1;  // launch_permute sets its grid
+  ps_ret.ticket = L->ret_ticket;
+
+  MP_TRY(mark());  // 0
+  if (T > 0) {
+    MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
+                         D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
+                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr));
+    ++launches;
+  } else if (G > 1) {
+    // no router / permute on this origin: publish zero counts, raise A and B
+    MP_TRY(launch_peer_sync(ps0, L->batch_counts, E, 2, st));
+    ++launches;
+  } else {
+    MP_CUDA(cudaMemsetAsync(L->batch_counts, 0, size_t(E) * 4, st));
+  }
+  MP_TRY(mark());  // 1 router (+ per-batch counts, count exchange)
+  const int32_t* counts_all = G > 1 ? L->counts : L->batch_counts;
+  const uint32_t* parity = G > 1 ? L->sync_state + 2 : nullptr;
+  MP_TRY(mark());  // 2 (count exchange: folded into the router tail / permute prologue)
   MP_TRY(mark());  // 3 (layout: folded into permute / GEMM prologues)
-  MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, parity, L->blk_prefix,
-                        src_ptrs, rank, G,
-                        T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st));
-  ++launches;
+  if (T > 0) {
+    MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, parity,
+                          L->blk_prefix, src_ptrs, rank, G, T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st,
+                          G > 1 ? &ps_perm : nullptr));
+    ++launches;
+  }
   MP_TRY(mark());  // 4 permute + dispatch
   const bool fused = L->fuse_shared && D.shared_f > 0 && T > 0;
   if (D.shared_f > 0 && T > 0 && !fused) {
@@ -553,11 +579,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     launches += 2;
   }
   MP_TRY(mark());  // 5 shared expert
-  if (G > 1) {
-    MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, L->sync_state, L->err, st));
-    ++launches;
-  }
-  MP_TRY(mark());  // 6 dispatch barrier
+  MP_TRY(mark());  // 6 (dispatch barrier: folded into the permute tail / GEMM1 producers)
   if (D.n_slots > 0) {
     GroupSpec gs;
     gs.mode = 1;
@@ -570,6 +592,11 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     gs.rank = rank;
     gs.order = L->gemm_order;
     const int pr = L->pair_routed;
+    const int big_grid = L->split_m > 0 ? kNumSMs - L->small_grid : 0;
+    // C is raised by the last GEMM2 CTA of both chains
+    ps_ret.total = grouped_gemm_ctas(big_grid, pr) + (L->split_m > 0 ? grouped_gemm_ctas(L->small_grid, 0) : 0);
+    const PeerSync* sw = G > 1 ? &ps_wait : nullptr;
+    const PeerSync* sr = G > 1 ? &ps_ret : nullptr;
     if (L->split_m > 0) {
       // fork: small groups (weight-bound) on the side stream over small_grid SMs, large
       // groups (compute-bound) on the main stream over the rest, then join
@@ -581,15 +608,13 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       if (events && events[11]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[11]), L->side));
       // (no PDL on the split chains: early-scheduled CTAs would contend for the other chain's SMs)
       MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, gsmall, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                                 L->small_grid, L->side, 0, nullptr, nullptr, false));
+                                 L->small_grid, L->side, 0, nullptr, nullptr, false, nullptr, sw));
       MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, gsmall, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs, false));
+                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs, false, nullptr, sr));
       if (events && events[12]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[12]), L->side));
       MP_CUDA(cudaEventRecord(L->ev_join, L->side));
       launches += 2;
     }
-    const int big_grid = L->split_m > 0 ? kNumSMs - L->small_grid : 0;
-
     const bool pdl = L->split_m == 0;
     // fused shared expert: its GEMM1 / GEMM2 tiles ride in the routed launches
     AuxProblem aux1, aux2;
@@ -611,25 +636,28 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       aux1.sched = aux2.sched = L->fuse_sched;
     }
     MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                               big_grid, st, pr, nullptr, nullptr, pdl, fused ? &aux1 : nullptr));
+                               big_grid, st, pr, nullptr, nullptr, pdl, fused ? &aux1 : nullptr, sw));
     MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
     // GEMM2 epilogue returns every output row to its origin GPU (NVLink stores)
     MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                               big_grid, st, pr, L->recv_src, ret_ptrs, pdl, fused ? &aux2 : nullptr));
+                               big_grid, st, pr, L->recv_src, ret_ptrs, pdl, fused ? &aux2 : nullptr, sr));
     if (L->split_m > 0) MP_CUDA(cudaStreamWaitEvent(st, L->ev_join, 0));
     launches += 2;
   } else {
     MP_TRY(mark());
+    if (G > 1) {  // no GEMM2 here to raise C
+      MP_TRY(launch_peer_sync(ps0, nullptr, E, 1, st));
+      ++launches;
+    }
   }
   MP_TRY(mark());  // 8 GEMM2
-  if (G > 1) {
-    MP_TRY(launch_publish_barrier(flag_ptrs, nullptr, nullptr, E, G, rank, L->sync_state, L->err, st));
+  MP_TRY(mark());  // 9 (return barrier: folded into the GEMM2 tails / combine prologue)
+  if (T > 0) {
+    MP_TRY(launch_combine(L->ret, L->w, T, D.d, k, D.shared_f > 0 ? L->ys : nullptr,
+                          D.shared_gate ? L->sgate : nullptr, static_cast<__nv_bfloat16*>(out), st,
+                          G > 1 ? &ps_wait : nullptr));
     ++launches;
   }
-  MP_TRY(mark());  // 9 return barrier
-  MP_TRY(launch_combine(L->ret, L->w, T, D.d, k, D.shared_f > 0 ? L->ys : nullptr,
-                        D.shared_gate ? L->sgate : nullptr, static_cast<__nv_bfloat16*>(out), st));
-  ++launches;
   MP_TRY(mark());  // 10 combine + return
   L->last_launches = launches;
   return MP_OK;

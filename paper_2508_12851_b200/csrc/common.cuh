@@ -247,12 +247,23 @@ MP_DEV uint64_t globaltimer_ns() {
   return t;
 }
 
+// Order this thread's earlier generic-proxy observations before its later
+// async-proxy (TMA) global reads.
+MP_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+constexpr uint64_t kPeerTimeoutNs = 30ull * 1000ull * 1000ull * 1000ull;
+
 // 16-byte streaming load / store.
 MP_DEV uint4 ld_nc_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+  return r;
+}
+MP_DEV uint4 ld_cg_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
 MP_DEV uint4 ld_v4(const void* p) {

@@ -18,6 +18,7 @@
 // exchanged count table -- there is no separate layout kernel.
 #include "common.cuh"
 #include "mp_internal.h"
+#include "peer_sync.cuh"
 
 namespace mp {
 
@@ -39,7 +40,7 @@ __global__ void __launch_bounds__(256)
                    const uint32_t* __restrict__ parity, const int32_t* __restrict__ blk_prefix,
                    int32_t* const* __restrict__ src_ptrs, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* __restrict__ recv_ptrs, int32_t* __restrict__ pos_dst,
-                   int32_t* __restrict__ pos_row) {
+                   int32_t* __restrict__ pos_row, const PeerSync sync) {
   constexpr int kTok = 32;
   __shared__ int s_e[kTok * 8];
   __shared__ int s_dst[kTok * 8];
@@ -53,9 +54,12 @@ __global__ void __launch_bounds__(256)
   const int tid = threadIdx.x;
   griddep_launch_dependents();
   griddep_wait();
+  // count exchange: every rank's counts of this forward are in our table once
+  // all flags reached epoch A (raised by each rank's router)
+  if (peer_on(sync) && sync.wait) peer_wait_cta(sync);
   if (parity != nullptr) counts_all += size_t(*parity) * G * E;
   for (int i = tid; i < G * E; i += blockDim.x) {
-    C[i / E][i % E] = counts_all[i];
+    C[i / E][i % E] = __ldcg(counts_all + i);
     R[i / E][i % E] = route[i];
   }
   if (tid < np) s_e[tid] = idx[size_t(t0) * k + tid];
@@ -104,22 +108,27 @@ __global__ void __launch_bounds__(256)
       }
     }
   }
+  // dispatch done: the last CTA raises epoch B once every CTA's rows are visible
+  if (peer_on(sync) && sync.total > 0) peer_arrive_and_raise(sync);
 }
 
 int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
                    const uint32_t* parity, const int32_t* blk_prefix, int32_t* const* src_ptrs, int rank, int G,
                    int T, int d, int E, int k,
-                   __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream) {
+                   __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream,
+                   const PeerSync* sync) {
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "permute: d=%d not a multiple of 8", d);
   if (k > 8) return set_error(MP_E_SHAPE, "permute: top_k=%d > 8", k);
   if (G < 1 || G > 8 || E < 1 || E > 64) return set_error(MP_E_SHAPE, "permute: G=%d E=%d", G, E);
   if (T <= 0) return MP_OK;
   const int grid = (T + 31) / 32;
   const int vpl = (d / 8 + 31) / 32;
+  PeerSync ps = sync ? *sync : PeerSync();
+  if (ps.total > 0) ps.total = grid;
   cudaError_t e;
 #define MP_PERM_LAUNCH(N)                                                                                    \
   e = launch_pdl(permute_kernel<N>, dim3(grid), dim3(256), 0, stream, x, idx, route, counts_all, parity, blk_prefix, \
-                 src_ptrs, rank, G, T, d, E, k, recv_ptrs, pos_dst, pos_row)
+                 src_ptrs, rank, G, T, d, E, k, recv_ptrs, pos_dst, pos_row, ps)
   if (vpl <= 1) MP_PERM_LAUNCH(1);
   else if (vpl <= 2) MP_PERM_LAUNCH(2);
   else if (vpl <= 4) MP_PERM_LAUNCH(4);
@@ -141,9 +150,11 @@ template <int K>
 __global__ void __launch_bounds__(256)
     combine_kernel(const __nv_bfloat16* __restrict__ ret, const float* __restrict__ w, int T, int d,
                    const __nv_bfloat16* __restrict__ shared_y, const float* __restrict__ shared_gate,
-                   __nv_bfloat16* __restrict__ out) {
+                   __nv_bfloat16* __restrict__ out, const PeerSync sync) {
   griddep_launch_dependents();
   griddep_wait();
+  // every rank's GEMM2 stored its rows of our tokens into ret (epoch C)
+  if (peer_on(sync) && sync.wait) peer_wait_cta(sync);
   const int t = blockIdx.x * 8 + warp_id();
   if (t >= T) return;
   const int lane = lane_id();
@@ -157,7 +168,7 @@ __global__ void __launch_bounds__(256)
   for (int c = lane; c < nvec; c += 32) {
     uint4 v[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) v[j] = ld_nc_v4(src + size_t(j) * d + 8 * c);
+    for (int j = 0; j < K; ++j) v[j] = ld_cg_v4(src + size_t(j) * d + 8 * c);  // peer-written: L2, not L1/nc
     float acc[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.f;
@@ -189,15 +200,16 @@ __global__ void __launch_bounds__(256)
 }
 
 int launch_combine(const __nv_bfloat16* ret, const float* w, int T, int d, int k, const __nv_bfloat16* shared_y,
-                   const float* shared_gate, __nv_bfloat16* out, cudaStream_t stream) {
+                   const float* shared_gate, __nv_bfloat16* out, cudaStream_t stream, const PeerSync* sync) {
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "combine: d=%d not a multiple of 8", d);
   if (k < 1 || k > 8) return set_error(MP_E_SHAPE, "combine: top_k=%d outside [1, 8]", k);
   if (T <= 0) return MP_OK;
   const int grid = (T + 7) / 8;
+  const PeerSync ps = sync ? *sync : PeerSync();
   cudaError_t e = cudaSuccess;
   switch (k) {
 #define MP_COMBINE_CASE(N) \
-  case N: e = launch_pdl(combine_kernel<N>, dim3(grid), dim3(256), 0, stream, ret, w, T, d, shared_y, shared_gate, out); break;
+  case N: e = launch_pdl(combine_kernel<N>, dim3(grid), dim3(256), 0, stream, ret, w, T, d, shared_y, shared_gate, out, ps); break;
     MP_COMBINE_CASE(1) MP_COMBINE_CASE(2) MP_COMBINE_CASE(3) MP_COMBINE_CASE(4)
     MP_COMBINE_CASE(5) MP_COMBINE_CASE(6) MP_COMBINE_CASE(7) MP_COMBINE_CASE(8)
 #undef MP_COMBINE_CASE

@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "mp_internal.h"
+#include "peer_sync.cuh"
 
 namespace mp {
 
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out,
                         int out_ld, int swiglu, const int32_t* __restrict__ scatter_src,
-                        __nv_bfloat16* const* __restrict__ scatter_ptrs) {
+                        __nv_bfloat16* const* __restrict__ scatter_ptrs, const PeerSync sync) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -265,6 +266,11 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
       // ================= TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      // rows from peers: wait for every rank's dispatch (epoch B) before the first A load
+      if (peer_on(sync) && sync.wait && blockIdx.x < total) {
+        peer_wait(sync, sync.state[0]);
+        fence_proxy_async_global();
+      }
       for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
         const TileCoord c = decode_any(st, tile, n_blocks, gg::BM);
         const int a_row = st.g_arow[c.g] + c.m_blk * gg::BM;
@@ -344,6 +350,8 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
     tc_fence_after();
     tmem_dealloc<gg::kTmemCols>(tmem_base);
   }
+  // GEMM2: the rows this CTA returned over NVLink are counted towards epoch C
+  if (peer_on(sync) && sync.total > 0) peer_arrive_and_raise(sync);
 }
 
 // ------------------------------------------------------------------ CTA-pair variant
@@ -515,7 +523,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
                             const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset,
                             __nv_bfloat16* __restrict__ out, int out_ld, int swiglu,
                             const int32_t* __restrict__ scatter_src, __nv_bfloat16* const* __restrict__ scatter_ptrs,
-                            const __grid_constant__ AuxProblem aux) {
+                            const __grid_constant__ AuxProblem aux, const PeerSync sync) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -570,7 +578,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
       // ================= TMA producer (both CTAs load their halves)
       int stage = 0;
       uint32_t phase = 0;
+      bool waited = !(peer_on(sync) && sync.wait);
       each_job([&](const PairJob& j) {
+        if (!waited && !j.aux) {
+          // first routed tile: rows from peers need every rank's dispatch (epoch B);
+          // the shared-expert tiles before it overlap the wait
+          peer_wait(sync, sync.state[0]);
+          fence_proxy_async_global();
+          waited = true;
+        }
         const int a_row = j.a_row + int(rank) * 128;
         const int b_row = j.b_row + int(rank) * 128;
         for (int kb = 0; kb < j.k_blocks; ++kb) {
@@ -646,6 +662,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
     tc_fence_after();
     tmem_dealloc_2sm<gg::kTmemCols>(tmem_base);
   }
+  if (peer_on(sync) && sync.total > 0) peer_arrive_and_raise(sync);
 }
 
 // ------------------------------------------------------------------ host side
@@ -679,7 +696,8 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
                         int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream, int pair,
                         const int32_t* scatter_src, __nv_bfloat16* const* scatter_ptrs, bool pdl,
-                        const AuxProblem* aux) {
+                        const AuxProblem* aux, const PeerSync* sync) {
+  const PeerSync ps = sync ? *sync : PeerSync();
   if (N % gg::BN != 0) return set_error(MP_E_SHAPE, "grouped GEMM N=%d not a multiple of %d", N, gg::BN);
   if (K % gg::BK != 0) return set_error(MP_E_SHAPE, "grouped GEMM K=%d not a multiple of %d", K, gg::BK);
   AuxProblem no_aux;
@@ -702,7 +720,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
     grid &= ~1;
     cudaError_t e = launch_pdl_if(pdl, grouped_gemm_2sm_kernel, dim3(grid), dim3(gg::kThreads), g2::kSmemBytes, stream, tmA,
                                tmB, gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src,
-                               scatter_ptrs, ax);
+                               scatter_ptrs, ax, ps);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_2sm_kernel launch");
     return MP_OK;
@@ -716,10 +734,15 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
   }
   if (grid <= 0) grid = kNumSMs;
   cudaError_t e = launch_pdl_if(pdl, grouped_gemm_kernel, dim3(grid), dim3(gg::kThreads), gg::kSmemBytes, stream, tmA, tmB,
-                             gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs);
+                             gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs, ps);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_kernel launch");
   return MP_OK;
+}
+
+int grouped_gemm_ctas(int grid, int pair) {
+  if (grid <= 0) grid = kNumSMs;
+  return pair ? (grid & ~1) : grid;
 }
 
 }  // namespace mp

@@ -36,6 +36,29 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   return launch_pdl_if(true, kernel, grid, block, smem, stream, static_cast<Args&&>(args)...);
 }
 
+// NVLink synchronisation folded into the layer's own kernels (G > 1).  Each
+// rank owns flags[G] in its window; "raise e" = st.release.sys e into
+// flags[rank] of every peer, "wait e" = ld.acquire.sys until every flags[p]
+// of this rank reached e.  The epoch lives in device memory (state[0]), so a
+// captured graph replays correctly: a raising kernel sets state[0] = e after
+// raising, and later kernels in stream order wait for state[0].
+//   router (last CTA)   publishes its batch counts, raises A   (count exchange)
+//   permute             waits A in its prologue; last CTA raises B (rows sent)
+//   GEMM1 producers     wait B before the first routed tile (the fused shared-
+//                       expert tiles go first and hide the wait)
+//   GEMM2 (both chains) last CTA of all raises C (rows returned)
+//   combine             waits C in its prologue
+struct PeerSync {
+  uint32_t* const* flag_ptrs = nullptr;  // [G] device array -> each rank's flags[G]
+  int32_t* const* count_ptrs = nullptr;  // [2][8] count-table halves (router only)
+  uint32_t* state = nullptr;             // [0] epoch, [1] forwards seen, [2] count parity
+  uint32_t* err = nullptr;               // timeout bits (mp_layer_check)
+  uint32_t* ticket = nullptr;            // arrival counter of a raising kernel
+  int G = 1, rank = 0;
+  int wait = 0;    // this launch waits for state[0] before touching peer-written rows
+  int total = 0;   // this launch raises once `total` CTAs (across launches sharing ticket) arrived
+};
+
 // Error state (thread-local, read through mp_last_error).
 int set_error(int code, const char* fmt, ...);
 int set_cuda_error(cudaError_t e, const char* what);
@@ -44,7 +67,7 @@ int set_cuda_error(cudaError_t e, const char* what);
 int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
-                  int32_t* blk_prefix, cudaStream_t stream);
+                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync = nullptr);
 int router_block_tokens();
 __host__ __device__ int router_e_pad(int E_tot);
 int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16* packed, cudaStream_t stream);
@@ -52,7 +75,8 @@ int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16*
 // ---- K2 permute (+ dispatch through peer pointers)
 int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
                    const uint32_t* parity, const int32_t* blk_prefix, int32_t* const* src_ptrs, int rank, int G, int T, int d, int E, int k,
-                   __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream);
+                   __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream,
+                   const PeerSync* sync = nullptr);
 
 // ---- K3 grouped GEMM
 // Where the GEMM takes its expert groups from (read in the kernel prologue).
@@ -86,17 +110,20 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream,
                         int pair = 0, const int32_t* scatter_src = nullptr,
                         __nv_bfloat16* const* scatter_ptrs = nullptr, bool pdl = true,
-                        const AuxProblem* aux = nullptr);
+                        const AuxProblem* aux = nullptr, const PeerSync* sync = nullptr);
+// CTAs a grouped-GEMM launch with this grid request runs (for PeerSync::total).
+int grouped_gemm_ctas(int grid, int pair);
 
 // ---- K5 combine (the expert outputs are already back in this GPU's return buffer)
 int launch_combine(const __nv_bfloat16* ret /*[T][k][d]*/, const float* w, int T, int d, int k,
                    const __nv_bfloat16* shared_y, const float* shared_gate, __nv_bfloat16* out,
-                   cudaStream_t stream);
+                   cudaStream_t stream, const PeerSync* sync = nullptr);
 
 // ---- exchange / barrier over NVLink peer memory
-int launch_publish_barrier(uint32_t* const* flag_ptrs /*[G] device array, each -> flags[G]*/,
-                           int32_t* const* count_ptrs /*[2][8] device array -> table halves, or null*/,
-                           const int32_t* my_counts, int E, int G, int rank, uint32_t* state /*[3] device*/,
-                           uint32_t* error_word, cudaStream_t stream);
+// Stand-ins when a raising kernel does not run (T == 0: no router / permute;
+// no local slots: no GEMM2): publish zero counts + raise A, then raise B
+// (`raise_count` = 2), or raise one epoch (`raise_count` = 1, counts unused).
+int launch_peer_sync(const PeerSync& sync, int32_t* batch_counts, int E, int raise_count, cudaStream_t stream);
+
 
 }  // namespace mp

@@ -1,0 +1,59 @@
+// Device side of PeerSync (mp_internal.h): the NVLink flag protocol folded into
+// the layer kernels.  All waits are bounded (kPeerTimeoutNs): on timeout the
+// missing ranks' bits are set in the error word that mp_layer_check reports,
+// and the kernel proceeds instead of hanging the GPU.
+#pragma once
+
+#include "common.cuh"
+#include "mp_internal.h"
+
+namespace mp {
+
+MP_DEV bool peer_on(const PeerSync& ps) { return ps.G > 1 && ps.flag_ptrs != nullptr; }
+
+// One thread: spin until every rank's flag in this rank's window reached `epoch`.
+MP_DEV void peer_wait(const PeerSync& ps, uint32_t epoch) {
+  const uint32_t* mine = ps.flag_ptrs[ps.rank];
+  for (int p = 0; p < ps.G; ++p) {
+    const uint64_t t0 = globaltimer_ns();
+    while (int32_t(ld_acquire_sys_u32(mine + p) - epoch) < 0) {
+      if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+        atomicOr(ps.err, 1u << p);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+}
+
+// One thread: raise `epoch` in every rank's window (flags[rank]).
+MP_DEV void peer_raise(const PeerSync& ps, uint32_t epoch) {
+  for (int p = 0; p < ps.G; ++p) st_release_sys_u32(ps.flag_ptrs[p] + ps.rank, epoch);
+}
+
+// Whole CTA, at kernel end: this CTA's peer stores are made visible system-wide
+// and counted; the CTA that completes `ps.total` arrivals raises the next epoch
+// and publishes it in state[0] for the kernels that follow in stream order.
+MP_DEV void peer_arrive_and_raise(const PeerSync& ps) {
+  __shared__ uint32_t s_last;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ps.ticket, 1u) == uint32_t(ps.total - 1) ? 1u : 0u;
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence_system();
+    const uint32_t e = ps.state[0] + 1;
+    peer_raise(ps, e);
+    ps.state[0] = e;
+    *ps.ticket = 0u;  // ready for the next forward (stream-ordered)
+  }
+}
+
+// Whole CTA, in a prologue: thread 0 waits for the epoch the preceding raising
+// kernel published; the rest of the CTA is released by the barrier.
+MP_DEV void peer_wait_cta(const PeerSync& ps) {
+  if (threadIdx.x == 0) peer_wait(ps, ps.state[0]);
+  __syncthreads();
+}
+
+}  // namespace mp

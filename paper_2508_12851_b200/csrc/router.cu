@@ -31,6 +31,7 @@
 
 #include "common.cuh"
 #include "mp_internal.h"
+#include "peer_sync.cuh"
 
 namespace mp {
 
@@ -94,7 +95,7 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
                   const float* __restrict__ bias, int T, int d, int E, int has_gate, int k, int score_mode,
                   int renorm, int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
                   uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
-                  uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix) {
+                  uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix, const PeerSync sync) {
   __shared__ float logits[rt::kTokens][rt::kMaxE + 9];
   __shared__ int cnt_s[rt::kMaxE];
   __shared__ uint64_t xbar;
@@ -311,19 +312,41 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
         run += cnt(blk);
       }
   }
+  // count exchange (G > 1): this origin's batch counts go into every rank's
+  // count table (half = forward parity), then epoch A is raised
+  if (peer_on(sync)) {
+    __syncthreads();
+    const uint32_t fwd = sync.state[1], par = fwd & 1u;
+    int32_t* const* half = sync.count_ptrs + 8 * par;
+    for (int i = tid; i < sync.G * E; i += blockDim.x) {
+      const int p = i / E, e2 = i - (i / E) * E;
+      half[p][sync.rank * E + e2] = batch_counts[e2];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t ep = sync.state[0] + 1;
+      peer_raise(sync, ep);
+      sync.state[0] = ep;
+      sync.state[1] = fwd + 1;
+      sync.state[2] = par;
+    }
+  }
   if (tid == 0) *ticket = 0u;  // ready for the next launch (stream-ordered)
 }
 
 int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
-                  int32_t* blk_prefix, cudaStream_t stream) {
+                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync) {
   if (batch_counts && !ticket) return set_error(MP_E_ARG, "router: batch counts need a ticket word");
   if (E < 1 || E > rt::kMaxE) return set_error(MP_E_SHAPE, "router: E=%d outside [1, %d]", E, rt::kMaxE);
   if (k < 1 || k > E || k > rt::kMaxK) return set_error(MP_E_SHAPE, "router: top_k=%d invalid for E=%d", k, E);
   if (d % 256 != 0) return set_error(MP_E_SHAPE, "router: d=%d not a multiple of 256", d);
   if (score_mode != 0 && score_mode != 1) return set_error(MP_E_ARG, "router: score_mode %d", score_mode);
   if (T <= 0) return MP_OK;
+  if (sync && sync->G > 1 && (!batch_counts || !blk_counts))
+    return set_error(MP_E_ARG, "router: the count exchange needs the batch counts");
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return set_error(MP_E_ARG, "router: x not 16-byte aligned");
   const int grid = (T + rt::kTokens - 1) / rt::kTokens;
   const size_t bc_bytes = blk_counts && batch_counts ? size_t(grid) * E * 4 : 0;
@@ -347,7 +370,7 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   }
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3((wide ? kMaxWarps : kQuads) * 32), smem, stream, x, wg_packed,
                              bias, T, d, E, has_gate ? 1 : 0, k, score_mode, renorm, idx, w, shared_gate, hist,
-                             blk_counts, batch_counts, ticket, blk_prefix);
+                             blk_counts, batch_counts, ticket, blk_prefix, sync ? *sync : PeerSync());
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_kernel launch");
 }

@@ -27,6 +27,9 @@ from paper_2508_12851_b200.shapes import LayerShape
 
 
 def check_close(got, ref, what):
+    if ref.size == 0:
+        assert got.size == 0, what
+        return
     err = float(np.abs(got - ref).max())
     scale = float(np.abs(ref).max())
     rel = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30))
@@ -135,6 +138,13 @@ def main():
     sets = [sorted(set(range(g * per, min(60, (g + 1) * per)))) for g in range(G)]
     sets2 = [sorted(set(range(g * per, min(60, (g + 1) * per))) | {(g * per + per + 2) % 60}) for g in range(G)]
     run_case(shape, G, rank, sets, sets2, [96 + 16 * s for s in range(G)], seed=3)
+
+    # case 4: an idle origin (T = 0 on rank 0: no router / permute launched there; it still
+    # publishes zero counts and its flags) next to busy ones, DeepSeek-like plan (fused shared)
+    shape = LayerShape("ds_small", d=256, f=256, E=64, k=6, score_mode=1, shared_f=512)
+    per = -(-64 // G)
+    sets = [sorted(set(range(g * per, min(64, (g + 1) * per))) | {(g * per + per) % 64}) for g in range(G)]
+    run_case(shape, G, rank, sets, sets, [0] + [120] * (G - 1), seed=4)
 
     dist.barrier()
     if rank == 0:
