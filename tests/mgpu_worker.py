@@ -36,7 +36,7 @@ def check_close(got, ref, what):
     assert err <= 2e-2 * scale + 1e-3 and rel <= 1e-2, f"{what}: max err {err} scale {scale} rel {rel}"
 
 
-def run_case(shape, G, rank, sets, sets2, T_list, seed):
+def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None):
     dev = torch.device("cuda", torch.cuda.current_device())
     E = shape.E
     experts = {e: orc.synthetic_expert(e, shape.d, shape.f, seed) for e in range(E)}
@@ -46,7 +46,7 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed):
     xs = [orc.synthetic_tokens(s, T_list[s], shape.d, seed) for s in range(G)]
     lat, bw = uniform_links(G)
 
-    cap = max(len(s) for s in sets + sets2)
+    cap = max(len(s) for s in sets + sets2) if caps is None else caps[rank]
     layer = B200MoELayer(shape, rank=rank, world=G, max_tokens=max(T_list), cap_slots=cap)
     layer.open_peers()
     layer.set_router(torch.from_numpy(wg[:E]), torch.from_numpy(biases[rank]),
@@ -145,6 +145,14 @@ def main():
     per = -(-64 // G)
     sets = [sorted(set(range(g * per, min(64, (g + 1) * per))) | {(g * per + per) % 64}) for g in range(G)]
     run_case(shape, G, rank, sets, sets, [0] + [120] * (G - 1), seed=4)
+
+    # case 5: a GPU with no expert memory at all (cap 0 -> no slots, no K3 launches; it still
+    # raises its return flag) while it keeps originating tokens
+    shape = LayerShape("toy_small", d=512, f=512, E=8, k=2)
+    holders = list(range(G - 1))
+    sets = [sorted(e for e in range(8) if e % len(holders) == g) if g < G - 1 else [] for g in range(G)]
+    caps = [max(len(x) for x in sets)] * (G - 1) + [0]
+    run_case(shape, G, rank, sets, sets, [100 + 20 * s for s in range(G)], seed=5, caps=caps)
 
     dist.barrier()
     if rank == 0:
