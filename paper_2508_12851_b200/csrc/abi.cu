@@ -96,10 +96,10 @@ struct mp_layer {
   CUtensorMap tm_recv, tm_w13, tm_h, tm_w2, tm_w13s, tm_hs, tm_w2s, tm_x;
   // B maps with 128-row boxes for the CTA-pair GEMM (each CTA loads half of N)
   CUtensorMap tm_w13_p, tm_w2_p, tm_w13s_p, tm_w2s_p;
-  int pair_routed = 0, pair_shared = 1, gemm_order = 0;
+  int pair_routed = 0, pair_shared = 1;
   // shared expert fused into the routed CTA-pair launches (one GEMM1 and one GEMM2
   // launch cover both problems; no per-launch tails / wave quantisation of its own)
-  int fuse_shared = 0, fuse_sched = 2;
+  int fuse_shared = 0;
   // small-group split: groups below split_m rows run on a side stream over small_grid SMs
   int split_m = 0, small_grid = 20;
   cudaStream_t side = nullptr;
@@ -326,9 +326,6 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   }
   // CTA pairs (256-row tiles) when the average expert group is large
   L->pair_routed = int64_t(D.world) * D.max_tokens * D.top_k >= int64_t(512) * D.E ? 1 : 0;
-  // tile order (0 = group-major) -- n-block-major interleaves weight-bound small groups with
-  // compute-bound large ones but loses the L2 reuse of each group's token tiles (measured slower)
-  L->gemm_order = 0;
   // many small expert groups (Qwen / DeepSeek): weight-bound small groups run concurrently
   // with the compute-bound large ones on a disjoint set of SMs
   L->split_m = D.E >= 16 ? 256 : 0;
@@ -344,10 +341,8 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
         (e = cudaEventCreateWithFlags(&L->ev_join, cudaEventDisableTiming)) != cudaSuccess)
       return fail(set_cuda_error(e, "cudaEventCreate(split)"));
   }
-  if (const char* env = getenv("MP_GEMM_ORDER")) L->gemm_order = atoi(env) ? 1 : 0;
   L->fuse_shared = (D.shared_f > 0 && D.n_slots > 0 && L->pair_routed && L->pair_shared) ? 1 : 0;
   if (const char* env = getenv("MP_FUSE_SHARED")) L->fuse_shared = L->fuse_shared && atoi(env) != 0;
-  if (const char* env = getenv("MP_FUSE_SCHED")) L->fuse_sched = atoi(env);
   if (D.shared_f > 0) {
     if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
       return fail(r);
@@ -590,7 +585,6 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     gs.G = G;
     gs.E = E;
     gs.rank = rank;
-    gs.order = L->gemm_order;
     const int pr = L->pair_routed;
     const int big_grid = L->split_m > 0 ? kNumSMs - L->small_grid : 0;
     // C is raised by the last GEMM2 CTA of both chains
@@ -633,7 +627,6 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       aux2.m = T;
       aux2.N = D.d;
       aux2.K = D.shared_f;
-      aux1.sched = aux2.sched = L->fuse_sched;
     }
     MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
                                big_grid, st, pr, nullptr, nullptr, pdl, fused ? &aux1 : nullptr, sw));

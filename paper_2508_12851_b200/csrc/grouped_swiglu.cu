@@ -49,10 +49,7 @@ struct GemmSmemTail {
   uint32_t tmem_base;
   int n_groups;
   int total_tiles;
-  int order;      // 0: (group, n, m) -- 1: (n, group, m)
-  int total_mb;   // sum of m-blocks over groups
   int tile_prefix[gg::kMaxGroups + 1];
-  int mb_prefix[gg::kMaxGroups + 1];
   int g_arow[gg::kMaxGroups];
   int g_m[gg::kMaxGroups];
   int g_slot[gg::kMaxGroups];
@@ -114,38 +111,23 @@ MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
   }
   __syncthreads();
   if (tid == 0) {
-    int acc = 0, mb = 0;
+    int acc = 0;
     st.tile_prefix[0] = 0;
-    st.mb_prefix[0] = 0;
     for (int g = 0; g < st.n_groups; ++g) {
       const int m_blocks = (st.g_m[g] + bm - 1) / bm;
       acc += m_blocks * n_blocks;
-      mb += m_blocks;
       st.tile_prefix[g + 1] = acc;
-      st.mb_prefix[g + 1] = mb;
     }
     st.total_tiles = acc;
-    st.total_mb = mb;
-    st.order = gs.order;
   }
 }
 
-// tile -> (group, n-block, m-block).  order 0 walks one group at a time (its
-// weight tiles are reused across its m-blocks while hot in L2); order 1 walks
-// n-blocks across all groups, so weight-bound small groups run concurrently
-// with compute-bound large ones.
+// tile -> (group, n-block, m-block): one group at a time, m fastest, so the
+// CTAs running concurrently share the group's weight tile in L2.  (An
+// n-block-major order that interleaves the groups was measured slower.)
 template <class Tail>
 MP_DEV TileCoord decode_any(const Tail& s, int tile, int n_blocks, int bm) {
   TileCoord c;
-  if (s.order == 1) {
-    c.n_blk = tile / s.total_mb;
-    const int r = tile - c.n_blk * s.total_mb;
-    int g = 0;
-    while (s.mb_prefix[g + 1] <= r) ++g;
-    c.g = g;
-    c.m_blk = r - s.mb_prefix[g];
-    return c;
-  }
   int g = 0;
   while (s.tile_prefix[g + 1] <= tile) ++g;
   const int local = tile - s.tile_prefix[g];
@@ -383,10 +365,7 @@ struct Gemm2SmemTail {
   uint32_t tmem_base;
   int n_groups;
   int total_tiles;
-  int order;      // 0: (group, n, m) -- 1: (n, group, m)
-  int total_mb;   // sum of m-blocks over groups
   int tile_prefix[gg::kMaxGroups + 1];
-  int mb_prefix[gg::kMaxGroups + 1];
   int g_arow[gg::kMaxGroups];
   int g_m[gg::kMaxGroups];
   int g_slot[gg::kMaxGroups];
@@ -408,13 +387,14 @@ struct PairJob {
   int g;               // routed group (aux: -1)
 };
 
-// Static schedule of one cluster: aux tiles round-robin (tile t -> cluster
-// t mod C), then routed tiles in up to two strided segments.
-//   sched 0  k-block-balanced contiguous ranges (closed form)
-//   sched 1  round-robin over the concatenated [aux | routed] list
-//   sched 2  round-robin (reversed cluster order), then the last routed tiles
-//            only to the clusters that drew one aux tile fewer
-// Without an aux problem every mode is the plain round-robin.
+// Static schedule of one cluster.  Without an aux problem: routed tiles
+// round-robin.  With one: aux tiles round-robin (tile t -> cluster t mod C),
+// then the routed tiles round-robin in reversed cluster order, except the last
+// few, which go only to the clusters that drew one aux tile fewer (about
+// aux K / routed K tiles each) -- so every cluster ends with about the same
+// number of k-blocks while concurrently running clusters still share weight
+// tiles in L2.  (Contiguous k-balanced ranges per cluster lose that sharing:
+// measured 30% slower.)
 struct PairSched {
   int A, aux_mb, aux_kb;
   int s1_begin, s1_end, s1_step;
@@ -428,53 +408,24 @@ MP_DEV PairSched make_sched(const AuxProblem& aux, int R, int k_blocks, int clus
   ps.aux_kb = aux.K / g2::BK;
   ps.s2_begin = ps.s2_end = 0;
   ps.s2_step = 1;
-  const int A = ps.A;
-  if (A == 0) {
+  if (ps.A == 0) {
     ps.s1_begin = cluster_id;
     ps.s1_end = R;
     ps.s1_step = C;
     return ps;
   }
-  const int q = A / C, rem = A - (A / C) * C;
-  if (aux.sched == 1) {
-    ps.s1_begin = ((cluster_id - A) % C + C) % C;
-    ps.s1_end = R;
-    ps.s1_step = C;
-    return ps;
+  const int rem = ps.A % C;
+  const int extra = rem > 0 ? (ps.aux_kb + k_blocks / 2) / k_blocks : 0;
+  const int X = min(R, (C - rem) * extra);
+  const int R1 = R - X;
+  ps.s1_begin = C - 1 - cluster_id;
+  ps.s1_end = R1;
+  ps.s1_step = C;
+  if (cluster_id >= rem && X > 0) {
+    ps.s2_begin = R1 + (cluster_id - rem);
+    ps.s2_end = R;
+    ps.s2_step = C - rem;
   }
-  if (aux.sched == 2) {
-    // clusters c >= rem drew q aux tiles, the others q + 1: give the former
-    // about ca/cr routed tiles more each, from the end of the list
-    const int extra = rem > 0 ? (ps.aux_kb + k_blocks / 2) / k_blocks : 0;
-    const int X = min(R, (C - rem) * extra);
-    const int R1 = R - X;
-    ps.s1_begin = C - 1 - cluster_id;
-    ps.s1_end = R1;
-    ps.s1_step = C;
-    if (cluster_id >= rem && X > 0) {
-      ps.s2_begin = R1 + (cluster_id - rem);
-      ps.s2_end = R;
-      ps.s2_step = C - rem;
-    }
-    return ps;
-  }
-  // sched 0: F(c) = c * total - C * ca * (#aux tiles of clusters < c), in (k-blocks x C)
-  const long long ca = ps.aux_kb, cr = k_blocks, total = ca * A + cr * R;
-  long long run = 0;
-  auto start_of = [&](int c, long long& best) -> int {
-    if (c >= C) return R;
-    const long long F = c * total - C * ca * ((long long)c * q + min(c, rem));
-    best = F > best ? F : best;
-    long long t = (best + C * cr / 2) / (C * cr);
-    return int(t < 0 ? 0 : (t > R ? R : t));
-  };
-  int b = 0;
-  for (int c = 1; c <= cluster_id; ++c) b = start_of(c, run);
-  ps.s1_begin = cluster_id == 0 ? 0 : b;
-  long long run2 = run;
-  ps.s1_end = start_of(cluster_id + 1, run2);
-  if (ps.s1_end < ps.s1_begin) ps.s1_end = ps.s1_begin;
-  ps.s1_step = 1;
   return ps;
 }
 

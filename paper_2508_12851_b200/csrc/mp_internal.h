@@ -90,7 +90,6 @@ struct GroupSpec {
   int G = 1, E = 0, rank = 0;
   int single_m = 0;                   // mode 2: one group {0, single_m, slot 0, 0}
   int mode = 0;
-  int order = 0;                      // tile order: 0 group-major, 1 n-block-major
   int m_lo = 0, m_hi = 1 << 30;       // mode 1: only groups with m_lo <= m < m_hi
 };
 // A second, dense problem fused into the same CTA-pair launch (the shared
@@ -102,7 +101,6 @@ struct alignas(64) AuxProblem {
   __nv_bfloat16* out = nullptr;   // [m, out_ld]
   int out_ld = 0;
   int m = 0, N = 0, K = 0;        // m == 0: no aux problem
-  int sched = 0;                  // tile schedule (grouped_swiglu.cu: make_sched)
 };
 int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,

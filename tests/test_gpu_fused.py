@@ -1,8 +1,8 @@
 """Shared expert fused into the routed CTA-pair launches (K3 plan `fuse_shared`).
 
 The fused launch only reschedules whole 256x256 tiles (aux tiles round-robin,
-routed tiles in k-block-balanced contiguous ranges); each tile's k-loop order is
-unchanged, so the layer output must be BIT-IDENTICAL to the unfused plan (shared
+routed tiles round-robin with a deficit tail for the clusters that drew fewer
+aux tiles); each tile's k-loop order is unchanged, so the layer output must be BIT-IDENTICAL to the unfused plan (shared
 expert in its own two launches) for every token count and cluster count.  The
 unfused plan itself is checked against the oracle in test_gpu_layer.py.
 """
