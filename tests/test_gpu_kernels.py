@@ -108,8 +108,53 @@ def test_grouped_gemm_large_k_many_tiles(pair, monkeypatch):
     assert rel < 1e-2, rel
 
 
+def _run_router(x, wg, bias, E, k, mode, gate):
+    L, lib = _lib()
+    T, d = x.shape
+    xt = torch.from_numpy(x).cuda().bfloat16()
+    wgt = torch.from_numpy(wg).cuda().bfloat16()
+    packed = torch.empty((E + gate + 7) // 8 * 8 * d, device="cuda", dtype=torch.bfloat16)
+    L.check(lib.mp_router_pack(_vp(wgt), E + gate, d, _vp(packed), _stream()))
+    bt = torch.from_numpy(bias).cuda()
+    idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    w = torch.empty(T, k, dtype=torch.float32, device="cuda")
+    go = torch.empty(T, dtype=torch.float32, device="cuda")
+    hist = torch.zeros(E, dtype=torch.int32, device="cuda")
+    L.check(lib.mp_router_topk_hist(_vp(xt), _vp(packed), _vp(bt), T, d, E, gate, k, mode, 0, _vp(idx), _vp(w),
+                                    _vp(go) if gate else None, _vp(hist), _stream()))
+    torch.cuda.synchronize()
+    return idx.cpu().numpy(), w.cpu().numpy(), hist.cpu().numpy()
+
+
+@pytest.mark.parametrize("E,k,mode,d", [(8, 2, 0, 512), (64, 6, 1, 256), (16, 4, 0, 4096)])
+def test_router_ties_go_to_the_lower_expert(E, k, mode, d):
+    """Exact logit ties (duplicated router rows + biases, all-zero tokens whose logits are the
+    biases alone) resolve to the lower expert id, bit-exact with the oracle -- in every router
+    variant (8-warp, 16-warp with x in smem, 16-warp with x from HBM)."""
+    T = 96
+    x = orc.synthetic_tokens(0, T, d, seed=7)
+    x[::3] = 0.0                       # every third token: logits == bias
+    wg = orc.synthetic_router(E, d, seed=7)
+    bias = orc.origin_bias(0, E, seed=7)
+    for a, b in [(2, 5), (1, E - 1)]:  # identical experts
+        wg[b] = wg[a]
+        bias[b] = bias[a]
+    bias[3] = bias[4] = bias[6] = np.float32(bias.max())   # three-way tie among the biases
+    lg = orc.router_logits(x, wg, bias)
+    idx_ref, w_ref = orc.topk_route(lg, E, k, mode)
+    idx, w, hist = _run_router(x, wg, bias, E, k, mode, 0)
+    assert np.array_equal(idx, idx_ref)
+    assert np.array_equal(hist, orc.histogram(idx_ref, E))
+    np.testing.assert_allclose(w, w_ref, rtol=1e-5, atol=1e-6)
+    for row in idx[::3]:               # zero tokens: 3 < 4 < 6 when tied at the top
+        pos = {int(e): i for i, e in enumerate(row)}
+        for lo, hi in [(3, 4), (4, 6), (2, 5)]:
+            if lo in pos and hi in pos:
+                assert pos[lo] < pos[hi], row
+
+
 @pytest.mark.parametrize("E,k,mode,gate,d,T", [(8, 2, 0, 0, 512, 333), (64, 6, 1, 0, 256, 200), (60, 4, 1, 1, 512, 64),
-                                               (8, 2, 0, 0, 4096, 48)])
+                                               (8, 2, 0, 0, 4096, 48), (16, 4, 0, 0, 4096, 100)])
 def test_router_bit_exact(E, k, mode, gate, d, T):
     L, lib = _lib()
     x = orc.synthetic_tokens(0, T, d, seed=3)
