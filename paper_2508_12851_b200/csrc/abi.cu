@@ -698,7 +698,7 @@ int mp_layer_check(mp_layer* L, void* stream) {
   MP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   uint32_t err = 0;
   MP_CUDA(cudaMemcpy(&err, L->err, 4, cudaMemcpyDeviceToHost));
-  if (err) return set_error(MP_E_PEER, "NVLink barrier timed out waiting for ranks mask 0x%x", err);
+  if (err) return set_error(MP_E_PEER, "NVLink flag wait timed out on ranks mask 0x%x", err);
   return MP_OK;
 }
 

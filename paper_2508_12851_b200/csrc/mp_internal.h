@@ -117,7 +117,7 @@ int launch_combine(const __nv_bfloat16* ret /*[T][k][d]*/, const float* w, int T
                    const __nv_bfloat16* shared_y, const float* shared_gate, __nv_bfloat16* out,
                    cudaStream_t stream, const PeerSync* sync = nullptr);
 
-// ---- exchange / barrier over NVLink peer memory
+// ---- stand-in flag raises over NVLink peer memory (exchange.cu)
 // Stand-ins when a raising kernel does not run (T == 0: no router / permute;
 // no local slots: no GEMM2): publish zero counts + raise A, then raise B
 // (`raise_count` = 2), or raise one epoch (`raise_count` = 1, counts unused).

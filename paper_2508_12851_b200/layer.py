@@ -383,7 +383,7 @@ class HostPipeline:
 def capture_graph(fn, warmup: int = 1):
     """Capture fn() (a sequence of layer forwards on static buffers) into a CUDA graph.
 
-    The forward is graph-safe: no host synchronisation, barrier epochs and
+    The forward is graph-safe: no host synchronisation, flag epochs and
     count-table parity live on the device, every tensor map is bound to a
     static buffer.  Warm-up calls run eagerly first (attribute setup).
     """
