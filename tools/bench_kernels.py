@@ -88,6 +88,18 @@ def main():
         us = timeit(lambda: _lib.check(lib.mp_grouped_gemm(vp(h), T * k, vp(b2), E * d, vp(groups), vp(ng), d, shape.f,
                                                            vp(y), d, 0, st)), args.iters)
         res["gemm2_uniform"] = {"us": us, "TFLOP/s": fl / 2 / us / 1e6}
+        # the same expert FLOPs through cuBLAS (torch.bmm over the E groups, no SwiGLU / scatter):
+        # a same-box, same-clock yardstick for the tcgen05 kernels above
+        a3 = a.view(E, M, d)
+        w13 = b13.view(E, 2 * shape.f, d).transpose(1, 2)
+        h3 = torch.empty(E, M, 2 * shape.f, device=dev, dtype=torch.bfloat16)
+        us = timeit(lambda: torch.bmm(a3, w13, out=h3), args.iters)
+        res["cublas_bmm1"] = {"us": us, "TFLOP/s": fl / us / 1e6}
+        hh = h.view(E, M, shape.f)
+        w2 = b2.view(E, d, shape.f).transpose(1, 2)
+        y3 = torch.empty(E, M, d, device=dev, dtype=torch.bfloat16)
+        us = timeit(lambda: torch.bmm(hh, w2, out=y3), args.iters)
+        res["cublas_bmm2"] = {"us": us, "TFLOP/s": fl / 2 / us / 1e6}
     print(json.dumps({"config": shape.name, "T": T, **res}))
 
 
