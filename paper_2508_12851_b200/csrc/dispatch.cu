@@ -30,7 +30,8 @@ namespace mp {
 //     sources for e (from the exchanged counts C[G][E] and the route table);
 //   * prefix[e]: rows of expert e in this origin's earlier router blocks
 //     (scanned once by the router's last CTA into blk_prefix).
-// Phase 1: one thread per (token, slot) pair computes its stable in-block rank.
+// Phase 1: one thread per (token, slot) pair computes its stable in-block rank
+//          (__match_any_sync within a warp, a per-expert prefix across warps).
 // Phase 2: one warp per token loads the x row once (16 B per lane per step) and
 //          stores it to its k destinations, local or peer (NVLink) rows.
 template <int kVecPerLane>
@@ -47,6 +48,7 @@ __global__ void __launch_bounds__(256)
   __shared__ int s_row[kTok * 8];
   __shared__ int C[8][64], R[8][64];
   __shared__ int base_s[64];
+  __shared__ int wcnt[8][64];  // per-warp, per-expert pair counts -> exclusive prefix over warps
   const int b = blockIdx.x;
   const int t0 = b * kTok;
   const int nt = min(kTok, T - t0);
@@ -63,6 +65,7 @@ __global__ void __launch_bounds__(256)
     R[i / E][i % E] = route[i];
   }
   if (tid < np) s_e[tid] = idx[size_t(t0) * k + tid];
+  for (int i = tid; i < 8 * 64; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   if (tid < E) {
     const int e = tid, D = R[rank][e];
@@ -74,11 +77,30 @@ __global__ void __launch_bounds__(256)
       if (R[s][e] == D) base += C[s][e];
     base_s[e] = base;
   }
+  // stable in-block rank of each pair among the block's pairs of the same expert:
+  // within a warp from __match_any_sync, across warps from a per-expert prefix
+  const int w = tid >> 5, l = tid & 31;
+  const int e_my = tid < np ? s_e[tid] : -1;
+  const unsigned act = __ballot_sync(0xffffffffu, tid < np);
+  int lrank = 0;
+  if (tid < np) {
+    const unsigned m = __match_any_sync(act, e_my);
+    lrank = __popc(m & ((1u << l) - 1u));
+    if (lrank == 0) wcnt[w][e_my] = __popc(m);
+  }
+  __syncthreads();
+  if (tid < E) {
+    int run = 0;
+    for (int w2 = 0; w2 < 8; ++w2) {
+      const int c = wcnt[w2][tid];
+      wcnt[w2][tid] = run;
+      run += c;
+    }
+  }
   __syncthreads();
   if (tid < np) {
-    const int e = s_e[tid];
-    int r = 0;
-    for (int q = 0; q < tid; ++q) r += (s_e[q] == e);
+    const int e = e_my;
+    const int r = wcnt[w][e] + lrank;
     const int dst = R[rank][e];
     const int row = base_s[e] + r;
     s_dst[tid] = dst;
