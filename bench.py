@@ -500,8 +500,11 @@ def main_b200(args):
         "stages_note": "side_chain_ms = [span of the small-group chain on the side stream, GEMM start -> its end]; "
                        "per-stage means from a diagnostic pass with events at every boundary (max over ranks); "
                        "the timed region records only the K3 boundaries",
-        "roofline": {"bound": "tensor", "kernel": f"grouped_gemm_kernel (GEMM1+SwiGLU, GEMM2), rank {hot} "
-                                                  "(most routed rows)"
+        "roofline": {"bound": "tensor",
+                     "kernel": ("grouped_gemm_2sm_kernel" if exec_plan["pair_routed"] else "grouped_gemm_kernel")
+                               + f" (GEMM1+SwiGLU, GEMM2), rank {hot} (most routed rows)"
+                               + ("; small groups on grouped_gemm_kernel over a side stream"
+                                  if exec_plan["split_m"] else "")
                                                   + ("; shared expert fused into the same launches"
                                                      if exec_plan["fuse_shared"] else ""),
                      "achieved_per_rank": per_rank_tf,
