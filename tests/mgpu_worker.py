@@ -116,7 +116,9 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None):
 def main():
     dist.init_process_group("gloo")
     rank, G = dist.get_rank(), dist.get_world_size()
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    # more ranks than GPUs (e.g. G = 8 on a 4-GPU box) share GPUs round-robin: the protocol
+    # and layouts are exercised at that G, the co-resident processes time-slice the GPU
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count())
 
     # case 1: toy-like shape, replicated experts; origins with different T (ragged)
     shape = LayerShape("toy_small", d=512, f=512, E=8, k=2)
