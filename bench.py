@@ -401,7 +401,7 @@ def main_b200(args):
     e2e_ms = e0.elapsed_time(e1)
     layer.check()
     # the host copy of the last output is the layer's output
-    assert torch.equal(oh[(K - 1) % N_ROTATE], pipe.od[(pipe.n - 1) & 1].cpu())
+    assert torch.equal(oh[(K - 1) % N_ROTATE], pipe.od[(pipe.n - 1) % pipe.depth].cpu())
 
     # ---- max over ranks
     vals = torch.tensor([t_ms, e2e_ms, float(np.median(step_ms))], dtype=torch.float64, device=dev)

@@ -337,34 +337,36 @@ class HostPipeline:
 
     Serving-style end-to-end path: batch i's host->device copy runs on a copy-in
     stream while batch i-1 is in the layer and batch i-2's output drains on a
-    copy-out stream (PCIe is full duplex), with double-buffered device tensors.
+    copy-out stream (PCIe is full duplex), with `depth` device buffers per
+    direction so a slow copy of one batch does not stall the next batch's layer.
     Each batch still crosses the host boundary in full: x in, layer output out.
     """
 
-    def __init__(self, layer: B200MoELayer, T: int):
+    def __init__(self, layer: B200MoELayer, T: int, depth: int = 2):
         self.layer = layer
         dev = layer.device
         d = layer.shape.d
-        self.xd = [torch.empty(T, d, device=dev, dtype=torch.bfloat16) for _ in range(2)]
-        self.od = [torch.empty(T, d, device=dev, dtype=torch.bfloat16) for _ in range(2)]
+        self.depth = depth  # device buffers per direction (batches in flight)
+        self.xd = [torch.empty(T, d, device=dev, dtype=torch.bfloat16) for _ in range(depth)]
+        self.od = [torch.empty(T, d, device=dev, dtype=torch.bfloat16) for _ in range(depth)]
         self.s_in = torch.cuda.Stream(dev)
         self.s_out = torch.cuda.Stream(dev)
         self.compute = torch.cuda.current_stream(dev)
-        self.ev_in = [torch.cuda.Event() for _ in range(2)]
-        self.ev_comp = [torch.cuda.Event() for _ in range(2)]
-        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.ev_in = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_out = [torch.cuda.Event() for _ in range(depth)]
         self.n = 0
 
     def submit(self, x_host: torch.Tensor, out_host: torch.Tensor) -> None:
         """Enqueue one batch: x_host [T, d] pinned bf16 -> layer -> out_host [T, d] pinned bf16."""
-        b = self.n & 1
-        if self.n >= 2:
-            self.s_in.wait_event(self.ev_comp[b])      # xd[b] free once batch n-2 left the layer
+        b = self.n % self.depth
+        if self.n >= self.depth:
+            self.s_in.wait_event(self.ev_comp[b])      # xd[b] free once batch n-depth left the layer
         with torch.cuda.stream(self.s_in):
             self.xd[b].copy_(x_host, non_blocking=True)
             self.ev_in[b].record(self.s_in)
         self.compute.wait_event(self.ev_in[b])
-        if self.n >= 2:
+        if self.n >= self.depth:
             self.compute.wait_event(self.ev_out[b])    # od[b] drained to the host
         with torch.cuda.stream(self.compute):
             self.layer.forward(self.xd[b], self.od[b])

@@ -128,3 +128,28 @@ def test_route_to_unplaced_expert_raises():
     with pytest.raises(UnplacedExpertError):
         layer.set_routes(np.zeros((1, shape.E), np.int32), bad_slots)
     layer.close()
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3])
+def test_host_pipeline_matches_device_forward(depth):
+    """HostPipeline (the bench's e2e path): pinned host batches in, host outputs out, copies on
+    their own streams with `depth` device buffers -- every host output equals the device-side
+    forward of the same batch."""
+    from paper_2508_12851_b200.layer import HostPipeline
+    shape = _shape("toy")
+    T = 96
+    experts, shared, wg = _weights(shape)
+    bias = orc.origin_bias(0, shape.E, seed=2)
+    layer = _build_layer(shape, T, experts, shared, wg, bias)
+    xs = [torch.from_numpy(orc.synthetic_tokens(0, T, shape.d, seed=20 + i)).bfloat16() for i in range(5)]
+    ref = [layer.forward(x.cuda()).cpu() for x in xs]
+    xh = [x.pin_memory() for x in xs]
+    oh = [torch.empty(T, shape.d, dtype=torch.bfloat16).pin_memory() for _ in xs]
+    pipe = HostPipeline(layer, T, depth=depth)
+    for x, o in zip(xh, oh):
+        pipe.submit(x, o)
+    pipe.drain()
+    torch.cuda.synchronize()
+    for i in range(len(xs)):
+        assert torch.equal(oh[i], ref[i]), i
+    layer.close()
