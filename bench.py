@@ -676,8 +676,7 @@ def main_shift(args):
     set_phase(E // 2)
     layer.reset_counts()
     tps_b_static, win_s = run(args.steps)
-    counts_b = all_counts()
-    acc_b_static = dispatch_accounting(counts_b, layer.route, shape.d)
+    acc_b_static = dispatch_accounting(all_counts(), layer.route, shape.d)
 
     # ---- migration check (sim.py:465-481) with measured costs
     # remote penalty per token-unit: wire time of one remote invocation (activations out, results
@@ -686,45 +685,23 @@ def main_shift(args):
     from paper_2508_12851_b200.calibrate import remote_penalty_seconds
     penalty = remote_penalty_seconds(shape.d, bw_probe)
     cluster = cluster_spec(shape, G, caps, link_bandwidth=bw_probe, load_bandwidth=bw_probe)
-    candidate, stats_b = placement_from(counts_b)
-    snapshot = mp.CostSnapshot(stats_b, penalty, 0.0, win_s)
-    decision, ledger = mp.should_migrate(pa, candidate, snapshot, cluster, model, "loads-only")
-    sets_b = gpu_expert_sets(candidate, 0)
+    from paper_2508_12851_b200.controller import MigrationController
+    ctl = MigrationController(layer, cluster, model, pa, strategy="ours", seed=seed, mode="loads-only",
+                              penalty_seconds=penalty)
+    adopt, ledger, candidate = ctl.check(win_s)      # window = the static phase-B run
     mig = {"decision": ledger["decision"], "cost_current_seconds": ledger["cost_current_seconds"],
            "cost_candidate_seconds": ledger["cost_candidate_seconds"],
            "migration_seconds_model": ledger["migration_seconds"], "penalty_seconds_per_token": penalty,
            "peer_copy_GBps": bw_probe / 1e9}
     tps_b_mig, acc_b_mig = None, None
-    if decision:
-        slot_maps = [None] * world
-        if world > 1:
-            dist.all_gather_object(slot_maps, layer.slot_of.tolist())
-        else:
-            slot_maps = [layer.slot_of.tolist()]
-        side = torch.cuda.Stream(dev)
-        e0, done = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        side.wait_stream(stream)
-        e0.record(side)
-        adds = layer.migrate_async(sets_a, sets_b, slot_maps, side, done)
+    if adopt:
         # traffic keeps flowing on the old placement while the weights move (a fixed number of
         # forwards on every rank: the layer is SPMD across GPUs)
-        overlap_steps = 3
-        for i in range(overlap_steps):
-            layer.forward(xs[i % N_ROTATE], out)
-        done.synchronize()
-        torch.cuda.synchronize()
-        copy_ms = e0.elapsed_time(done)
-        if world > 1:
-            dist.barrier()
-        layer.finish_migration(sets_b, adds)
-        n_add = torch.tensor([len(adds)], device=dev)
-        t_copy = torch.tensor([copy_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(n_add)
-            dist.all_reduce(t_copy, op=dist.ReduceOp.MAX)
-        mig.update({"slots_copied": int(n_add.item()), "bytes_copied": int(n_add.item()) * shape.expert_bytes,
-                    "copy_ms_max_gpu": t_copy.item(), "forwards_during_copy_rank0": overlap_steps})
-        layer.reset_counts()
+        def overlap():
+            for i in range(3):
+                layer.forward(xs[i % N_ROTATE], out)
+            return 3
+        mig.update(ctl.migrate(candidate, torch.cuda.Stream(dev), overlap))
         tps_b_mig, _ = run(args.steps)
         acc_b_mig = dispatch_accounting(all_counts(), layer.route, shape.d)
 

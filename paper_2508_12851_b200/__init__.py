@@ -12,7 +12,7 @@ from .shapes import DEEPSEEK, MIXTRAL, QWEN, SHAPES, TOY, LayerShape, get_shape,
 from .routing import dispatch_accounting, route_table, route_table_for, slot_map
 
 __all__ = [
-    "B200MoELayer", "DEEPSEEK", "DimensionMismatch", "InfeasibleError", "LayerShape", "MIXTRAL", "QWEN",
+    "B200MoELayer", "DEEPSEEK", "MigrationController", "DimensionMismatch", "InfeasibleError", "LayerShape", "MIXTRAL", "QWEN",
     "SHAPES", "TOY", "UnplacedExpertError", "dispatch_accounting", "get_shape", "route_table",
     "route_table_for", "slot_caps", "slot_map",
 ]
@@ -23,4 +23,7 @@ def __getattr__(name):
     if name == "B200MoELayer":
         from .layer import B200MoELayer
         return B200MoELayer
+    if name == "MigrationController":
+        from .controller import MigrationController
+        return MigrationController
     raise AttributeError(name)

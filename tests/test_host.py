@@ -110,3 +110,38 @@ def test_interleave_w13_layout():
     w13 = interleave_w13(w1, w3)
     assert torch.equal(w13[0:128], w1[0:128]) and torch.equal(w13[128:256], w3[0:128])
     assert torch.equal(w13[256:384], w1[128:256]) and torch.equal(w13[384:512], w3[128:256])
+
+
+@pytest.mark.parametrize("penalty,expect", [(2.5e-8, False), (1e-4, True)])
+def test_migration_controller_check_is_the_reference_decision(penalty, expect):
+    """MigrationController.check == build_placement + should_migrate of the reference on the
+    same window statistics (_migration_check, sim.py:465-481), for a drifted window."""
+    mp = import_moeplace()
+    if mp is None:
+        pytest.skip("reference package not importable")
+    from types import SimpleNamespace
+
+    from paper_2508_12851_b200 import workload as wl
+    from paper_2508_12851_b200.controller import MigrationController
+    from paper_2508_12851_b200.shapes import cluster_spec, model_spec
+
+    shape, G = DEEPSEEK, 4
+    caps = slot_caps(shape, G)
+    cluster, model = cluster_spec(shape, G, caps), model_spec(shape)
+    T, k = 4096, shape.k
+    counts_a = np.stack([np.rint(T * k * wl.origin_dist(g, shape.E)) for g in range(G)]).astype(np.int64)
+    counts_b = np.stack([np.roll(c, shape.E // 2) for c in counts_a])
+    stats_a = mp.ActivationStats.from_counts(counts_a[:, None, :].astype(float), (shape.E,))
+    current = mp.build_placement("ours", cluster, model, stats_a, 0)
+    fake = SimpleNamespace(gathered_counts=lambda group=None: counts_b, shape=shape, world=1,
+                           reset_counts=lambda: None)
+    window = 0.05
+    ctl = MigrationController(fake, cluster, model, current, penalty_seconds=penalty)
+    adopt, ledger, cand = ctl.check(window)
+    stats_b = mp.ActivationStats.from_counts(counts_b[:, None, :].astype(float), (shape.E,))
+    ref_cand = mp.build_placement("ours", cluster, model, stats_b, 0)
+    ref_adopt, ref_ledger = mp.should_migrate(current, ref_cand, mp.CostSnapshot(stats_b, penalty, 0.0, window),
+                                              cluster, model, "loads-only")
+    assert adopt == bool(ref_adopt) == expect
+    assert ledger == ref_ledger
+    assert routing.gpu_expert_sets(cand, 0) == routing.gpu_expert_sets(ref_cand, 0)
