@@ -28,8 +28,11 @@ MP_SCORE_TOPK_SOFTMAX = 0
 MP_SCORE_SOFTMAX_TOPK = 1
 NUM_STAGE_EVENTS = 13
 MAIN_STAGE_EVENTS = 11  # 11, 12: side-chain start / end (side stream, split plan only)
-STAGES = ("router", "count_exchange", "unused", "permute_dispatch", "shared_expert", "dispatch_barrier",
-          "gemm1_swiglu", "gemm2", "return_barrier", "combine_return")
+# Intervals between consecutive stage events.  The count exchange and the dispatch / return
+# waits are folded into the router, permute, GEMM and combine kernels (PeerSync), so their
+# intervals only hold event overhead; "shared_expert" is empty when the plan fuses it into K3.
+STAGES = ("router", "unused", "unused", "permute_dispatch", "shared_expert", "unused",
+          "gemm1_swiglu", "gemm2", "unused", "combine_return")
 GEMM_START, GEMM1_END, GEMM_END = 6, 7, 8
 CFG_KEYS = {"pair_routed": 0, "split_m": 1, "small_grid": 2, "fuse_shared": 3}
 
