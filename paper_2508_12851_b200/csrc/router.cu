@@ -351,24 +351,29 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   const int grid = (T + rt::kTokens - 1) / rt::kTokens;
   const size_t bc_bytes = blk_counts && batch_counts ? size_t(grid) * E * 4 : 0;
   if (bc_bytes > 200 * 1024) return set_error(MP_E_SHAPE, "router: %d blocks x %d experts too large", grid, E);
-  static const int wide_env = [] {
-    const char* v = getenv("MP_ROUTER_WIDE");
-    return v ? atoi(v) : -1;
-  }();
-  const bool wide = wide_env >= 0 ? wide_env != 0 : router_e_pad(E + (has_gate ? 1 : 0)) >= 2 * kExpPerPass;
+  // variant: 0 = 8 warps, x from HBM (one expert pass); 1 = 16 warps, x from HBM;
+  // 2 = 16 warps, x rows in smem; 3 = 8 warps, x rows in smem (MP_ROUTER_VARIANT overrides)
+  const char* venv = getenv("MP_ROUTER_VARIANT");
+  const int variant_env = venv ? atoi(venv) : -1;
   const size_t x_bytes = size_t(rt::kTokens) * d * 2;
-  const bool xsmem = wide && x_bytes <= 160 * 1024;
-  auto kern = xsmem ? router_kernel<kMaxWarps, true>
-                    : (wide ? router_kernel<kMaxWarps, false> : router_kernel<kQuads, false>);
-  const int variant = xsmem ? 2 : (wide ? 1 : 0);
+  const bool multi_pass = router_e_pad(E + (has_gate ? 1 : 0)) >= 2 * kExpPerPass;
+  int variant = multi_pass ? (x_bytes <= 160 * 1024 ? 2 : 1) : 0;
+  if (variant_env >= 0 && variant_env <= 3) variant = variant_env;
+  if ((variant == 2 || variant == 3) && x_bytes > 160 * 1024) variant = variant == 2 ? 1 : 0;
+  using KernT = decltype(&router_kernel<kQuads, false>);
+  const KernT kerns[4] = {router_kernel<kQuads, false>, router_kernel<kMaxWarps, false>,
+                          router_kernel<kMaxWarps, true>, router_kernel<kQuads, true>};
+  const KernT kern = kerns[variant];
+  const bool xsmem = variant >= 2;
+  const int warps = (variant == 1 || variant == 2) ? kMaxWarps : kQuads;
   const size_t smem = std::max(bc_bytes, xsmem ? x_bytes : size_t(0));
-  static size_t smem_set[3] = {0, 0, 0};
+  static size_t smem_set[4] = {0, 0, 0, 0};
   if (smem > 48 * 1024 && smem > smem_set[variant]) {
     cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (ea != cudaSuccess) return set_cuda_error(ea, "cudaFuncSetAttribute(router)");
     smem_set[variant] = smem;
   }
-  cudaError_t e = launch_pdl(kern, dim3(grid), dim3((wide ? kMaxWarps : kQuads) * 32), smem, stream, x, wg_packed,
+  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(warps * 32), smem, stream, x, wg_packed,
                              bias, T, d, E, has_gate ? 1 : 0, k, score_mode, renorm, idx, w, shared_gate, hist,
                              blk_counts, batch_counts, ticket, blk_prefix, sync ? *sync : PeerSync());
   if (e == cudaSuccess) e = cudaGetLastError();
