@@ -31,9 +31,9 @@ __global__ void __launch_bounds__(256)
       half[p][ps.rank * E + e] = 0;
     }
   }
-  __threadfence_system();
   __syncthreads();
   if (tid == 0) {
+    __threadfence_system();
     uint32_t ep = ps.state[0];
     peer_raise(ps, ++ep);
     if (raise_count == 2) {

@@ -35,17 +35,18 @@ MP_DEV void peer_raise(const PeerSync& ps, uint32_t epoch) {
 // and counted; the CTA that completes `ps.total` arrivals raises the next epoch
 // and publishes it in state[0] for the kernels that follow in stream order.
 MP_DEV void peer_arrive_and_raise(const PeerSync& ps) {
-  __shared__ uint32_t s_last;
-  __threadfence_system();
+  // the CTA barrier orders every thread's stores before thread 0's system-scope
+  // fence (cumulative), as in a cooperative grid barrier: one fence per CTA
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(ps.ticket, 1u) == uint32_t(ps.total - 1) ? 1u : 0u;
-  __syncthreads();
-  if (s_last && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     __threadfence_system();
-    const uint32_t e = ps.state[0] + 1;
-    peer_raise(ps, e);
-    ps.state[0] = e;
-    *ps.ticket = 0u;  // ready for the next forward (stream-ordered)
+    if (atomicAdd(ps.ticket, 1u) == uint32_t(ps.total - 1)) {
+      __threadfence_system();
+      const uint32_t e = ps.state[0] + 1;
+      peer_raise(ps, e);
+      ps.state[0] = e;
+      *ps.ticket = 0u;  // ready for the next forward (stream-ordered)
+    }
   }
 }
 

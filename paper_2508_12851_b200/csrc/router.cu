@@ -322,9 +322,9 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
       const int p = i / E, e2 = i - (i / E) * E;
       half[p][sync.rank * E + e2] = batch_counts[e2];
     }
-    __threadfence_system();
     __syncthreads();
     if (tid == 0) {
+      __threadfence_system();  // cumulative over the CTA's count stores (ordered by the barrier)
       const uint32_t ep = sync.state[0] + 1;
       peer_raise(sync, ep);
       sync.state[0] = ep;
