@@ -156,6 +156,28 @@ def main():
     caps = [max(len(x) for x in sets)] * (G - 1) + [0]
     run_case(shape, G, rank, sets, sets, [100 + 20 * s for s in range(G)], seed=5, caps=caps)
 
+    # case 6: randomised shapes and placements (every rank draws the same ones): replicated
+    # experts, ragged T including empty origins, migration between two random placements
+    for seed in (11, 12):
+        r = np.random.default_rng(seed * 100 + G)
+        E = int(r.choice([8, 16, 60, 64]))
+        k = int(r.integers(1, min(6, E) + 1))
+        shared_f = int(r.choice([0, 256]))
+        shape = LayerShape(f"rand{seed}", d=int(r.choice([256, 512])), f=int(r.choice([128, 256, 384])), E=E, k=k,
+                           score_mode=int(r.integers(0, 2)), shared_f=shared_f,
+                           shared_gate=int(r.integers(0, 2)) if shared_f else 0)
+
+        def random_sets():
+            held = [set() for _ in range(G)]
+            for e in range(E):
+                for g in r.choice(G, size=int(r.integers(1, min(2, G) + 1)), replace=False):
+                    held[int(g)].add(e)
+            return [sorted(h) for h in held]
+        sets, sets2 = random_sets(), random_sets()
+        T_list = [int(t) for t in r.integers(0, 300, size=G)]
+        T_list[int(r.integers(0, G))] = max(1, T_list[0])
+        run_case(shape, G, rank, sets, sets2, T_list, seed=seed)
+
     dist.barrier()
     if rank == 0:
         print(f"mgpu ok: G={G}")
