@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--cpu-tokens", type=int, default=256, help="tokens per CPU-baseline sample")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--stages", action="store_true", help="print the per-stage table on stderr")
-    ap.add_argument("--scenario", default="steady", choices=["steady", "shift"],
+    ap.add_argument("--layers", type=int, default=4, help="--scenario stack: MoE layers in the stack")
+    ap.add_argument("--scenario", default="steady", choices=["steady", "shift", "stack"],
                     help="shift: BASELINE config 5, drifting routing + expert migration vs static placement")
     return ap.parse_args()
 
@@ -722,6 +723,97 @@ def main_shift(args):
     layer.close()
 
 
+def main_stack(args):
+    """F3: an L-layer MoEStack (ModelSpec.num_layers > 1, the reference walks a request through
+    its layers in order, sim.py:500-505), each layer with its own router, expert weights and
+    placement, run eagerly and as one captured CUDA graph (device-side flag epochs and count
+    parity make the forward replayable).  Reports tokens/s through the whole stack both ways."""
+    import torch
+    import torch.distributed as dist
+    from paper_2508_12851_b200 import workload as wl
+    from paper_2508_12851_b200.layer import B200MoELayer, MoEStack
+    from paper_2508_12851_b200.shapes import get_shape
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        init_dist_quiet(dev)
+    shape = get_shape(args.config)
+    T, G, L = args.tokens, world, args.layers
+    layers = []
+    for l in range(L):
+        seed = args.seed + 101 * l
+        wg = wl.router_weights(shape.E + shape.shared_gate, shape.d, dev, seed)
+        src = (lambda s: lambda e: wl.expert_weights(e, shape.d, shape.f, dev, s, layer=l))(seed)
+        # placement of layer l: the reference solver on this layer's warm-up histogram
+        prov = [[e for e in range(shape.E) if e % G == r] for r in range(G)]
+        caps = [max(len(p) for p in prov)] * G if G > 1 else [shape.E]
+        probe = B200MoELayer(shape, rank=rank, world=world, device=local, max_tokens=T,
+                             cap_slots=max(caps[rank], max(len(p) for p in prov)))
+        probe.open_peers()
+        probe.set_router(wg[:shape.E], wl.origin_bias(rank, shape.E, seed), wg[shape.E] if shape.shared_gate else None)
+        if shape.shared_f:
+            probe.set_shared(*wl.shared_weights(shape.d, shape.shared_f, dev, seed, layer=l))
+        probe.set_placement_sets(prov, src)
+        probe.forward(wl.tokens(T, shape.d, dev, seed, rank, batch=10_000))
+        torch.cuda.synchronize()
+        counts = probe.gathered_counts()
+        probe.close()
+        sets, caps, _ = build_placement_sets(shape, G, counts, args.strategy, seed)
+        layer = B200MoELayer(shape, rank=rank, world=world, device=local, max_tokens=T, cap_slots=caps[rank])
+        layer.open_peers()
+        layer.set_router(wg[:shape.E], wl.origin_bias(rank, shape.E, seed), wg[shape.E] if shape.shared_gate else None)
+        if shape.shared_f:
+            layer.set_shared(*wl.shared_weights(shape.d, shape.shared_f, dev, seed, layer=l))
+        layer.set_placement_sets(sets, src)
+        layers.append(layer)
+    stack = MoEStack(layers)
+    x = wl.tokens(T, shape.d, dev, args.seed, rank, batch=0)
+    out = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, steps):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return ms.item()
+
+    eager_ms = timed(lambda: stack.forward(x, out), args.steps)
+    eager_out = out.clone()
+    graph = stack.capture(x, out)
+    graph_ms = timed(graph.replay, args.steps)
+    torch.cuda.synchronize()
+    for layer in layers:
+        layer.check()
+    same = bool(torch.equal(out, eager_out))
+    launches = sum(layer.last_launches() for layer in layers)
+    if rank == 0:
+        line = {"scenario": "multi-layer stack (F3)", "metric": METRIC, "unit": UNIT, "n_gpus": G,
+                "config": {"model": shape.name, "layers": L, "tokens_per_gpu": T, "steps": args.steps},
+                "eager": {"value": G * T / (eager_ms * 1e-3), "ms_per_stack_forward": eager_ms},
+                "cuda_graph": {"value": G * T / (graph_ms * 1e-3), "ms_per_stack_forward": graph_ms},
+                "graph_output_equals_eager": same, "kernel_launches_per_stack_forward": launches}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    del graph
+    for layer in layers:
+        layer.close()
+
+
 def measure_peer_copy(layer, world, rank):
     """NVLink pull bandwidth: copy one expert slot from the next GPU into a free staging slot."""
     import torch
@@ -755,6 +847,9 @@ if __name__ == "__main__":
     a = parse()
     if a.scenario == "shift" and a.impl != "reference":
         main_shift(a)
+        raise SystemExit(0)
+    if a.scenario == "stack" and a.impl != "reference":
+        main_stack(a)
         raise SystemExit(0)
     if a.impl == "reference":
         # keep the whole --steps K run within minutes: clamp the sample size for the big shapes
