@@ -95,7 +95,8 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
                   const float* __restrict__ bias, int T, int d, int E, int has_gate, int k, int score_mode,
                   int renorm, int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
                   uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
-                  uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix, const PeerSync sync) {
+                  uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix, const PeerSync sync,
+                  int stage_counts) {
   __shared__ float logits[rt::kTokens][rt::kMaxE + 9];
   __shared__ int cnt_s[rt::kMaxE];
   __shared__ uint64_t xbar;
@@ -279,8 +280,8 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
   __threadfence();
   const int nb = gridDim.x;
   // stage the [nb][E] block-count matrix in shared memory with coalesced loads
-  // (when it fits), then per-expert scans run from there
-  const bool staged = true;
+  // (when it fits: up to 200 KB), then per-expert scans run from there
+  const bool staged = stage_counts != 0;
   if (staged)
     for (int i = tid; i < nb * E; i += blockDim.x) bc[i] = __ldcg(&blk_counts[i]);
   __syncthreads();
@@ -349,8 +350,9 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
     return set_error(MP_E_ARG, "router: the count exchange needs the batch counts");
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return set_error(MP_E_ARG, "router: x not 16-byte aligned");
   const int grid = (T + rt::kTokens - 1) / rt::kTokens;
-  const size_t bc_bytes = blk_counts && batch_counts ? size_t(grid) * E * 4 : 0;
-  if (bc_bytes > 200 * 1024) return set_error(MP_E_SHAPE, "router: %d blocks x %d experts too large", grid, E);
+  size_t bc_bytes = blk_counts && batch_counts ? size_t(grid) * E * 4 : 0;
+  const bool stage_counts = bc_bytes <= 200 * 1024;  // larger T: the last CTA scans from global memory
+  if (!stage_counts) bc_bytes = 0;
   // variant: 0 = 8 warps, x from HBM (one expert pass); 1 = 16 warps, x from HBM;
   // 2 = 16 warps, x rows in smem; 3 = 8 warps, x rows in smem (MP_ROUTER_VARIANT overrides)
   const char* venv = getenv("MP_ROUTER_VARIANT");
@@ -375,7 +377,8 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   }
   cudaError_t e = launch_pdl(kern, dim3(grid), dim3(warps * 32), smem, stream, x, wg_packed,
                              bias, T, d, E, has_gate ? 1 : 0, k, score_mode, renorm, idx, w, shared_gate, hist,
-                             blk_counts, batch_counts, ticket, blk_prefix, sync ? *sync : PeerSync());
+                             blk_counts, batch_counts, ticket, blk_prefix, sync ? *sync : PeerSync(),
+                             stage_counts ? 1 : 0);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_kernel launch");
 }

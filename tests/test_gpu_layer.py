@@ -153,3 +153,26 @@ def test_host_pipeline_matches_device_forward(depth):
     for i in range(len(xs)):
         assert torch.equal(oh[i], ref[i]), i
     layer.close()
+
+
+def test_large_batch_block_scan_from_global():
+    """T large enough that the router's [blocks][E] count matrix (1250 x 64 ints) no longer
+    fits the last CTA's shared memory: the block scan reads it from global memory instead.
+    Routing, counts and receive positions stay bit-exact."""
+    from paper_2508_12851_b200.shapes import LayerShape
+    shape = LayerShape("wide_batch", d=256, f=128, E=64, k=6, score_mode=1)
+    T = 40_000
+    experts, shared, wg = _weights(shape)
+    x = orc.synthetic_tokens(0, T, shape.d, seed=8)
+    bias = orc.origin_bias(0, shape.E, seed=8)
+    layer = _build_layer(shape, T, experts, shared, wg, bias)
+    out = layer.forward(torch.from_numpy(x).cuda().bfloat16())
+    torch.cuda.synchronize()
+    layer.check()
+    route = np.zeros((1, shape.E), dtype=np.int32)
+    ref = orc.moe_layer_forward(shape, [x], wg[:shape.E], [bias], route, experts, shared, None)
+    assert np.array_equal(layer.idx[:T].cpu().numpy(), ref.idx[0])
+    assert np.array_equal(layer.read_counts(), ref.counts)
+    assert np.array_equal(layer.pos_row[:T].cpu().numpy(), ref.pos_row[0])
+    _check_close(out.float().cpu().numpy(), ref.out[0])
+    layer.close()
