@@ -377,6 +377,9 @@ def main_b200(args):
     acc_ours = layer.dispatch_accounting()
     counts_last = layer.read_counts()
     recv_rows = int(np.sum([counts_last[s, e] for s in range(G) for e in range(shape.E) if layer.route[s, e] == rank]))
+    # expert slots this GPU streamed per step (groups with rows) -- the weight bytes of K3
+    active_local = int(sum(1 for e in range(shape.E)
+                           if sum(counts_last[s, e] for s in range(G) if layer.route[s, e] == rank) > 0))
 
     # ---- e2e: the same forward through the public API with HOST buffers: every step copies its
     # x from pinned host memory and its output back (HostPipeline overlaps the copies of
@@ -412,14 +415,16 @@ def main_b200(args):
     stage_mean = stage_ms.mean(axis=0)
     stage_t = torch.tensor(stage_mean, dtype=torch.float64, device=dev)
     gemm_local = float(gemm1_ms.mean() + gemm2_ms.mean())
-    rank_t = torch.tensor([recv_rows, gemm_local], dtype=torch.float64, device=dev)
+    rank_t = torch.tensor([recv_rows, gemm_local, active_local], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(stage_t, op=dist.ReduceOp.MAX)
         parts = [torch.zeros_like(rank_t) for _ in range(world)]
         dist.all_gather(parts, rank_t)
         per_rank = [(int(p[0].item()), float(p[1].item())) for p in parts]
+        active_list = [int(p[2].item()) for p in parts]
     else:
         per_rank = [(recv_rows, gemm_local)]
+        active_list = [active_local]
     rows_list = [r for r, _ in per_rank]
 
     # naive placement accounting on the same counts (counts do not depend on placement)
@@ -439,6 +444,14 @@ def main_b200(args):
     flops = 2.0 * rows_list[hot] * 3 * shape.d * shape.f + shared_flops
     achieved_tflops = per_rank_tf[hot]
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    # the same launches seen from HBM: every active expert slot's weights are streamed once
+    # (+ the shared expert's when fused); small batches are bound by this, not by the tensor pipe
+    w_bytes = active_list[hot] * shape.expert_bytes + (3 * shape.d * shape.shared_f * 2 if exec_plan["fuse_shared"]
+                                                        else 0)
+    w_gbs = w_bytes / (per_rank[hot][1] * 1e-3) / 1e9 if per_rank[hot][1] > 0 else None
+    hbm_peak = float(peaks.get("hbm_gbs", 6546.6))
+    ridge = peak * 1e12 / (hbm_peak * 1e9)  # flop/B where the two roofs meet
+    bound = "tensor" if flops / max(w_bytes, 1) >= ridge else "hbm"
     traffic = None
     tf = REPO / "profiles" / "traffic.json"
     if tf.exists():
@@ -501,7 +514,7 @@ def main_b200(args):
         "stages_note": "side_chain_ms = [span of the small-group chain on the side stream, GEMM start -> its end]; "
                        "per-stage means from a diagnostic pass with events at every boundary (max over ranks); "
                        "the timed region records only the K3 boundaries",
-        "roofline": {"bound": "tensor",
+        "roofline": {"bound": bound,
                      "kernel": ("grouped_gemm_2sm_kernel" if exec_plan["pair_routed"] else "grouped_gemm_kernel")
                                + f" (GEMM1+SwiGLU, GEMM2), rank {hot} (most routed rows)"
                                + ("; small groups on grouped_gemm_kernel over a side stream"
@@ -509,10 +522,20 @@ def main_b200(args):
                                                   + ("; shared expert fused into the same launches"
                                                      if exec_plan["fuse_shared"] else ""),
                      "achieved_per_rank": per_rank_tf,
-                     "achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved_tflops / peak if peak else None, "traffic": traffic,
+                     **({"achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved_tflops / peak if peak else None}
+                        if bound == "tensor" else
+                        {"achieved": w_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": w_gbs / hbm_peak if w_gbs else None,
+                         "tensor_view": {"achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s"}}),
+                     "traffic": traffic,
                      "peak_source": f"{peaks_src} bf16 sustained (kernel timed inside the step)",
-                     "flops_per_step": flops},
+                     "flops_per_step": flops,
+                     "weights": {"bytes_per_step": w_bytes, "GB/s": w_gbs, "peak_GB/s": hbm_peak,
+                                 "frac": w_gbs / hbm_peak if w_gbs else None,
+                                 "note": "active expert slots' weights streamed by the same K3 launches; "
+                                         "'bound' is hbm when flops/weight-bytes is below the ridge "
+                                         f"({ridge:.0f} flop/B)"}},
         "cpu_baseline": cpu,
         "e2e": {"value": tokens_total / (e2e_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": T * shape.d * 2, "d2h_bytes_per_step": T * shape.d * 2,

@@ -100,6 +100,10 @@ struct mp_layer {
   // shared expert fused into the routed CTA-pair launches (one GEMM1 and one GEMM2
   // launch cover both problems; no per-launch tails / wave quantisation of its own)
   int fuse_shared = 0;
+  // below this many rows per expert on average (G*T*k/E) a forward streams every group
+  // over all SMs on the 1-CTA kernel (no side chain, shared expert in its own launches)
+  int stream_rows = 256;
+  int last_pair = -1, last_split = -1, last_fused = -1;  // plan of the last forward (-1: none yet)
   // small-group split: groups below split_m rows run on a side stream over small_grid SMs
   int split_m = 0, small_grid = 20;
   cudaStream_t side = nullptr;
@@ -342,6 +346,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       return fail(set_cuda_error(e, "cudaEventCreate(split)"));
   }
   L->fuse_shared = (D.shared_f > 0 && D.n_slots > 0 && L->pair_routed && L->pair_shared) ? 1 : 0;
+  if (const char* env = getenv("MP_STREAM_ROWS")) L->stream_rows = atoi(env);
   if (const char* env = getenv("MP_FUSE_SHARED")) L->fuse_shared = L->fuse_shared && atoi(env) != 0;
   if (D.shared_f > 0) {
     if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
@@ -561,7 +566,17 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     ++launches;
   }
   MP_TRY(mark());  // 4 permute + dispatch
-  const bool fused = L->fuse_shared && D.shared_f > 0 && T > 0;
+  // Per-forward K3 plan.  With few rows per expert (small batches) every group is
+  // weight-bound: stream all of them over every SM on the 1-CTA kernel instead of
+  // confining them to the small-group side chain (the shared expert then runs in
+  // its own launches).
+  const int64_t avg_rows = int64_t(G) * T * k / std::max(1, E);
+  const bool stream_plan = L->split_m > 0 && avg_rows < L->stream_rows;
+  const bool split = L->split_m > 0 && !stream_plan;
+  const bool fused = L->fuse_shared && D.shared_f > 0 && T > 0 && !stream_plan;
+  L->last_split = split ? L->split_m : 0;
+  L->last_fused = fused ? 1 : 0;
+  L->last_pair = stream_plan ? 0 : L->pair_routed;
   if (D.shared_f > 0 && T > 0 && !fused) {
     GroupSpec gsh;
     gsh.mode = 2;
@@ -585,13 +600,13 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     gs.G = G;
     gs.E = E;
     gs.rank = rank;
-    const int pr = L->pair_routed;
-    const int big_grid = L->split_m > 0 ? kNumSMs - L->small_grid : 0;
+    const int pr = stream_plan ? 0 : L->pair_routed;
+    const int big_grid = split ? kNumSMs - L->small_grid : 0;
     // C is raised by the last GEMM2 CTA of both chains
-    ps_ret.total = grouped_gemm_ctas(big_grid, pr) + (L->split_m > 0 ? grouped_gemm_ctas(L->small_grid, 0) : 0);
+    ps_ret.total = grouped_gemm_ctas(big_grid, pr) + (split ? grouped_gemm_ctas(L->small_grid, 0) : 0);
     const PeerSync* sw = G > 1 ? &ps_wait : nullptr;
     const PeerSync* sr = G > 1 ? &ps_ret : nullptr;
-    if (L->split_m > 0) {
+    if (split) {
       // fork: small groups (weight-bound) on the side stream over small_grid SMs, large
       // groups (compute-bound) on the main stream over the rest, then join
       GroupSpec gsmall = gs;
@@ -609,7 +624,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       MP_CUDA(cudaEventRecord(L->ev_join, L->side));
       launches += 2;
     }
-    const bool pdl = L->split_m == 0;
+    const bool pdl = !split;
     // fused shared expert: its GEMM1 / GEMM2 tiles ride in the routed launches
     AuxProblem aux1, aux2;
     if (fused) {
@@ -634,7 +649,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     // GEMM2 epilogue returns every output row to its origin GPU (NVLink stores)
     MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
                                big_grid, st, pr, L->recv_src, ret_ptrs, pdl, fused ? &aux2 : nullptr, sr));
-    if (L->split_m > 0) MP_CUDA(cudaStreamWaitEvent(st, L->ev_join, 0));
+    if (split) MP_CUDA(cudaStreamWaitEvent(st, L->ev_join, 0));
     launches += 2;
   } else {
     MP_TRY(mark());
@@ -670,10 +685,10 @@ int mp_layer_last_launches(mp_layer* L) { return L ? L->last_launches : 0; }
 int mp_layer_config(mp_layer* L, int key) {
   if (!L) return set_error(MP_E_ARG, "mp_layer_config: null layer");
   switch (key) {
-    case MP_CFG_PAIR_ROUTED: return L->pair_routed;
-    case MP_CFG_SPLIT_M: return L->split_m;
-    case MP_CFG_SMALL_GRID: return L->split_m > 0 ? L->small_grid : 0;
-    case MP_CFG_FUSE_SHARED: return L->fuse_shared;
+    case MP_CFG_PAIR_ROUTED: return L->last_pair >= 0 ? L->last_pair : L->pair_routed;
+    case MP_CFG_SPLIT_M: return L->last_split >= 0 ? L->last_split : L->split_m;
+    case MP_CFG_SMALL_GRID: return (L->last_split >= 0 ? L->last_split : L->split_m) > 0 ? L->small_grid : 0;
+    case MP_CFG_FUSE_SHARED: return L->last_fused >= 0 ? L->last_fused : L->fuse_shared;
     default: return set_error(MP_E_ARG, "mp_layer_config: key %d", key);
   }
 }
