@@ -73,6 +73,15 @@ MP_DEV uint32_t cluster_ctarank() {
 MP_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Store a float at the same smem offset in CTA `cta` of the cluster (DSMEM).
+MP_DEV void st_cluster_f32(const void* local_equiv, uint32_t cta, float v) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "st.shared::cluster.f32 [ra], %2;\n\t}" ::"r"(smem_u32(local_equiv)),
+      "r"(cta), "f"(v)
+      : "memory");
+}
 // Arrive on the mbarrier at the same smem offset in CTA `cta` of the cluster.
 MP_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
   asm volatile(

@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
                   int renorm, int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
                   uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
                   uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix, const PeerSync sync,
-                  int stage_counts) {
+                  int stage_counts, int csplit) {
   __shared__ float logits[rt::kTokens][rt::kMaxE + 9];
   __shared__ int cnt_s[rt::kMaxE];
   __shared__ uint64_t xbar;
@@ -106,7 +106,12 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
 
   const int E_tot = E + has_gate;
   const int E_pad = router_e_pad(E_tot);
-  const int t0 = blockIdx.x * rt::kTokens;
+  // csplit > 1: a cluster of csplit CTAs shares one 32-token block, CTA r computing the
+  // expert passes r, r + csplit, ... and storing its logits into the leader's smem (DSMEM);
+  // the leader does the rest.  Small batches get csplit x the CTAs on the chains.
+  const int blk = blockIdx.x / csplit, crank = blockIdx.x - blk * csplit;
+  const int n_blk = gridDim.x / csplit;
+  const int t0 = blk * rt::kTokens;
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   const int n_tok = min(rt::kTokens, T - t0);
   for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
   if (kXSmem) mbar_wait(&xbar, 0);
   const int S = d / 256;
 
-  for (int e0 = kExpPerPass * (warp / kQuads); e0 < E_pad; e0 += kExpPerPass * n_pg) {
+  for (int e0 = kExpPerPass * (crank * n_pg + warp / kQuads); e0 < E_pad; e0 += kExpPerPass * n_pg * csplit) {
     unsigned long long acc[kTokPerWarp][kExpPerPass / 2];
 #pragma unroll
     for (int i = 0; i < kTokPerWarp; ++i)
@@ -201,8 +206,15 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
     if (e < E_tot) {
       float val = v[0];
       if (bias != nullptr && e < E) val = __fadd_rn(val, bias[e]);
-      logits[tt][e] = val;
+      if (csplit > 1)
+        st_cluster_f32(&logits[tt][e], 0, val);
+      else
+        logits[tt][e] = val;
     }
+  }
+  if (csplit > 1) {
+    cluster_sync();  // every CTA's logits are in the leader's smem
+    if (crank != 0) return;
   }
   __syncthreads();
 
@@ -264,7 +276,7 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) {
     const int c = cnt_s[e];
-    if (blk_counts) blk_counts[size_t(blockIdx.x) * E + e] = c;
+    if (blk_counts) blk_counts[size_t(blk) * E + e] = c;
     if (c && hist) atomicAdd(&hist[e], uint32_t(c));
   }
   if (batch_counts == nullptr || blk_counts == nullptr) return;
@@ -274,11 +286,11 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
   __shared__ int is_last;
   __threadfence();
   __syncthreads();
-  if (tid == 0) is_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  if (tid == 0) is_last = atomicAdd(ticket, 1u) == uint32_t(n_blk - 1);
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  const int nb = gridDim.x;
+  const int nb = n_blk;
   // stage the [nb][E] block-count matrix in shared memory with coalesced loads
   // (when it fits: up to 200 KB), then per-expert scans run from there
   const bool staged = stage_counts != 0;
@@ -375,10 +387,37 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
     if (ea != cudaSuccess) return set_cuda_error(ea, "cudaFuncSetAttribute(router)");
     smem_set[variant] = smem;
   }
-  cudaError_t e = launch_pdl(kern, dim3(grid), dim3(warps * 32), smem, stream, x, wg_packed,
-                             bias, T, d, E, has_gate ? 1 : 0, k, score_mode, renorm, idx, w, shared_gate, hist,
-                             blk_counts, batch_counts, ticket, blk_prefix, sync ? *sync : PeerSync(),
-                             stage_counts ? 1 : 0);
+  // small batches: split each block's expert passes over a cluster of up to 8 CTAs so the
+  // grid covers the SMs (one CTA per SM for the register-heavy variants)
+  const int n_pass = router_e_pad(E + (has_gate ? 1 : 0)) / kExpPerPass;
+  const int n_pg = warps / kQuads;
+  int csplit = 1;
+  while (csplit * 2 <= 8 && csplit * 2 * n_pg <= n_pass && grid * csplit * 2 <= kNumSMs) csplit *= 2;
+  if (const char* cs = getenv("MP_ROUTER_SPLIT")) csplit = std::max(1, std::min(8, atoi(cs)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid * csplit);
+  cfg.blockDim = dim3(warps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (csplit > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = csplit;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, x, wg_packed, bias, T, d, E, has_gate ? 1 : 0, k, score_mode,
+                                     renorm, idx, w, shared_gate, hist, blk_counts, batch_counts, ticket, blk_prefix,
+                                     sync ? *sync : PeerSync(), stage_counts ? 1 : 0, csplit);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_kernel launch");
 }

@@ -126,14 +126,17 @@ def _run_router(x, wg, bias, E, k, mode, gate):
     return idx.cpu().numpy(), w.cpu().numpy(), hist.cpu().numpy()
 
 
+@pytest.mark.parametrize("split", ["", "1", "2", "4", "8"])
 @pytest.mark.parametrize("variant", ["", "0", "1", "2", "3"])
 @pytest.mark.parametrize("E,k,mode,d", [(8, 2, 0, 512), (64, 6, 1, 256), (16, 4, 0, 4096)])
-def test_router_ties_go_to_the_lower_expert(E, k, mode, d, variant, monkeypatch):
+def test_router_ties_go_to_the_lower_expert(E, k, mode, d, variant, split, monkeypatch):
     """Exact logit ties (duplicated router rows + biases, all-zero tokens whose logits are the
     biases alone) resolve to the lower expert id, bit-exact with the oracle -- in every router
     variant (8 or 16 warps, x from HBM or staged in smem; "" = the shape's default)."""
     if variant:
         monkeypatch.setenv("MP_ROUTER_VARIANT", variant)
+    if split:  # passes split over a cluster of CTAs, logits gathered in the leader's smem
+        monkeypatch.setenv("MP_ROUTER_SPLIT", split)
     T = 96
     x = orc.synthetic_tokens(0, T, d, seed=7)
     x[::3] = 0.0                       # every third token: logits == bias
