@@ -176,7 +176,8 @@ int mp_layer_last_launches(mp_layer* layer);
 /* K3 execution plan of the last forward (before any forward: the plan chosen at
  * creation from the shape; MP_* environment knobs override), for reporting.
  * Small batches (G*T*k/E below MP_STREAM_ROWS, default 256) stream every
- * expert group over all SMs instead of splitting off a side chain. */
+ * expert group over all SMs on the 1-CTA kernel instead of splitting off a
+ * side chain; the shared expert rides in the routed launches either way. */
 #define MP_CFG_PAIR_ROUTED 0   /* routed experts on CTA-pair (256-row) tiles   */
 #define MP_CFG_SPLIT_M 1       /* groups below this many rows: side-stream chain */
 #define MP_CFG_SMALL_GRID 2    /* SMs given to that side chain                   */

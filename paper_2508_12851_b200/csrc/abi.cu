@@ -345,7 +345,8 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
         (e = cudaEventCreateWithFlags(&L->ev_join, cudaEventDisableTiming)) != cudaSuccess)
       return fail(set_cuda_error(e, "cudaEventCreate(split)"));
   }
-  L->fuse_shared = (D.shared_f > 0 && D.n_slots > 0 && L->pair_routed && L->pair_shared) ? 1 : 0;
+  // the shared expert rides in the routed launches (either kernel) as the aux problem
+  L->fuse_shared = (D.shared_f > 0 && D.n_slots > 0) ? 1 : 0;
   if (const char* env = getenv("MP_STREAM_ROWS")) L->stream_rows = atoi(env);
   if (const char* env = getenv("MP_FUSE_SHARED")) L->fuse_shared = L->fuse_shared && atoi(env) != 0;
   if (D.shared_f > 0) {
@@ -568,12 +569,12 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   MP_TRY(mark());  // 4 permute + dispatch
   // Per-forward K3 plan.  With few rows per expert (small batches) every group is
   // weight-bound: stream all of them over every SM on the 1-CTA kernel instead of
-  // confining them to the small-group side chain (the shared expert then runs in
-  // its own launches).
+  // confining them to the small-group side chain (the shared expert rides along as
+  // the aux problem of those launches).
   const int64_t avg_rows = int64_t(G) * T * k / std::max(1, E);
   const bool stream_plan = L->split_m > 0 && avg_rows < L->stream_rows;
   const bool split = L->split_m > 0 && !stream_plan;
-  const bool fused = L->fuse_shared && D.shared_f > 0 && T > 0 && !stream_plan;
+  const bool fused = L->fuse_shared && D.shared_f > 0 && T > 0;
   L->last_split = split ? L->split_m : 0;
   L->last_fused = fused ? 1 : 0;
   L->last_pair = stream_plan ? 0 : L->pair_routed;
@@ -629,14 +630,14 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     AuxProblem aux1, aux2;
     if (fused) {
       aux1.tmA = L->tm_x;
-      aux1.tmB = L->tm_w13s_p;
+      aux1.tmB = pr ? L->tm_w13s_p : L->tm_w13s;
       aux1.out = L->hs;
       aux1.out_ld = D.shared_f;
       aux1.m = T;
       aux1.N = 2 * D.shared_f;
       aux1.K = D.d;
       aux2.tmA = L->tm_hs;
-      aux2.tmB = L->tm_w2s_p;
+      aux2.tmB = pr ? L->tm_w2s_p : L->tm_w2s;
       aux2.out = L->ys;
       aux2.out_ld = D.d;
       aux2.m = T;

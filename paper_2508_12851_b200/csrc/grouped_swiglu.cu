@@ -200,11 +200,108 @@ MP_DEV void epilogue_store(uint32_t taddr, bool valid, __nv_bfloat16* __restrict
   }
 }
 
+// One tile of work (a CTA pair's 256-row tile, or a CTA's 128-row tile): where its
+// A / B rows come from, how many k-blocks it runs and where its output goes.
+struct TileJob {
+  const CUtensorMap* ma;
+  const CUtensorMap* mb;
+  int a_row, b_row;   // first row of the tile (A) and of its 256 N rows (B)
+  int k_blocks;
+  int n_blk;
+  int m_row0, m_rows;  // tile's first row inside its group, and the group's row count
+  bool aux;
+  int g;               // routed group (aux: -1)
+};
+
+// Static schedule of one cluster.  Without an aux problem: routed tiles
+// round-robin.  With one: aux tiles round-robin (tile t -> cluster t mod C),
+// then the routed tiles round-robin in reversed cluster order, except the last
+// few, which go only to the clusters that drew one aux tile fewer (about
+// aux K / routed K tiles each) -- so every cluster ends with about the same
+// number of k-blocks while concurrently running clusters still share weight
+// tiles in L2.  (Contiguous k-balanced ranges per cluster lose that sharing:
+// measured 30% slower.)
+struct TileSched {
+  int A, aux_mb, aux_kb;
+  int s1_begin, s1_end, s1_step;
+  int s2_begin, s2_end, s2_step;
+};
+
+template <int BM_>
+MP_DEV TileSched make_sched(const AuxProblem& aux, int R, int k_blocks, int cluster_id, int C) {
+  TileSched ps;
+  ps.aux_mb = aux.m > 0 ? (aux.m + BM_ - 1) / BM_ : 0;
+  ps.A = ps.aux_mb * (aux.N / gg::BN);
+  ps.aux_kb = aux.K / gg::BK;
+  ps.s2_begin = ps.s2_end = 0;
+  ps.s2_step = 1;
+  if (ps.A == 0) {
+    ps.s1_begin = cluster_id;
+    ps.s1_end = R;
+    ps.s1_step = C;
+    return ps;
+  }
+  const int rem = ps.A % C;
+  const int extra = rem > 0 ? (ps.aux_kb + k_blocks / 2) / k_blocks : 0;
+  const int X = min(R, (C - rem) * extra);
+  const int R1 = R - X;
+  ps.s1_begin = C - 1 - cluster_id;
+  ps.s1_end = R1;
+  ps.s1_step = C;
+  if (cluster_id >= rem && X > 0) {
+    ps.s2_begin = R1 + (cluster_id - rem);
+    ps.s2_end = R;
+    ps.s2_step = C - rem;
+  }
+  return ps;
+}
+
+template <int BM_, class Tail, class Fn>
+MP_DEV void for_each_job(const TileSched& ps, const Tail& st, const AuxProblem& aux,
+                              const CUtensorMap* tmA, const CUtensorMap* tmB, int n_blocks, int k_blocks,
+                              int b_slot_stride, int b_offset, int cluster_id, int C, Fn&& fn) {
+  for (int t = cluster_id; t < ps.A; t += C) {
+    TileJob j;
+    j.aux = true;
+    j.g = -1;
+    j.n_blk = t / ps.aux_mb;
+    const int m_blk = t - j.n_blk * ps.aux_mb;
+    j.ma = &aux.tmA;
+    j.mb = &aux.tmB;
+    j.m_row0 = m_blk * BM_;
+    j.m_rows = aux.m;
+    j.a_row = j.m_row0;
+    j.b_row = j.n_blk * gg::BN;
+    j.k_blocks = ps.aux_kb;
+    fn(j);
+  }
+  for (int seg = 0; seg < 2; ++seg) {
+    const int t0 = seg ? ps.s2_begin : ps.s1_begin, t1 = seg ? ps.s2_end : ps.s1_end;
+    const int dt = seg ? ps.s2_step : ps.s1_step;
+    for (int t = t0; t < t1; t += dt) {
+    const TileCoord c = decode_any(st, t, n_blocks, BM_);
+    TileJob j;
+    j.aux = false;
+    j.g = c.g;
+    j.n_blk = c.n_blk;
+    j.ma = tmA;
+    j.mb = tmB;
+    j.m_row0 = c.m_blk * BM_;
+    j.m_rows = st.g_m[c.g];
+    j.a_row = st.g_arow[c.g] + j.m_row0;
+    j.b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * gg::BN;
+    j.k_blocks = k_blocks;
+    fn(j);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset, __nv_bfloat16* __restrict__ out,
                         int out_ld, int swiglu, const int32_t* __restrict__ scatter_src,
-                        __nv_bfloat16* const* __restrict__ scatter_ptrs, const PeerSync sync) {
+                        __nv_bfloat16* const* __restrict__ scatter_ptrs, const PeerSync sync,
+                        const __grid_constant__ AuxProblem aux) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
@@ -233,6 +330,10 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if (aux.m > 0) {
+      tma_prefetch_desc(&aux.tmA);
+      tma_prefetch_desc(&aux.tmB);
+    }
   }
   if (warp == 2) tmem_alloc<gg::kTmemCols>(&st.tmem_base);
   griddep_wait();
@@ -241,33 +342,36 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = st.tmem_base;
-  const int total = st.total_tiles;
+  const TileSched ts = make_sched<gg::BM>(aux, st.total_tiles, k_blocks, blockIdx.x, gridDim.x);
+  auto each_job = [&](auto&& fn) {
+    for_each_job<gg::BM>(ts, st, aux, &tmA, &tmB, n_blocks, k_blocks, b_slot_stride, b_offset, blockIdx.x,
+                         gridDim.x, fn);
+  };
 
   if (warp == 0) {
     if (lane == 0) {
       // ================= TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      // rows from peers: wait for every rank's dispatch (epoch B) before the first A load
-      if (peer_on(sync) && sync.wait && blockIdx.x < total) {
-        peer_wait(sync, sync.state[0]);
-        fence_proxy_async_global();
-      }
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const TileCoord c = decode_any(st, tile, n_blocks, gg::BM);
-        const int a_row = st.g_arow[c.g] + c.m_blk * gg::BM;
-        const int b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * gg::BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+      bool waited = !(peer_on(sync) && sync.wait);
+      each_job([&](const TileJob& j) {
+        if (!waited && !j.aux) {
+          // rows from peers: every rank's dispatch (epoch B) before the first routed A load
+          peer_wait(sync, sync.state[0]);
+          fence_proxy_async_global();
+          waited = true;
+        }
+        for (int kb = 0; kb < j.k_blocks; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&st.full[stage], gg::kStageBytes);
-          tma_load_2d(smA + stage * gg::kABytes, &tmA, &st.full[stage], kb * gg::BK, a_row);
-          tma_load_2d(smB + stage * gg::kBBytes, &tmB, &st.full[stage], kb * gg::BK, b_row);
+          tma_load_2d(smA + stage * gg::kABytes, j.ma, &st.full[stage], kb * gg::BK, j.a_row);
+          tma_load_2d(smB + stage * gg::kBBytes, j.mb, &st.full[stage], kb * gg::BK, j.b_row);
           if (++stage == gg::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-      }
+      });
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -277,11 +381,11 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      each_job([&](const TileJob& j) {
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * gg::BN);
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        for (int kb = 0; kb < j.k_blocks; ++kb) {
           mbar_wait(&st.full[stage], phase);
           tc_fence_after();
           const uint64_t adesc = make_sdesc_sw128(smem_u32(smA + stage * gg::kABytes));
@@ -301,29 +405,29 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
         umma_commit(&st.tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
-      }
+      });
     }
   } else if (warp >= 4) {
     // ================= epilogue (warp w owns TMEM lanes 32*(w%4) .. +31)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const TileCoord c = decode_any(st, tile, n_blocks, gg::BM);
-      const int row = c.m_blk * gg::BM + q * 32 + lane;
-      const bool valid = row < st.g_m[c.g];
-      const size_t orow = size_t(st.g_orow[c.g] + row);
+    each_job([&](const TileJob& j) {
+      const int row = j.m_row0 + q * 32 + lane;
+      const bool valid = row < j.m_rows;
+      __nv_bfloat16* rowp =
+          j.aux ? aux.out + size_t(row) * aux.out_ld
+                : out_row_ptr(out, size_t(st.g_orow[j.g] + row), out_ld, scatter_src, scatter_ptrs, valid);
       mbar_wait(&st.tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * gg::BN);
-      epilogue_store(taddr, valid, out_row_ptr(out, orow, out_ld, scatter_src, scatter_ptrs, valid), c.n_blk,
-                     swiglu);
+      epilogue_store(taddr, valid, rowp, j.n_blk, swiglu);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&st.tempty[acc]);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
-    }
+    });
   }
 
   tc_fence_before();
@@ -374,101 +478,6 @@ struct Gemm2SmemTail {
 };
 
 
-// One unit of pair work: where its A / B rows come from, how many k-blocks it
-// runs and where its 128 x 256 half-tile of output goes.
-struct PairJob {
-  const CUtensorMap* ma;
-  const CUtensorMap* mb;
-  int a_row, b_row;   // first row of the 256-row tile (A) and of its 256 N rows (B)
-  int k_blocks;
-  int n_blk;
-  int m_row0, m_rows;  // tile's first row inside its group, and the group's row count
-  bool aux;
-  int g;               // routed group (aux: -1)
-};
-
-// Static schedule of one cluster.  Without an aux problem: routed tiles
-// round-robin.  With one: aux tiles round-robin (tile t -> cluster t mod C),
-// then the routed tiles round-robin in reversed cluster order, except the last
-// few, which go only to the clusters that drew one aux tile fewer (about
-// aux K / routed K tiles each) -- so every cluster ends with about the same
-// number of k-blocks while concurrently running clusters still share weight
-// tiles in L2.  (Contiguous k-balanced ranges per cluster lose that sharing:
-// measured 30% slower.)
-struct PairSched {
-  int A, aux_mb, aux_kb;
-  int s1_begin, s1_end, s1_step;
-  int s2_begin, s2_end, s2_step;
-};
-
-MP_DEV PairSched make_sched(const AuxProblem& aux, int R, int k_blocks, int cluster_id, int C) {
-  PairSched ps;
-  ps.aux_mb = aux.m > 0 ? (aux.m + g2::BM - 1) / g2::BM : 0;
-  ps.A = ps.aux_mb * (aux.N / g2::BN);
-  ps.aux_kb = aux.K / g2::BK;
-  ps.s2_begin = ps.s2_end = 0;
-  ps.s2_step = 1;
-  if (ps.A == 0) {
-    ps.s1_begin = cluster_id;
-    ps.s1_end = R;
-    ps.s1_step = C;
-    return ps;
-  }
-  const int rem = ps.A % C;
-  const int extra = rem > 0 ? (ps.aux_kb + k_blocks / 2) / k_blocks : 0;
-  const int X = min(R, (C - rem) * extra);
-  const int R1 = R - X;
-  ps.s1_begin = C - 1 - cluster_id;
-  ps.s1_end = R1;
-  ps.s1_step = C;
-  if (cluster_id >= rem && X > 0) {
-    ps.s2_begin = R1 + (cluster_id - rem);
-    ps.s2_end = R;
-    ps.s2_step = C - rem;
-  }
-  return ps;
-}
-
-template <class Fn>
-MP_DEV void for_each_pair_job(const PairSched& ps, const Gemm2SmemTail& st, const AuxProblem& aux,
-                              const CUtensorMap* tmA, const CUtensorMap* tmB, int n_blocks, int k_blocks,
-                              int b_slot_stride, int b_offset, int cluster_id, int C, Fn&& fn) {
-  for (int t = cluster_id; t < ps.A; t += C) {
-    PairJob j;
-    j.aux = true;
-    j.g = -1;
-    j.n_blk = t / ps.aux_mb;
-    const int m_blk = t - j.n_blk * ps.aux_mb;
-    j.ma = &aux.tmA;
-    j.mb = &aux.tmB;
-    j.m_row0 = m_blk * g2::BM;
-    j.m_rows = aux.m;
-    j.a_row = j.m_row0;
-    j.b_row = j.n_blk * g2::BN;
-    j.k_blocks = ps.aux_kb;
-    fn(j);
-  }
-  for (int seg = 0; seg < 2; ++seg) {
-    const int t0 = seg ? ps.s2_begin : ps.s1_begin, t1 = seg ? ps.s2_end : ps.s1_end;
-    const int dt = seg ? ps.s2_step : ps.s1_step;
-    for (int t = t0; t < t1; t += dt) {
-    const TileCoord c = decode_any(st, t, n_blocks, g2::BM);
-    PairJob j;
-    j.aux = false;
-    j.g = c.g;
-    j.n_blk = c.n_blk;
-    j.ma = tmA;
-    j.mb = tmB;
-    j.m_row0 = c.m_blk * g2::BM;
-    j.m_rows = st.g_m[c.g];
-    j.a_row = st.g_arow[c.g] + j.m_row0;
-    j.b_row = st.g_slot[c.g] * b_slot_stride + b_offset + c.n_blk * g2::BN;
-    j.k_blocks = k_blocks;
-    fn(j);
-    }
-  }
-}
-
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
     grouped_gemm_2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                             const __grid_constant__ GroupSpec gs, int N, int K, int b_slot_stride, int b_offset,
@@ -518,10 +527,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
   cluster_sync();  // the peer's barriers are initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = st.tmem_base;
-  const PairSched ps = make_sched(aux, st.total_tiles, k_blocks, cluster_id, n_clusters);
+  const TileSched ps = make_sched<g2::BM>(aux, st.total_tiles, k_blocks, cluster_id, n_clusters);
   auto each_job = [&](auto&& fn) {
-    for_each_pair_job(ps, st, aux, &tmA, &tmB, n_blocks, k_blocks, b_slot_stride, b_offset, cluster_id, n_clusters,
-                      fn);
+    for_each_job<g2::BM>(ps, st, aux, &tmA, &tmB, n_blocks, k_blocks, b_slot_stride, b_offset, cluster_id,
+                         n_clusters, fn);
   };
 
   if (warp == 0) {
@@ -530,7 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       bool waited = !(peer_on(sync) && sync.wait);
-      each_job([&](const PairJob& j) {
+      each_job([&](const TileJob& j) {
         if (!waited && !j.aux) {
           // first routed tile: rows from peers need every rank's dispatch (epoch B);
           // the shared-expert tiles before it overlap the wait
@@ -560,7 +569,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      each_job([&](const PairJob& j) {
+      each_job([&](const TileJob& j) {
         mbar_wait(&st.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * g2::BN);
@@ -588,7 +597,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
     const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
-    each_job([&](const PairJob& j) {
+    each_job([&](const TileJob& j) {
       const int row = j.m_row0 + int(rank) * 128 + q * 32 + lane;
       const bool valid = row < j.m_rows;
       __nv_bfloat16* rowp =
@@ -653,7 +662,6 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
   if (K % gg::BK != 0) return set_error(MP_E_SHAPE, "grouped GEMM K=%d not a multiple of %d", K, gg::BK);
   AuxProblem no_aux;
   if (aux && aux->m > 0) {
-    if (!pair) return set_error(MP_E_ARG, "grouped GEMM: a fused aux problem needs the CTA-pair kernel");
     if (aux->N % g2::BN != 0 || aux->K % g2::BK != 0 || aux->K <= 0)
       return set_error(MP_E_SHAPE, "grouped GEMM aux problem N=%d K=%d", aux->N, aux->K);
     if (swiglu && aux->out_ld < aux->N / 2) return set_error(MP_E_SHAPE, "aux out_ld %d", aux->out_ld);
@@ -685,7 +693,8 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
   }
   if (grid <= 0) grid = kNumSMs;
   cudaError_t e = launch_pdl_if(pdl, grouped_gemm_kernel, dim3(grid), dim3(gg::kThreads), gg::kSmemBytes, stream, tmA, tmB,
-                             gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs, ps);
+                             gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs, ps,
+                             ax);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_kernel launch");
   return MP_OK;

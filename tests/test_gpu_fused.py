@@ -70,13 +70,28 @@ def test_fused_shared_bit_identical(name, T, monkeypatch):
 @pytest.mark.parametrize("name", ["qwen_small", "ds_mid"])
 @pytest.mark.parametrize("T", [64, 700])
 def test_stream_plan_matches_split_plan(name, T, monkeypatch):
-    """Small batches stream every group over all SMs (1-CTA kernel, shared expert in its own
-    launches) instead of the split / fused plan: same products, different tile shapes, equal
-    within bf16 rounding of the tensor-core accumulation."""
+    """Small batches stream every group over all SMs (1-CTA kernel, shared expert as its aux
+    problem) instead of the split / pair-fused plan: same products, different tile shapes,
+    equal within bf16 rounding of the tensor-core accumulation."""
     shape = _shape(name)
     ref, p0 = _run(shape, T, {}, monkeypatch)
     got, p1 = _run(shape, T, {"MP_STREAM_ROWS": "1000000"}, monkeypatch)
-    assert p0["split_m"] > 0 and p1["split_m"] == 0 and p1["fuse_shared"] == 0 and p1["pair_routed"] == 0
+    assert p0["split_m"] > 0 and p1["split_m"] == 0 and p1["pair_routed"] == 0
+    assert p1["fuse_shared"] == 1      # the shared expert rides in the 1-CTA routed launches
+    r, g = ref.float(), got.float()
+    assert ((g - r).abs().max() <= 1e-2 * r.abs().max() + 1e-3).item()
+    assert ((g - r).norm() / r.norm()).item() <= 5e-3
+
+
+@pytest.mark.parametrize("T", [1, 200, 1000])
+def test_stream_plan_fused_shared_matches_separate(T, monkeypatch):
+    """Stream plan: the shared expert as the aux problem of the 1-CTA launches against its own
+    launches (MP_FUSE_SHARED=0)."""
+    shape = _shape("qwen_small")
+    env = {"MP_STREAM_ROWS": "1000000"}
+    ref, p0 = _run(shape, T, {**env, "MP_FUSE_SHARED": "0"}, monkeypatch)
+    got, p1 = _run(shape, T, env, monkeypatch)
+    assert p0["fuse_shared"] == 0 and p1["fuse_shared"] == 1 and p1["pair_routed"] == 0
     r, g = ref.float(), got.float()
     assert ((g - r).abs().max() <= 1e-2 * r.abs().max() + 1e-3).item()
     assert ((g - r).norm() / r.norm()).item() <= 5e-3
