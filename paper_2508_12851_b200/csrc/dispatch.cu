@@ -105,29 +105,57 @@ __global__ void __launch_bounds__(256)
     const int row = base_s[e] + r;
     s_dst[tid] = dst;
     s_row[tid] = row;
-    pos_dst[size_t(t0) * k + tid] = dst;
-    pos_row[size_t(t0) * k + tid] = row;
-    // where this row's expert output must return: (origin rank, pair index)
-    src_ptrs[dst][row] = int32_t((uint32_t(rank) << 24) | uint32_t(t0 * k + tid));
+    if (blockIdx.y == 0) {
+      pos_dst[size_t(t0) * k + tid] = dst;
+      pos_row[size_t(t0) * k + tid] = row;
+      // where this row's expert output must return: (origin rank, pair index)
+      src_ptrs[dst][row] = int32_t((uint32_t(rank) << 24) | uint32_t(t0 * k + tid));
+    }
   }
   __syncthreads();
   const int warp = warp_id(), lane = lane_id();
-  const int nvec = d / 8;  // 16 B vectors per row
-  for (int tt = warp; tt < nt; tt += 8) {
-    const __nv_bfloat16* src = x + size_t(t0 + tt) * d;
-    uint4 v[kVecPerLane];
+  // blockIdx.y: this CTA's column slice of the rows (small batches spread the row
+  // copies over more SMs; the pair bookkeeping above is repeated, slice 0 writes it)
+  const int nvec_all = d / 8;  // 16 B vectors per row
+  const int per = nvec_all / gridDim.y;
+  const int c_lo = blockIdx.y * per;
+  const int nvec = per;
+  // the next token's row is loaded before this token's k stores are issued (the asm
+  // loads / stores keep program order): one load round trip per warp, not per token
+  auto load_row = [&](int tt, uint4 (&v)[kVecPerLane]) {
+    const __nv_bfloat16* src = x + size_t(t0 + tt) * d + 8 * c_lo;
 #pragma unroll
     for (int i = 0; i < kVecPerLane; ++i) {
       const int c = lane + 32 * i;
       if (c < nvec) v[i] = ld_nc_v4(src + 8 * c);
     }
+  };
+  auto store_row = [&](int tt, const uint4 (&v)[kVecPerLane]) {
     for (int j = 0; j < k; ++j) {
-      __nv_bfloat16* dst = recv_ptrs[s_dst[tt * k + j]] + size_t(s_row[tt * k + j]) * d;
+      __nv_bfloat16* dst = recv_ptrs[s_dst[tt * k + j]] + size_t(s_row[tt * k + j]) * d + 8 * c_lo;
 #pragma unroll
       for (int i = 0; i < kVecPerLane; ++i) {
         const int c = lane + 32 * i;
         if (c < nvec) st_v4(dst + 8 * c, v[i]);
       }
+    }
+  };
+  if (kVecPerLane <= 8) {
+    uint4 va[kVecPerLane], vb[kVecPerLane];
+    int tt = warp;
+    if (tt < nt) load_row(tt, va);
+    for (; tt < nt; tt += 16) {
+      if (tt + 8 < nt) load_row(tt + 8, vb);
+      store_row(tt, va);
+      if (tt + 8 >= nt) break;
+      if (tt + 16 < nt) load_row(tt + 16, va);
+      store_row(tt + 8, vb);
+    }
+  } else {
+    for (int tt = warp; tt < nt; tt += 8) {
+      uint4 v[kVecPerLane];
+      load_row(tt, v);
+      store_row(tt, v);
     }
   }
   // dispatch done: the last CTA raises epoch B once every CTA's rows are visible
@@ -144,12 +172,16 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   if (G < 1 || G > 8 || E < 1 || E > 64) return set_error(MP_E_SHAPE, "permute: G=%d E=%d", G, E);
   if (T <= 0) return MP_OK;
   const int grid = (T + 31) / 32;
-  const int vpl = (d / 8 + 31) / 32;
+  // small batches: split each block's row copies into column slices so that the
+  // grid reaches about one CTA per SM (the copies are bound by per-SM store rate)
+  int ny = 1;
+  while (ny < 16 && grid * ny * 2 <= kNumSMs && (d / 8) % (ny * 2) == 0 && (d / 8) / (ny * 2) >= 32) ny *= 2;
+  const int vpl = ((d / 8) / ny + 31) / 32;
   PeerSync ps = sync ? *sync : PeerSync();
-  if (ps.total > 0) ps.total = grid;
+  if (ps.total > 0) ps.total = grid * ny;
   cudaError_t e;
 #define MP_PERM_LAUNCH(N)                                                                                    \
-  e = launch_pdl(permute_kernel<N>, dim3(grid), dim3(256), 0, stream, x, idx, route, counts_all, parity, blk_prefix, \
+  e = launch_pdl(permute_kernel<N>, dim3(grid, ny), dim3(256), 0, stream, x, idx, route, counts_all, parity, blk_prefix, \
                  src_ptrs, rank, G, T, d, E, k, recv_ptrs, pos_dst, pos_row, ps)
   if (vpl <= 1) MP_PERM_LAUNCH(1);
   else if (vpl <= 2) MP_PERM_LAUNCH(2);
@@ -186,38 +218,52 @@ __global__ void __launch_bounds__(256)
   for (int j = 0; j < K; ++j) wj[j] = w[size_t(t) * K + j];
   const float g = shared_gate ? shared_gate[t] : 1.0f;
   const int nvec = d / 8;
-#pragma unroll 4
-  for (int c = lane; c < nvec; c += 32) {
-    uint4 v[K];
+  // U column vectors per lane per batch: all their loads are issued before any
+  // of their stores (the asm loads / stores keep program order, so an unbatched
+  // loop would serialise one load round trip per vector)
+  constexpr int U = K <= 4 ? 4 : 2;
+  for (int c0 = lane; c0 < nvec; c0 += 32 * U) {
+    uint4 v[U][K], sv[U];
 #pragma unroll
-    for (int j = 0; j < K; ++j) v[j] = ld_cg_v4(src + size_t(j) * d + 8 * c);  // peer-written: L2, not L1/nc
-    float acc[8];
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + 32 * u;
+      if (c < nvec) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      const uint32_t u[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc[2 * q] = fmaf(wj[j], bf16_lo(u[q]), acc[2 * q]);
-        acc[2 * q + 1] = fmaf(wj[j], bf16_hi(u[q]), acc[2 * q + 1]);
+        for (int j = 0; j < K; ++j) v[u][j] = ld_cg_v4(src + size_t(j) * d + 8 * c);  // peer-written: L2
+        if (shared_y) sv[u] = ld_nc_v4(shared_y + size_t(t) * d + 8 * c);
       }
     }
-    if (shared_y) {
-      const uint4 sv = ld_nc_v4(shared_y + size_t(t) * d + 8 * c);
-      const uint32_t u[4] = {sv.x, sv.y, sv.z, sv.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc[2 * q] = fmaf(g, bf16_lo(u[q]), acc[2 * q]);
-        acc[2 * q + 1] = fmaf(g, bf16_hi(u[q]), acc[2 * q + 1]);
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + 32 * u;
+      if (c >= nvec) break;
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const uint32_t q4[4] = {v[u][j].x, v[u][j].y, v[u][j].z, v[u][j].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[2 * q] = fmaf(wj[j], bf16_lo(q4[q]), acc[2 * q]);
+          acc[2 * q + 1] = fmaf(wj[j], bf16_hi(q4[q]), acc[2 * q + 1]);
+        }
       }
+      if (shared_y) {
+        const uint32_t q4[4] = {sv[u].x, sv[u].y, sv[u].z, sv[u].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[2 * q] = fmaf(g, bf16_lo(q4[q]), acc[2 * q]);
+          acc[2 * q + 1] = fmaf(g, bf16_hi(q4[q]), acc[2 * q + 1]);
+        }
+      }
+      uint4 o;
+      o.x = pack_bf16x2(acc[0], acc[1]);
+      o.y = pack_bf16x2(acc[2], acc[3]);
+      o.z = pack_bf16x2(acc[4], acc[5]);
+      o.w = pack_bf16x2(acc[6], acc[7]);
+      st_v4(out + size_t(t) * d + 8 * c, o);
     }
-    uint4 o;
-    o.x = pack_bf16x2(acc[0], acc[1]);
-    o.y = pack_bf16x2(acc[2], acc[3]);
-    o.z = pack_bf16x2(acc[4], acc[5]);
-    o.w = pack_bf16x2(acc[6], acc[7]);
-    st_v4(out + size_t(t) * d + 8 * c, o);
   }
 }
 
