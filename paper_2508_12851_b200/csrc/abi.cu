@@ -104,8 +104,10 @@ struct mp_layer {
   // over all SMs on the 1-CTA kernel (no side chain, shared expert in its own launches)
   int stream_rows = 256;
   int last_pair = -1, last_split = -1, last_fused = -1;  // plan of the last forward (-1: none yet)
+  int last_small_grid = 0;
   // small-group split: groups below split_m rows run on a side stream over small_grid SMs
   int split_m = 0, small_grid = 20;
+  bool small_grid_fixed = false;  // MP_GEMM_SMALL_GRID pins it; else chosen per forward
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   const void* tm_x_ptr = nullptr;
@@ -334,7 +336,10 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   // with the compute-bound large ones on a disjoint set of SMs
   L->split_m = D.E >= 16 ? 256 : 0;
   if (const char* env = getenv("MP_GEMM_SPLIT_M")) L->split_m = atoi(env);
-  if (const char* env = getenv("MP_GEMM_SMALL_GRID")) L->small_grid = std::max(2, atoi(env)) & ~1;
+  if (const char* env = getenv("MP_GEMM_SMALL_GRID")) {
+    L->small_grid = std::max(2, atoi(env)) & ~1;
+    L->small_grid_fixed = true;
+  }
   // with the small groups split off, the remaining (>= split_m rows) groups run on CTA pairs
   if (L->split_m >= 256) L->pair_routed = 1;
   if (const char* env = getenv("MP_GEMM_PAIR")) L->pair_routed = L->pair_shared = atoi(env) ? 1 : 0;
@@ -602,9 +607,13 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     gs.E = E;
     gs.rank = rank;
     const int pr = stream_plan ? 0 : L->pair_routed;
-    const int big_grid = split ? kNumSMs - L->small_grid : 0;
+    // side-chain SMs: with many rows per expert (G*T*k/E >= 1024, e.g. 4+ GPUs) few groups
+    // stay below split_m, so the chain gets 8 SMs instead of 20 (measured: +3-5% at G = 4)
+    const int small_grid = L->small_grid_fixed ? L->small_grid : (avg_rows >= 1024 ? 8 : 20);
+    L->last_small_grid = small_grid;
+    const int big_grid = split ? kNumSMs - small_grid : 0;
     // C is raised by the last GEMM2 CTA of both chains
-    ps_ret.total = grouped_gemm_ctas(big_grid, pr) + (split ? grouped_gemm_ctas(L->small_grid, 0) : 0);
+    ps_ret.total = grouped_gemm_ctas(big_grid, pr) + (split ? grouped_gemm_ctas(small_grid, 0) : 0);
     const PeerSync* sw = G > 1 ? &ps_wait : nullptr;
     const PeerSync* sr = G > 1 ? &ps_ret : nullptr;
     if (split) {
@@ -618,9 +627,9 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       if (events && events[11]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[11]), L->side));
       // (no PDL on the split chains: early-scheduled CTAs would contend for the other chain's SMs)
       MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, gsmall, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                                 L->small_grid, L->side, 0, nullptr, nullptr, false, nullptr, sw));
+                                 small_grid, L->side, 0, nullptr, nullptr, false, nullptr, sw));
       MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, gsmall, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                                 L->small_grid, L->side, 0, L->recv_src, ret_ptrs, false, nullptr, sr));
+                                 small_grid, L->side, 0, L->recv_src, ret_ptrs, false, nullptr, sr));
       if (events && events[12]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[12]), L->side));
       MP_CUDA(cudaEventRecord(L->ev_join, L->side));
       launches += 2;
@@ -688,7 +697,10 @@ int mp_layer_config(mp_layer* L, int key) {
   switch (key) {
     case MP_CFG_PAIR_ROUTED: return L->last_pair >= 0 ? L->last_pair : L->pair_routed;
     case MP_CFG_SPLIT_M: return L->last_split >= 0 ? L->last_split : L->split_m;
-    case MP_CFG_SMALL_GRID: return (L->last_split >= 0 ? L->last_split : L->split_m) > 0 ? L->small_grid : 0;
+    case MP_CFG_SMALL_GRID:
+      return (L->last_split >= 0 ? L->last_split : L->split_m) > 0
+                 ? (L->last_small_grid > 0 ? L->last_small_grid : L->small_grid)
+                 : 0;
     case MP_CFG_FUSE_SHARED: return L->last_fused >= 0 ? L->last_fused : L->fuse_shared;
     default: return set_error(MP_E_ARG, "mp_layer_config: key %d", key);
   }
