@@ -81,6 +81,7 @@ struct mp_layer {
   // scratch views
   __nv_bfloat16 *h = nullptr, *wg = nullptr, *w13s = nullptr, *w2s = nullptr, *hs = nullptr, *ys = nullptr;
   __nv_bfloat16* wg_packed = nullptr;
+  float* wg32 = nullptr;  // Wg in fp32, router consumption order
   float *bias = nullptr, *w = nullptr, *sgate = nullptr;
   int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr, *blk_prefix = nullptr,
           *batch_counts = nullptr, *route_d = nullptr,
@@ -263,6 +264,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       L->h = cv.take<__nv_bfloat16>(size_t(L->recv_cap) * D.f);
       L->wg = cv.take<__nv_bfloat16>(size_t(E_tot) * D.d);
       L->wg_packed = cv.take<__nv_bfloat16>(size_t(router_e_pad(E_tot)) * D.d);
+      L->wg32 = cv.take<float>(size_t(router_e_pad(E_tot)) * D.d);
       L->bias = cv.take<float>(E);
       L->w = cv.take<float>(size_t(T) * k);
       L->sgate = D.shared_gate ? cv.take<float>(T) : nullptr;
@@ -490,6 +492,8 @@ int mp_layer_set_routes(mp_layer* L, const int32_t* route, const int32_t* slot_o
 int mp_layer_prepare_router(mp_layer* L, void* stream) {
   if (!L) return set_error(MP_E_ARG, "mp_layer_prepare_router: null layer");
   MP_CUDA(cudaSetDevice(L->desc.device));
+  MP_TRY(launch_router_pack32(L->wg, L->desc.E + (L->desc.shared_gate ? 1 : 0), L->desc.d, L->wg32,
+                              static_cast<cudaStream_t>(stream)));
   MP_TRY(launch_router_pack(L->wg, L->desc.E + (L->desc.shared_gate ? 1 : 0), L->desc.d, L->wg_packed,
                             static_cast<cudaStream_t>(stream)));
   L->router_ready = true;
@@ -551,7 +555,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   if (T > 0) {
     MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
                          D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
-                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr));
+                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr, L->wg32));
     ++launches;
   } else if (G > 1) {
     // no router / permute on this origin: publish zero counts, raise A and B

@@ -67,7 +67,10 @@ int set_cuda_error(cudaError_t e, const char* what);
 int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
-                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync = nullptr);
+                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync = nullptr,
+                  const float* w32 = nullptr);
+// Wg pre-converted to fp32 in the router's consumption order (E_pad * d floats).
+int launch_router_pack32(const __nv_bfloat16* wg, int E_tot, int d, float* w32, cudaStream_t stream);
 int router_block_tokens();
 __host__ __device__ int router_e_pad(int E_tot);
 int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16* packed, cudaStream_t stream);

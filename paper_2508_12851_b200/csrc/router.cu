@@ -61,6 +61,32 @@ int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16*
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_pack_kernel launch");
 }
 
+// Wg pre-converted to fp32 in the order the router's lanes consume it: float4
+// number t of lane l in (pass, step) sits at ((pass * S + step) * 16 + t) * 32 + l
+// (a warp's load of float4 t is 512 contiguous bytes) and holds experts
+// 8 pass + 4 (t & 1) .. +3 at k = 256 step + 8 l + (t >> 1) -- two
+// (expert 2i, 2i+1) pairs ready for FFMA2, no bf16 conversions in the FMA loop.
+// Same products and chains as the bf16 path (bit-identical logits).
+__global__ void router_pack32_kernel(const __nv_bfloat16* __restrict__ wg, int E_tot, int E_pad, int d,
+                                     float* __restrict__ w32) {
+  const size_t o = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (o >= size_t(E_pad) * d) return;
+  const int S = d / 256;
+  const int i = int(o & 3), l = int((o >> 2) & 31), t = int((o >> 7) & 15);
+  const size_t rest = o >> 11;  // pass * S + step
+  const int st = int(rest % S), p = int(rest / S);
+  const int e = 8 * p + 4 * (t & 1) + i, kk = 256 * st + 8 * l + (t >> 1);
+  w32[o] = e < E_tot ? __bfloat162float(wg[size_t(e) * d + kk]) : 0.0f;
+}
+
+int launch_router_pack32(const __nv_bfloat16* wg, int E_tot, int d, float* w32, cudaStream_t stream) {
+  if (d % 256 != 0) return set_error(MP_E_SHAPE, "router d=%d not a multiple of 256", d);
+  const size_t n = size_t(router_e_pad(E_tot)) * d;
+  router_pack32_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(wg, E_tot, router_e_pad(E_tot), d, w32);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_pack32_kernel launch");
+}
+
 // acc = (acc.lo + x*w.lo, acc.hi + x*w.hi): two independent fp32 FMAs (FFMA2),
 // each rounded exactly like fmaf -- the per-lane chain contract is unchanged.
 MP_DEV void ffma2(unsigned long long& acc, float x, unsigned long long w) {
@@ -89,9 +115,10 @@ constexpr int kExpPerPass = 8;
 // when there are >= 2 passes (E_pad >= 16); with kXSmem the CTA's 32 x rows
 // (contiguous, 32 d bf16) are bulk-copied into shared memory once and every
 // pass reads them from there.
-template <int kWarpsT, bool kXSmem>
+template <int kWarpsT, bool kXSmem, bool kW32>
 __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
     router_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wp,
+                  const float4* __restrict__ w32,
                   const float* __restrict__ bias, int T, int d, int E, int has_gate, int k, int score_mode,
                   int renorm, int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
                   uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
@@ -155,6 +182,39 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
 #pragma unroll
       for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
     const __nv_bfloat16* wr = wp + size_t(e0) * d + 8 * lane;
+    if (kW32) {
+      // fp32 pairs straight from the pre-converted Wg (two halves of 4 k each)
+      const float4* w4 = w32 + size_t(e0 / kExpPerPass) * S * 16 * 32 + lane;
+#pragma unroll 1
+      for (int s = 0; s < S; ++s, w4 += 16 * 32) {
+        uint4 xv[kTokPerWarp];
+#pragma unroll
+        for (int i = 0; i < kTokPerWarp; ++i)
+          xv[i] = kXSmem ? *reinterpret_cast<const uint4*>(xr[i] + 256 * s) : ld_nc_v4(xr[i] + 256 * s);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float4 wv[8];
+#pragma unroll
+          for (int t2 = 0; t2 < 8; ++t2) wv[t2] = __ldg(w4 + (8 * h + t2) * 32);
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {  // strictly ascending k inside the lane's slice
+            const int q = 4 * h + qq;
+            float xs[kTokPerWarp];
+#pragma unroll
+            for (int i = 0; i < kTokPerWarp; ++i) {
+              const uint32_t u = (&xv[i].x)[q >> 1];
+              xs[i] = (q & 1) ? bf16_hi(u) : bf16_lo(u);
+            }
+            const float4 a = wv[2 * qq], b = wv[2 * qq + 1];
+            const unsigned long long w2[4] = {pack2(a.x, a.y), pack2(a.z, a.w), pack2(b.x, b.y), pack2(b.z, b.w)};
+#pragma unroll
+            for (int j = 0; j < kExpPerPass / 2; ++j)
+#pragma unroll
+              for (int i = 0; i < kTokPerWarp; ++i) ffma2(acc[i][j], xs[i], w2[j]);
+          }
+        }
+      }
+    } else
 #pragma unroll(kWarpsT == kQuads ? 2 : 1)
     for (int s = 0; s < S; ++s) {
       uint4 xv[kTokPerWarp], wv[kExpPerPass];
@@ -351,7 +411,7 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
 int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
-                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync) {
+                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync, const float* w32) {
   if (batch_counts && !ticket) return set_error(MP_E_ARG, "router: batch counts need a ticket word");
   if (E < 1 || E > rt::kMaxE) return set_error(MP_E_SHAPE, "router: E=%d outside [1, %d]", E, rt::kMaxE);
   if (k < 1 || k > E || k > rt::kMaxK) return set_error(MP_E_SHAPE, "router: top_k=%d invalid for E=%d", k, E);
@@ -374,18 +434,23 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   int variant = multi_pass ? (x_bytes <= 160 * 1024 ? 2 : 1) : 0;
   if (variant_env >= 0 && variant_env <= 3) variant = variant_env;
   if ((variant == 2 || variant == 3) && x_bytes > 160 * 1024) variant = variant == 2 ? 1 : 0;
-  using KernT = decltype(&router_kernel<kQuads, false>);
-  const KernT kerns[4] = {router_kernel<kQuads, false>, router_kernel<kMaxWarps, false>,
-                          router_kernel<kMaxWarps, true>, router_kernel<kQuads, true>};
-  const KernT kern = kerns[variant];
+  using KernT = decltype(&router_kernel<kQuads, false, false>);
+  const KernT kerns[4] = {router_kernel<kQuads, false, false>, router_kernel<kMaxWarps, false, false>,
+                          router_kernel<kMaxWarps, true, false>, router_kernel<kQuads, true, false>};
+  const KernT kerns32[4] = {router_kernel<kQuads, false, true>, router_kernel<kMaxWarps, false, true>,
+                            router_kernel<kMaxWarps, true, true>, router_kernel<kQuads, true, true>};
+  const char* w32env = getenv("MP_ROUTER_W32");
+  const bool use32 = w32 != nullptr && (w32env == nullptr || atoi(w32env) != 0);
+  const KernT kern = use32 ? kerns32[variant] : kerns[variant];
   const bool xsmem = variant >= 2;
   const int warps = (variant == 1 || variant == 2) ? kMaxWarps : kQuads;
   const size_t smem = std::max(bc_bytes, xsmem ? x_bytes : size_t(0));
-  static size_t smem_set[4] = {0, 0, 0, 0};
-  if (smem > 48 * 1024 && smem > smem_set[variant]) {
+  static size_t smem_set[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const int slot = variant + (use32 ? 4 : 0);
+  if (smem > 48 * 1024 && smem > smem_set[slot]) {
     cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (ea != cudaSuccess) return set_cuda_error(ea, "cudaFuncSetAttribute(router)");
-    smem_set[variant] = smem;
+    smem_set[slot] = smem;
   }
   // small batches: split each block's expert passes over a cluster of up to 8 CTAs so the
   // grid covers the SMs (one CTA per SM for the register-heavy variants)
@@ -415,7 +480,8 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, x, wg_packed, bias, T, d, E, has_gate ? 1 : 0, k, score_mode,
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, x, wg_packed, reinterpret_cast<const float4*>(w32), bias, T, d, E,
+                                     has_gate ? 1 : 0, k, score_mode,
                                      renorm, idx, w, shared_gate, hist, blk_counts, batch_counts, ticket, blk_prefix,
                                      sync ? *sync : PeerSync(), stage_counts ? 1 : 0, csplit);
   if (e == cudaSuccess) e = cudaGetLastError();
