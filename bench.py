@@ -160,6 +160,16 @@ def stage_roofline(shape, T, rows, stage_ms, hbm_gbs):
         ms = stage_ms.get(name, 0.0)
         gbs = b / (ms * 1e-3) / 1e9 if ms > 0 else None
         out[name] = {"bytes": b, "ms": ms, "GB/s": gbs, "frac_hbm": gbs / hbm_gbs if gbs else None}
+    # the router's bit-exact fp32 lane chains make it FMA-issue bound, not HBM bound: its
+    # gate FLOPs against the CUDA-core fp32 FMA peak (148 SMs x 128 lanes x 2 x 1.965 GHz)
+    e_pad = (shape.E + shape.shared_gate + 7) // 8 * 8
+    r_ms = stage_ms.get("router", 0.0)
+    if r_ms > 0:
+        fl = 2.0 * T * e_pad * d
+        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        out["router"].update({"fp32_FLOP": fl, "fp32_TFLOP/s": fl / (r_ms * 1e-3) / 1e12,
+                              "fp32_peak_TFLOP/s": fp32_peak,
+                              "frac_fp32": fl / (r_ms * 1e-3) / 1e12 / fp32_peak})
     return out
 
 
