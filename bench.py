@@ -238,10 +238,34 @@ def cpu_weights(shape, seed, expert_src):
     return out
 
 
-def time_cpu_baseline(shape, seed, T_cpu, budget_s, weights_cpu, wg_np, bias_np, min_reps=1):
+def cpu_threads() -> tuple[int, dict]:
+    """Use every host core for the oracle's numpy BLAS (threadpoolctl sets OpenBLAS' pool; torch's
+    setting does not govern it) and report what actually runs."""
     import torch
-    threads = os.cpu_count() or 1
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     torch.set_num_threads(threads)
+    info = {"cpu_model": None, "blas": None}
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        threadpool_limits(threads)
+        pools = [p for p in threadpool_info() if p.get("user_api") == "blas"]
+        if pools:
+            info["blas"] = f"{pools[0].get('internal_api')} {pools[0].get('version')}, {pools[0].get('num_threads')} threads"
+            threads = int(pools[0].get("num_threads", threads))
+    except Exception:
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu_model"] = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return threads, info
+
+
+def time_cpu_baseline(shape, seed, T_cpu, budget_s, weights_cpu, wg_np, bias_np, min_reps=1):
+    threads, _ = cpu_threads()
     cpu_layer_sample(shape, min(T_cpu, 32), seed, weights_cpu, wg_np, bias_np)  # warm (BLAS init)
     reps, t0 = 0, time.perf_counter()
     while True:
@@ -390,6 +414,11 @@ def main_b200(args):
     # expert slots this GPU streamed per step (groups with rows) -- the weight bytes of K3
     active_local = int(sum(1 for e in range(shape.E)
                            if sum(counts_last[s, e] for s in range(G) if layer.route[s, e] == rank) > 0))
+    # K4 wire bytes of this GPU: token rows it dispatched to peers (inside the permute kernel)
+    # and expert-output rows it returned to peers (inside its GEMM2 epilogue)
+    sent_rows = int(sum(counts_last[rank, e] for e in range(shape.E) if layer.route[rank, e] != rank))
+    ret_rows = int(sum(counts_last[s, e] for s in range(G) for e in range(shape.E)
+                       if s != rank and layer.route[s, e] == rank))
 
     # ---- e2e: the same forward through the public API with HOST buffers: every step copies its
     # x from pinned host memory and its output back (HostPipeline overlaps the copies of
@@ -425,16 +454,37 @@ def main_b200(args):
     stage_mean = stage_ms.mean(axis=0)
     stage_t = torch.tensor(stage_mean, dtype=torch.float64, device=dev)
     gemm_local = float(gemm1_ms.mean() + gemm2_ms.mean())
-    rank_t = torch.tensor([recv_rows, gemm_local, active_local], dtype=torch.float64, device=dev)
+    stage_local = dict(zip(_lib.STAGES, stage_mean.tolist()))
+    rank_t = torch.tensor([recv_rows, gemm_local, active_local, sent_rows, ret_rows,
+                           stage_local["permute_dispatch"], float(gemm2_ms.mean())], dtype=torch.float64,
+                          device=dev)
     if world > 1:
         dist.all_reduce(stage_t, op=dist.ReduceOp.MAX)
         parts = [torch.zeros_like(rank_t) for _ in range(world)]
         dist.all_gather(parts, rank_t)
         per_rank = [(int(p[0].item()), float(p[1].item())) for p in parts]
         active_list = [int(p[2].item()) for p in parts]
+        k4_rank = [p[3:].tolist() for p in parts]
     else:
         per_rank = [(recv_rows, gemm_local)]
         active_list = [active_local]
+        k4_rank = [[sent_rows, ret_rows, stage_local["permute_dispatch"], float(gemm2_ms.mean())]]
+    # K4 over NVLink: dispatch wire rate = a GPU's outgoing token rows / its permute-kernel time
+    # (rows are stored to the peers' receive buffers by that kernel); the return rides the GEMM2
+    # epilogue, so its rate is bounded by the GEMM, reported as bytes / GEMM2 time
+    nvl_peak = 770.0
+    k4 = None
+    if G > 1:
+        row_b = shape.d * 2
+        disp = [r[0] * row_b / (r[2] * 1e-3) / 1e9 if r[2] > 0 else 0.0 for r in k4_rank]
+        retr = [r[1] * row_b / (r[3] * 1e-3) / 1e9 if r[3] > 0 else 0.0 for r in k4_rank]
+        k4 = {"dispatch_bytes_per_gpu": [int(r[0] * row_b) for r in k4_rank],
+              "return_bytes_per_gpu": [int(r[1] * row_b) for r in k4_rank],
+              "dispatch_GBps_per_gpu": disp, "return_GBps_per_gpu": retr,
+              "dispatch_frac_of_peer_copy": max(disp) / nvl_peak, "peak_GBps": nvl_peak,
+              "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+              "note": "dispatch = outgoing rows / permute kernel time (the kernel also writes the local rows); "
+                      "return = rows sent back / GEMM2 time (the stores ride the GEMM epilogue)"}
     rows_list = [r for r, _ in per_rank]
 
     # naive placement accounting on the same counts (counts do not depend on placement)
@@ -453,7 +503,10 @@ def main_b200(args):
     hot = int(np.argmax(rows_list))
     flops = 2.0 * rows_list[hot] * 3 * shape.d * shape.f + shared_flops
     achieved_tflops = per_rank_tf[hot]
-    peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    # headline against the burst peak (the timed region is K short steps, not the seconds-long
+    # power-capped loop the sustained figure was measured in); sustained reported beside it
+    peak = float(peaks.get("bf16_tflops"))
+    peak_sus = float(peaks.get("bf16_tflops_sustained", peak))
     # the same launches seen from HBM: every active expert slot's weights are streamed once
     # (+ the shared expert's when fused); small batches are bound by this, not by the tensor pipe
     w_bytes = active_list[hot] * shape.expert_bytes + (3 * shape.d * shape.shared_f * 2 if exec_plan["fuse_shared"]
@@ -484,7 +537,7 @@ def main_b200(args):
         wg_np = wg.float().cpu().numpy()
         rate, reps, el, thr = time_cpu_baseline(shape, seed, args.cpu_tokens, args.cpu_seconds, wcpu, wg_np,
                                                 bias.numpy())
-        cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port",
+        cpu = {"value": rate, "unit": UNIT, "cores": thr, "kind": "port", **cpu_threads()[1],
                "sample": f"oracle/moe_oracle.py numpy fp32 layer forward, {shape.name} shape, {args.cpu_tokens} "
                          f"tokens x {reps} reps ({el:.1f} s), all experts local, {thr} threads"}
 
@@ -516,6 +569,8 @@ def main_b200(args):
             "ours": {k: acc_ours[k] for k in ("remote_invocations", "remote_bytes", "wire_bytes", "local_ratio")},
             "uniform": {k: acc_naive[k] for k in ("remote_invocations", "remote_bytes", "wire_bytes", "local_ratio")},
             "recv_rows_per_gpu": rows_list,
+            "gpus_active": int(sum(1 for r in rows_list if r > 0)),
+            "k4_nvlink": k4,
         },
         "stages_ms": {name: float(v) for name, v in zip(_lib.STAGES, stage_t.tolist()) if name != "unused"},
         "stage_roofline": stage_roofline(shape, T, rows_list[hot], dict(zip(_lib.STAGES, stage_t.tolist())),
@@ -533,13 +588,15 @@ def main_b200(args):
                                                      if exec_plan["fuse_shared"] else ""),
                      "achieved_per_rank": per_rank_tf,
                      **({"achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved_tflops / peak if peak else None}
+                         "frac": achieved_tflops / peak if peak else None,
+                         "peak_sustained": peak_sus, "frac_sustained": achieved_tflops / peak_sus}
                         if bound == "tensor" else
                         {"achieved": w_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": w_gbs / hbm_peak if w_gbs else None,
                          "tensor_view": {"achieved": achieved_tflops, "peak": peak, "unit": "TFLOP/s"}}),
                      "traffic": traffic,
-                     "peak_source": f"{peaks_src} bf16 sustained (kernel timed inside the step)",
+                     "peak_source": f"{peaks_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops); "
+                                    "frac_sustained against the power-capped bf16_tflops_sustained",
                      "flops_per_step": flops,
                      "weights": {"bytes_per_step": w_bytes, "GB/s": w_gbs, "peak_GB/s": hbm_peak,
                                  "frac": w_gbs / hbm_peak if w_gbs else None,
@@ -565,6 +622,49 @@ def main_b200(args):
 
 
 # ----------------------------------------------------------------------------- reference arm
+def time_reference_package(shape, G: int, seed: int, budget_s: float = 8.0) -> dict | None:
+    """The reference package's own hot-path Python, single-threaded as written (BASELINE.md CPU
+    plan item 2): `sim.run` on a synthetic workload of this shape over G servers (its
+    `_dispatch_layer` invocations/s, sim.py:441-463 -- analytic comm/comp, no layer arithmetic),
+    `stats_from_requests` (sim.py:194-205 -> ActivationStats.ingest, stats.py:82-96) and
+    `build_placement("ours")` (placement.py:541-566)."""
+    from paper_2508_12851_b200.errors import import_moeplace
+    from paper_2508_12851_b200.shapes import cluster_spec, model_spec, slot_caps
+    mp = import_moeplace()
+    if mp is None:
+        return None
+    import moeplace.sim as msim
+    Gs = max(G, 3 if shape.E == 8 and shape.d == 512 else 2)
+    cluster = cluster_spec(shape, Gs, slot_caps(shape, Gs))
+    model = model_spec(shape)
+    tm = mp.TimeModel.from_cluster(cluster)
+    policy = msim.SchedulerPolicy(migration_enabled=False)
+    n_req = 200
+    while True:
+        wl = msim.WorkloadSpec.synthetic(Gs, 0.05, n_req, tokens=64, seed=seed)
+        reqs = msim.generate_workload(wl, model)
+        t0 = time.perf_counter()
+        stats = msim.stats_from_requests(reqs, model, Gs)
+        t_stats = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        placement = mp.build_placement("ours", cluster, model, stats, seed)
+        t_place = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        m = msim.run(cluster, model, "ours", reqs, tm, policy, initial_stats=stats, seed=seed)
+        t_run = time.perf_counter() - t0
+        if t_run >= budget_s / 4 or n_req >= 20000:
+            break
+        n_req = min(20000, int(n_req * max(2.0, budget_s / 4 / max(t_run, 1e-3))))
+    inv = len(reqs) * model.num_layers * model.top_k
+    toks = sum(int(r.tokens) for r in reqs)
+    del placement, m
+    return {"what": "reference moeplace package, 1 thread as written: sim.run (analytic comm/comp -- it "
+                    "simulates the layer, no arithmetic), stats_from_requests, build_placement('ours')",
+            "servers": Gs, "requests": len(reqs), "tokens_per_request": 64,
+            "sim_run_s": t_run, "sim_invocations_per_s": inv / t_run, "sim_tokens_per_s": toks / t_run,
+            "stats_from_requests_ms": t_stats * 1e3, "build_placement_ms": t_place * 1e3}
+
+
 def main_reference(args):
     """The reference's CPU path for this workload: the oracle port (the reference itself has no
     layer arithmetic -- SPEC.md:8 -- so its CPU implementation is the restatement in oracle/)."""
@@ -577,8 +677,7 @@ def main_reference(args):
 
     shape = get_shape(args.config)
     seed = args.seed
-    threads = os.cpu_count() or 1
-    torch.set_num_threads(threads)
+    threads, cinfo = cpu_threads()
     T_cpu = args.cpu_tokens
     oshape = orc.LayerShape(shape.name, shape.d, shape.f, shape.E, shape.k, shape.score_mode, shape.renorm,
                             shape.shared_f, shape.shared_gate)
@@ -610,6 +709,10 @@ def main_reference(args):
         step()
     el = time.perf_counter() - t0
     value = args.steps * T_cpu / el
+    try:
+        ref_pkg = time_reference_package(shape, max(1, args.gpus), seed)
+    except Exception as ex:  # reported, never fatal for the arm
+        ref_pkg = {"error": repr(ex)}
     line = {
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
@@ -617,9 +720,10 @@ def main_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{shape.name} MoE layer on the host CPU, {T_cpu} tokens per step (bounded sample)",
                    "model": shape.name, "tokens_per_step": T_cpu},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", **cinfo,
                          "sample": f"oracle/moe_oracle.py numpy fp32, {T_cpu} tokens/step x {args.steps} steps"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_package": ref_pkg,
     }
     print(json.dumps(line), flush=True)
 
@@ -876,8 +980,25 @@ def measure_peer_copy(layer, world, rank):
     return float(bw.item())
 
 
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: re-exec this script under
+    torch.distributed.run with one process per GPU (127.0.0.1 rendezvous); rank 0's single JSON
+    line comes through on stdout."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
+
+
 if __name__ == "__main__":
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ and a.impl != "reference":
+        raise SystemExit(self_launch(a))
     if a.scenario == "shift" and a.impl != "reference":
         main_shift(a)
         raise SystemExit(0)

@@ -32,7 +32,8 @@
 extern "C" {
 #endif
 
-#define MP_ABI_VERSION 1
+#define MP_ABI_VERSION 2
+#define MP_MAX_GROUPS 128 /* expert groups per mp_grouped_gemm call */
 
 #define MP_OK 0
 #define MP_E_ARG -1        /* bad argument (null pointer, unknown mode)                  */
@@ -61,6 +62,11 @@ int mp_last_error(char* buf, int buf_len);
  * shared-expert gate row. */
 int mp_router_pack(const void* wg_bf16, int E_tot, int d, void* packed, void* stream);
 
+/* Wg [E_tot, d] bf16 pre-converted to fp32 in K1's lane-consumption order
+ * (E_pad * d floats; the layer's default router operand): same products and
+ * chains as the bf16 operand, so the logits are bit-identical. */
+int mp_router_pack32(const void* wg_bf16, int E_tot, int d, float* packed32, void* stream);
+
 /* K1 -- replaces ActivationStats.ingest (stats.py:82-96) fed by sampled expert
  * sets (sim.py:181-185): top-k routing of T tokens plus a fused histogram.
  *   x        [T, d] bf16           packed  from mp_router_pack (E + has_gate rows)
@@ -73,12 +79,24 @@ int mp_router_pack(const void* wg_bf16, int E_tot, int d, void* packed, void* st
 int mp_router_topk_hist(const void* x, const void* packed, const float* bias, int T, int d, int E, int has_gate,
                         int k, int score_mode, int renorm, int32_t* idx, float* w, float* gate_out, uint32_t* hist,
                         void* stream);
+/* The same with the fp32 operand of mp_router_pack32 (`packed32`), the kernels
+ * mp_layer_forward runs; `packed` (bf16) must still be given. */
+int mp_router_topk_hist_f32w(const void* x, const void* packed, const float* packed32, const float* bias, int T,
+                             int d, int E, int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w,
+                             float* gate_out, uint32_t* hist, void* stream);
+/* Logits-in parity variant of K1's selection stage: top-k (descending, ties ->
+ * lower id), gate weights and histogram from fp32 logits [T][ld] (+ bias [E]
+ * or NULL) -- pins the selection rule independently of the dot products. */
+int mp_router_topk_logits(const float* logits, int ld, const float* bias, int T, int E, int k, int score_mode,
+                          int renorm, int32_t* idx, float* w, uint32_t* hist, void* stream);
 
 /* K3 -- replaces comp_time (cost.py:132-136).  Grouped GEMM on tcgen05:
  *   for g < *n_groups: rows [a_row, a_row+m) of A [a_rows, K] times slot `slot`
  *   of B (rows slot*N .. slot*N+N of B [b_rows, K]) -> out rows [o_row, o_row+m).
  *   swiglu = 1: B holds interleaved gate/up blocks of 128 rows, out [*, N/2].
- *   groups (device) = n x {a_row, m, slot, o_row}; n_groups (device) int32.   */
+ *   groups (device) = n x {a_row, m, slot, o_row}; n_groups (device) int32,
+ *   at most MP_MAX_GROUPS (else MP_E_SHAPE; this parity entry reads it with a
+ *   stream sync).                                                             */
 int mp_grouped_gemm(const void* a, int64_t a_rows, const void* b, int64_t b_rows, const int32_t* groups,
                     const int32_t* n_groups, int N, int K, void* out, int out_ld, int swiglu, void* stream);
 
@@ -107,8 +125,9 @@ typedef struct mp_layer_desc {
 /* Device pointers of the layer's buffers (for filling weights and for
  * parity inspection).  Sizes in elements. */
 typedef struct mp_layer_ptrs {
-  void* w13_pool;    /* [n_slots][2f][d] bf16, gate/up interleaved per 128 rows  */
-  void* w2_pool;     /* [n_slots][d][f] bf16                                     */
+  void* pool;        /* expert slot s at pool + s * slot_bytes (n_slots slots), holding
+                        [W13: 2f x d bf16, gate/up rows interleaved per 128 rows | W2: d x f bf16]
+                        -- one contiguous m_e-byte block per slot (migration copies it whole) */
   void* wg;          /* [E + shared_gate][d] bf16 router weights (packed on set)  */
   float* bias;       /* [E] fp32                                                 */
   void* w13_shared;  /* [2*shared_f][d] bf16 or NULL                             */

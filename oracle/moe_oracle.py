@@ -315,6 +315,8 @@ class OracleResult:
     pos_row: list = field(default_factory=list)
     recv_M: np.ndarray | None = None
     shared_gate: list = field(default_factory=list)
+    mag: list = field(default_factory=list)  # per origin [T, d]: sum_j |w_j y_j| (+ |g ysh|), the
+                                             # magnitude the per-element tolerance is relative to
 
 
 def moe_layer_forward(shape: LayerShape, xs, wg, biases, route, experts, shared=None, wsg=None) -> OracleResult:
@@ -348,7 +350,7 @@ def moe_layer_forward(shape: LayerShape, xs, wg, biases, route, experts, shared=
         pos_dst.append(dst)
         pos_row.append(rows)
     # expert outputs per (origin, token, slot)
-    outs = []
+    outs, mags = [], []
     for s in range(G):
         T = xs[s].shape[0]
         y = np.zeros((T, k, shape.d), dtype=np.float32)
@@ -356,14 +358,18 @@ def moe_layer_forward(shape: LayerShape, xs, wg, biases, route, experts, shared=
             sel = np.nonzero(idxs[s] == e)
             y[sel] = swiglu_ffn(xs[s][sel[0]], *experts[int(e)])
         acc = np.zeros((T, shape.d), dtype=np.float32)
+        mag = np.zeros((T, shape.d), dtype=np.float32)
         for j in range(k):
             acc = acc + ws[s][:, j:j + 1] * y[:, j, :]
+            mag = mag + np.abs(ws[s][:, j:j + 1] * y[:, j, :])
         if shared is not None:
             ysh = swiglu_ffn(xs[s], *shared)
             g = gates[s][:, None] if wsg is not None else np.float32(1.0)
             acc = acc + g * ysh
+            mag = mag + np.abs(g * ysh)
         outs.append(bf16_round(acc.astype(np.float32)))
-    return OracleResult(outs, idxs, ws, hists, counts, route, pos_dst, pos_row, M, gates)
+        mags.append(mag)
+    return OracleResult(outs, idxs, ws, hists, counts, route, pos_dst, pos_row, M, gates, mags)
 
 
 # ----------------------------------------------------------------------------- accounting

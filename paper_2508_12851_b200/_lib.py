@@ -14,7 +14,8 @@ from pathlib import Path
 from .errors import DimensionMismatch, InfeasibleError, UnplacedExpertError
 
 LIB_PATH = Path(__file__).resolve().parent / "libmoeplace_b200.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
+MAX_GROUPS = 128
 
 MP_OK = 0
 MP_E_ARG = -1
@@ -38,7 +39,8 @@ CFG_KEYS = {"pair_routed": 0, "split_m": 1, "small_grid": 2, "fuse_shared": 3}
 
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
-    "mp_abi_version", "mp_last_error", "mp_router_pack", "mp_router_topk_hist", "mp_grouped_gemm",
+    "mp_abi_version", "mp_last_error", "mp_router_pack", "mp_router_pack32", "mp_router_topk_hist",
+    "mp_router_topk_hist_f32w", "mp_router_topk_logits", "mp_grouped_gemm",
     "mp_layer_create", "mp_layer_destroy", "mp_layer_get_ptrs", "mp_layer_export_handles",
     "mp_layer_open_peers", "mp_layer_set_routes", "mp_layer_prepare_router", "mp_layer_forward",
     "mp_layer_forward_timed",
@@ -57,7 +59,7 @@ class LayerDesc(Structure):
 
 class LayerPtrs(Structure):
     _fields_ = [
-        ("w13_pool", c_void_p), ("w2_pool", c_void_p), ("wg", c_void_p), ("bias", c_void_p),
+        ("pool", c_void_p), ("wg", c_void_p), ("bias", c_void_p),
         ("w13_shared", c_void_p), ("w2_shared", c_void_p), ("idx", c_void_p), ("w", c_void_p),
         ("pos_dst", c_void_p), ("pos_row", c_void_p), ("recv", c_void_p), ("h", c_void_p), ("ret", c_void_p),
         ("recv_src", c_void_p),
@@ -92,7 +94,10 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         "mp_abi_version": ([], I),
         "mp_last_error": ([c_char_p, I], I),
         "mp_router_pack": ([V, I, I, V, V], I),
+        "mp_router_pack32": ([V, I, I, V, V], I),
         "mp_router_topk_hist": ([V, V, V, I, I, I, I, I, I, I, V, V, V, V, V], I),
+        "mp_router_topk_hist_f32w": ([V, V, V, V, I, I, I, I, I, I, I, V, V, V, V, V], I),
+        "mp_router_topk_logits": ([V, I, V, I, I, I, I, I, V, V, V, V], I),
         "mp_grouped_gemm": ([V, I64, V, I64, V, V, I, I, V, I, I, V], I),
         "mp_layer_create": ([POINTER(LayerDesc), POINTER(c_void_p)], I),
         "mp_layer_destroy": ([V], I),

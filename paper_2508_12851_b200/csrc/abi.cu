@@ -12,6 +12,7 @@
 #include <cstring>
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -41,6 +42,33 @@ bool pdl_enabled() {
 
 int set_cuda_error(cudaError_t e, const char* what) {
   return set_error(MP_E_CUDA, "%s: %s (%d)", what, cudaGetErrorString(e), int(e));
+}
+
+int ensure_max_dyn_smem(const void* kernel, size_t bytes, const char* what) {
+  if (bytes <= 48 * 1024) return MP_OK;
+  struct Entry {
+    const void* fn;
+    int dev;
+    size_t bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return set_cuda_error(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  for (Entry& x : done)
+    if (x.fn == kernel && x.dev == dev) {
+      if (x.bytes >= bytes) return MP_OK;
+      e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+      if (e != cudaSuccess) return set_cuda_error(e, what);
+      x.bytes = bytes;
+      return MP_OK;
+    }
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e != cudaSuccess) return set_cuda_error(e, what);
+  done.push_back({kernel, dev, bytes});
+  return MP_OK;
 }
 
 }  // namespace mp
@@ -87,6 +115,9 @@ struct mp_layer {
           *batch_counts = nullptr, *route_d = nullptr,
           *slot_of_d = nullptr;
   uint32_t *hist = nullptr, *err = nullptr, *ticket = nullptr, *sync_state = nullptr;
+  // peer-timeout bits mirrored into mapped pinned host memory: read by the next forward
+  volatile uint32_t* err_host = nullptr;
+  uint32_t* err_host_d = nullptr;
   uint32_t *perm_ticket = nullptr, *ret_ticket = nullptr;  // arrival counters of the raising kernels
   void** ptr_arrays = nullptr;  // device: recv[8], ret[8], flags[8], counts0[8], counts1[8], recv_src[8]
 
@@ -178,9 +209,38 @@ int mp_router_topk_hist(const void* x, const void* packed, const float* bias, in
                        idx, w, gate_out, hist, nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream));
 }
 
+int mp_router_pack32(const void* wg_bf16, int E_tot, int d, float* packed32, void* stream) {
+  if (!wg_bf16 || !packed32) return set_error(MP_E_ARG, "mp_router_pack32: null pointer");
+  return launch_router_pack32(static_cast<const __nv_bfloat16*>(wg_bf16), E_tot, d, packed32,
+                              static_cast<cudaStream_t>(stream));
+}
+
+int mp_router_topk_hist_f32w(const void* x, const void* packed, const float* packed32, const float* bias, int T,
+                             int d, int E, int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w,
+                             float* gate_out, uint32_t* hist, void* stream) {
+  if (!x || !packed || !packed32 || !idx || !w) return set_error(MP_E_ARG, "mp_router_topk_hist_f32w: null pointer");
+  return launch_router(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(packed), bias, T, d,
+                       E, has_gate, k, score_mode, renorm, idx, w, gate_out, hist, nullptr, nullptr, nullptr, nullptr,
+                       static_cast<cudaStream_t>(stream), nullptr, packed32);
+}
+
+int mp_router_topk_logits(const float* logits, int ld, const float* bias, int T, int E, int k, int score_mode,
+                          int renorm, int32_t* idx, float* w, uint32_t* hist, void* stream) {
+  if ((!logits || !idx || !w) && T > 0) return set_error(MP_E_ARG, "mp_router_topk_logits: null pointer");
+  return launch_router_logits(logits, ld, bias, T, E, k, score_mode, renorm, idx, w, hist,
+                              static_cast<cudaStream_t>(stream));
+}
+
 int mp_grouped_gemm(const void* a, int64_t a_rows, const void* b, int64_t b_rows, const int32_t* groups,
                     const int32_t* n_groups, int N, int K, void* out, int out_ld, int swiglu, void* stream) {
   if (!a || !b || !groups || !n_groups || !out) return set_error(MP_E_ARG, "mp_grouped_gemm: null pointer");
+  // the group count lives on the device (the kernel reads it in its prologue); this
+  // stateless entry reads it once so an oversized table fails instead of being clipped
+  int32_t ng = 0;
+  MP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  MP_CUDA(cudaMemcpy(&ng, n_groups, 4, cudaMemcpyDeviceToHost));
+  if (ng < 0 || ng > MP_MAX_GROUPS)
+    return set_error(MP_E_SHAPE, "mp_grouped_gemm: n_groups=%d outside [0, %d]", ng, MP_MAX_GROUPS);
   CUtensorMap ta, tb;
   int pair = 0;
   if (const char* env = getenv("MP_GEMM_PAIR")) pair = atoi(env);
@@ -197,7 +257,8 @@ int mp_grouped_gemm(const void* a, int64_t a_rows, const void* b, int64_t b_rows
 int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   if (!desc || !out) return set_error(MP_E_ARG, "mp_layer_create: null pointer");
   MP_TRY(validate_desc(*desc));
-  MP_CUDA(cudaSetDevice(desc->device));
+  DeviceGuard dg(desc->device);
+  MP_CUDA(dg.status);
   cudaDeviceProp prop;
   MP_CUDA(cudaGetDeviceProperties(&prop, desc->device));
   if (prop.major != 10)
@@ -302,6 +363,19 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       return fail(set_cuda_error(e, "cudaMemset(scratch)"));
   }
 
+  // ---- peer-error word in mapped pinned host memory (no sync needed to read it)
+  {
+    void* hp = nullptr;
+    if ((e = cudaHostAlloc(&hp, 64, cudaHostAllocMapped | cudaHostAllocPortable)) != cudaSuccess)
+      return fail(set_cuda_error(e, "cudaHostAlloc(error word)"));
+    memset(hp, 0, 64);
+    L->err_host = static_cast<volatile uint32_t*>(hp);
+    void* dp = nullptr;
+    if ((e = cudaHostGetDevicePointer(&dp, hp, 0)) != cudaSuccess)
+      return fail(set_cuda_error(e, "cudaHostGetDevicePointer(error word)"));
+    L->err_host_d = static_cast<uint32_t*>(dp);
+  }
+
   // ---- own pointer arrays (peers filled by mp_layer_open_peers)
   {
     void* host[6 * 8] = {};
@@ -375,7 +449,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
 
 int mp_layer_destroy(mp_layer* L) {
   if (!L) return MP_OK;
-  cudaSetDevice(L->desc.device);
+  DeviceGuard dg(L->desc.device);
   for (int p = 0; p < 8; ++p) {
     if (L->peer_window[p]) cudaIpcCloseMemHandle(L->peer_window[p]);
     if (L->peer_pool[p]) cudaIpcCloseMemHandle(L->peer_pool[p]);
@@ -384,6 +458,7 @@ int mp_layer_destroy(mp_layer* L) {
   if (L->ev_join) cudaEventDestroy(L->ev_join);
   if (L->side) cudaStreamDestroy(L->side);
   if (L->scratch) cudaFree(L->scratch);
+  if (L->err_host) cudaFreeHost(const_cast<uint32_t*>(L->err_host));
   if (L->window) cudaFree(L->window);
   if (L->pool) cudaFree(L->pool);
   delete L;
@@ -393,8 +468,7 @@ int mp_layer_destroy(mp_layer* L) {
 int mp_layer_get_ptrs(mp_layer* L, mp_layer_ptrs* o) {
   if (!L || !o) return set_error(MP_E_ARG, "mp_layer_get_ptrs: null pointer");
   memset(o, 0, sizeof(*o));
-  o->w13_pool = L->w13;
-  o->w2_pool = L->w2;
+  o->pool = L->pool;
   o->wg = L->wg;
   o->bias = L->bias;
   o->w13_shared = L->w13s;
@@ -418,7 +492,8 @@ int mp_layer_get_ptrs(mp_layer* L, mp_layer_ptrs* o) {
 int mp_layer_export_handles(mp_layer* L, void* handles_out) {
   if (!L || !handles_out) return set_error(MP_E_ARG, "mp_layer_export_handles: null pointer");
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  MP_CUDA(cudaSetDevice(L->desc.device));
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
   cudaIpcMemHandle_t hw, hp;
   MP_CUDA(cudaIpcGetMemHandle(&hw, L->window));
   MP_CUDA(cudaIpcGetMemHandle(&hp, L->pool));
@@ -429,7 +504,8 @@ int mp_layer_export_handles(mp_layer* L, void* handles_out) {
 
 int mp_layer_open_peers(mp_layer* L, const void* all_handles) {
   if (!L || !all_handles) return set_error(MP_E_ARG, "mp_layer_open_peers: null pointer");
-  MP_CUDA(cudaSetDevice(L->desc.device));
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
   const uint8_t* h = static_cast<const uint8_t*>(all_handles);
   void* host[6 * 8] = {};
   for (int p = 0; p < L->G; ++p) {
@@ -479,7 +555,8 @@ int mp_layer_set_routes(mp_layer* L, const int32_t* route, const int32_t* slot_o
                          s, slot_of[e]);
     }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  MP_CUDA(cudaSetDevice(L->desc.device));
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
   // small synchronous staging: route tables change once per placement
   std::vector<int32_t> r(route, route + G * E), so(slot_of, slot_of + E);
   MP_CUDA(cudaMemcpyAsync(L->route_d, r.data(), r.size() * 4, cudaMemcpyHostToDevice, st));
@@ -491,7 +568,8 @@ int mp_layer_set_routes(mp_layer* L, const int32_t* route, const int32_t* slot_o
 
 int mp_layer_prepare_router(mp_layer* L, void* stream) {
   if (!L) return set_error(MP_E_ARG, "mp_layer_prepare_router: null layer");
-  MP_CUDA(cudaSetDevice(L->desc.device));
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
   MP_TRY(launch_router_pack32(L->wg, L->desc.E + (L->desc.shared_gate ? 1 : 0), L->desc.d, L->wg32,
                               static_cast<cudaStream_t>(stream)));
   MP_TRY(launch_router_pack(L->wg, L->desc.E + (L->desc.shared_gate ? 1 : 0), L->desc.d, L->wg_packed,
@@ -508,6 +586,12 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   if (!L->routes_set) return set_error(MP_E_UNPLACED, "mp_layer_forward: route table not set");
   if (!L->router_ready) return set_error(MP_E_ARG, "mp_layer_forward: router weights not prepared");
   if (!L->peers_open) return set_error(MP_E_PEER, "mp_layer_forward: peers not opened (G=%d)", L->G);
+  // a peer wait of an earlier forward timed out: its outputs were garbage and the
+  // protocol is out of step -- refuse to run (read from mapped host memory, no sync)
+  if (const uint32_t bad = *L->err_host)
+    return set_error(MP_E_PEER, "an earlier forward timed out waiting for NVLink peers (ranks mask 0x%x)", bad);
+  DeviceGuard dg(D.device);
+  MP_CUDA(dg.status);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int G = L->G, E = D.E, k = D.top_k, rank = L->rank;
   auto** recv_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 0 * 8);
@@ -541,6 +625,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     ps0.count_ptrs = count_ptrs;
     ps0.state = L->sync_state;
     ps0.err = L->err;
+    ps0.err_host = L->err_host_d;
     ps0.G = G;
     ps0.rank = rank;
   }
@@ -713,6 +798,8 @@ int mp_layer_config(mp_layer* L, int key) {
 int mp_layer_read_counts(mp_layer* L, int32_t* host_counts, void* stream) {
   if (!L || !host_counts) return set_error(MP_E_ARG, "mp_layer_read_counts: null pointer");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
   MP_CUDA(cudaStreamSynchronize(st));
   const int G = L->G, E = L->desc.E;
   if (G == 1) {
@@ -727,16 +814,20 @@ int mp_layer_read_counts(mp_layer* L, int32_t* host_counts, void* stream) {
 
 int mp_layer_check(mp_layer* L, void* stream) {
   if (!L) return set_error(MP_E_ARG, "mp_layer_check: null layer");
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
   MP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   uint32_t err = 0;
   MP_CUDA(cudaMemcpy(&err, L->err, 4, cudaMemcpyDeviceToHost));
+  err |= *L->err_host;
   if (err) return set_error(MP_E_PEER, "NVLink flag wait timed out on ranks mask 0x%x", err);
   return MP_OK;
 }
 
 int mp_layer_migrate(mp_layer* L, const mp_copy_op* ops, int n_ops, void* stream, void* done_event) {
   if (!L || (n_ops > 0 && !ops)) return set_error(MP_E_ARG, "mp_layer_migrate: null pointer");
-  MP_CUDA(cudaSetDevice(L->desc.device));
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int S = L->desc.n_slots;
   for (int i = 0; i < n_ops; ++i) {

@@ -35,7 +35,7 @@ constexpr int kStages = 4;
 constexpr int kABytes = BM * BK * 2;  // 16 KB
 constexpr int kBBytes = BN * BK * 2;  // 32 KB
 constexpr int kStageBytes = kABytes + kBBytes;
-constexpr int kMaxGroups = 128;
+constexpr int kMaxGroups = MP_MAX_GROUPS;
 constexpr int kThreads = 256;
 constexpr int kTmemCols = 512;
 constexpr size_t kSmemBytes = 1024 /*align slack*/ + size_t(kStages) * kStageBytes + 4096;
@@ -668,13 +668,9 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
   }
   const AuxProblem& ax = (aux && aux->m > 0) ? *aux : no_aux;
   if (pair) {  // the B map must have 128-row boxes (each CTA loads half of N)
-    static bool attr2 = false;
-    if (!attr2) {
-      cudaError_t e = cudaFuncSetAttribute(grouped_gemm_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(g2::kSmemBytes));
-      if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(grouped_gemm_2sm)");
-      attr2 = true;
-    }
+    const int ra = ensure_max_dyn_smem(reinterpret_cast<const void*>(grouped_gemm_2sm_kernel), g2::kSmemBytes,
+                                       "cudaFuncSetAttribute(grouped_gemm_2sm)");
+    if (ra != MP_OK) return ra;
     if (grid <= 0) grid = kNumSMs;
     grid &= ~1;
     cudaError_t e = launch_pdl_if(pdl, grouped_gemm_2sm_kernel, dim3(grid), dim3(gg::kThreads), g2::kSmemBytes, stream, tmA,
@@ -684,13 +680,9 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
     if (e != cudaSuccess) return set_cuda_error(e, "grouped_gemm_2sm_kernel launch");
     return MP_OK;
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(grouped_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(gg::kSmemBytes));
-    if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(grouped_gemm)");
-    attr_set = true;
-  }
+  const int ra = ensure_max_dyn_smem(reinterpret_cast<const void*>(grouped_gemm_kernel), gg::kSmemBytes,
+                                     "cudaFuncSetAttribute(grouped_gemm)");
+  if (ra != MP_OK) return ra;
   if (grid <= 0) grid = kNumSMs;
   cudaError_t e = launch_pdl_if(pdl, grouped_gemm_kernel, dim3(grid), dim3(gg::kThreads), gg::kSmemBytes, stream, tmA, tmB,
                              gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs, ps,

@@ -53,6 +53,8 @@ struct PeerSync {
   int32_t* const* count_ptrs = nullptr;  // [2][8] count-table halves (router only)
   uint32_t* state = nullptr;             // [0] epoch, [1] forwards seen, [2] count parity
   uint32_t* err = nullptr;               // timeout bits (mp_layer_check)
+  uint32_t* err_host = nullptr;          // the same bits in mapped pinned host memory: the next
+                                         // mp_layer_forward reads them without a sync
   uint32_t* ticket = nullptr;            // arrival counter of a raising kernel
   int G = 1, rank = 0;
   int wait = 0;    // this launch waits for state[0] before touching peer-written rows
@@ -63,6 +65,24 @@ struct PeerSync {
 int set_error(int code, const char* fmt, ...);
 int set_cuda_error(cudaError_t e, const char* what);
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device attribute: raise it
+// once per (kernel, current device) to at least `bytes` (thread-safe).
+int ensure_max_dyn_smem(const void* kernel, size_t bytes, const char* what);
+
+// Makes `device` current for the scope and restores the caller's device after.
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t status = cudaSuccess;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != device) status = cudaSetDevice(device);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
 // ---- K1 router
 int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
@@ -71,6 +91,8 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
                   const float* w32 = nullptr);
 // Wg pre-converted to fp32 in the router's consumption order (E_pad * d floats).
 int launch_router_pack32(const __nv_bfloat16* wg, int E_tot, int d, float* w32, cudaStream_t stream);
+int launch_router_logits(const float* logits, int ld, const float* bias, int T, int E, int k, int score_mode,
+                         int renorm, int32_t* idx, float* w, uint32_t* hist, cudaStream_t stream);
 int router_block_tokens();
 __host__ __device__ int router_e_pad(int E_tot);
 int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16* packed, cudaStream_t stream);

@@ -1,7 +1,9 @@
 // Device side of PeerSync (mp_internal.h): the NVLink flag protocol folded into
 // the layer kernels.  All waits are bounded (kPeerTimeoutNs): on timeout the
-// missing ranks' bits are set in the error word that mp_layer_check reports,
-// and the kernel proceeds instead of hanging the GPU.
+// missing ranks' bits are set in the error word -- in device memory for
+// mp_layer_check and in mapped host memory, which the next mp_layer_forward
+// reads before launching anything and turns into MP_E_PEER -- and the kernel
+// proceeds (its outputs are garbage) instead of hanging the GPU.
 #pragma once
 
 #include "common.cuh"
@@ -18,7 +20,8 @@ MP_DEV void peer_wait(const PeerSync& ps, uint32_t epoch) {
     const uint64_t t0 = globaltimer_ns();
     while (int32_t(ld_acquire_sys_u32(mine + p) - epoch) < 0) {
       if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
-        atomicOr(ps.err, 1u << p);
+        const uint32_t bits = atomicOr(ps.err, 1u << p) | (1u << p);
+        if (ps.err_host != nullptr) st_release_sys_u32(ps.err_host, bits);
         break;
       }
       __nanosleep(64);

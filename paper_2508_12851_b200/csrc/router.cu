@@ -100,6 +100,59 @@ MP_DEV unsigned long long pack2(float lo, float hi) {
 // Larger logit wins; equal logits -> lower expert id.
 MP_DEV bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
 
+// Warp-collective top-k + gate weights of one token from its logits (lane l holds
+// experts l and l + 32): k rounds of a warp arg-max (larger logit, ties -> lower
+// id), then softmax over the k (mode 0) or over all E (mode 1, optional
+// renormalisation).  Lane 0 writes idx_row / w_row and bumps cnt_s.
+MP_DEV void select_topk_store(float v0, float v1, int E, int k, int score_mode, int renorm, int32_t* idx_row,
+                              float* w_row, int* cnt_s) {
+  const int lane = lane_id();
+  bool taken0 = lane >= E, taken1 = lane + 32 >= E;
+  float sel_v[rt::kMaxK];
+  int sel_i[rt::kMaxK];
+  for (int j = 0; j < k; ++j) {
+    float bv = -INFINITY;
+    int bi = 0x7fffffff;
+    if (!taken0) { bv = v0; bi = lane; }
+    if (!taken1 && (bi == 0x7fffffff || better(v1, lane + 32, bv, bi))) { bv = v1; bi = lane + 32; }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (oi != 0x7fffffff && (bi == 0x7fffffff || better(ov, oi, bv, bi))) { bv = ov; bi = oi; }
+    }
+    sel_v[j] = bv;
+    sel_i[j] = bi;
+    if (bi == lane) taken0 = true;
+    if (bi == lane + 32) taken1 = true;
+  }
+  // weights
+  const float mx = sel_v[0];
+  float denom;
+  if (score_mode == 0) {
+    denom = 0.f;
+    for (int j = 0; j < k; ++j) denom += expf(sel_v[j] - mx);
+  } else {
+    float s = (lane < E ? expf(v0 - mx) : 0.f) + (lane + 32 < E ? expf(v1 - mx) : 0.f);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    denom = s;
+  }
+  if (lane == 0) {
+    float wsum = 0.f;
+    float wj[rt::kMaxK];
+    for (int j = 0; j < k; ++j) {
+      wj[j] = expf(sel_v[j] - mx) / denom;
+      wsum += wj[j];
+    }
+    for (int j = 0; j < k; ++j) {
+      idx_row[j] = sel_i[j];
+      w_row[j] = (score_mode == 1 && renorm) ? wj[j] / wsum : wj[j];
+      atomicAdd(&cnt_s[sel_i[j]], 1);
+    }
+  }
+}
+
 #ifndef MP_ROUTER_MIN_BLOCKS
 #define MP_ROUTER_MIN_BLOCKS 1
 #endif
@@ -282,51 +335,10 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
   for (int tt = warp; tt < rt::kTokens; tt += blockDim.x / 32) {
     const int t = t0 + tt;
     if (t >= T) break;
-    float v0 = lane < E ? logits[tt][lane] : -INFINITY;
-    float v1 = lane + 32 < E ? logits[tt][lane + 32] : -INFINITY;
-    bool taken0 = lane >= E, taken1 = lane + 32 >= E;
-    float sel_v[rt::kMaxK];
-    int sel_i[rt::kMaxK];
-    for (int j = 0; j < k; ++j) {
-      float bv = -INFINITY;
-      int bi = 0x7fffffff;
-      if (!taken0) { bv = v0; bi = lane; }
-      if (!taken1 && (bi == 0x7fffffff || better(v1, lane + 32, bv, bi))) { bv = v1; bi = lane + 32; }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (oi != 0x7fffffff && (bi == 0x7fffffff || better(ov, oi, bv, bi))) { bv = ov; bi = oi; }
-      }
-      sel_v[j] = bv;
-      sel_i[j] = bi;
-      if (bi == lane) taken0 = true;
-      if (bi == lane + 32) taken1 = true;
-    }
-    // weights
-    const float mx = sel_v[0];
-    float denom;
-    if (score_mode == 0) {
-      denom = 0.f;
-      for (int j = 0; j < k; ++j) denom += expf(sel_v[j] - mx);
-    } else {
-      float s = (lane < E ? expf(v0 - mx) : 0.f) + (lane + 32 < E ? expf(v1 - mx) : 0.f);
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-      denom = s;
-    }
+    const float v0 = lane < E ? logits[tt][lane] : -INFINITY;
+    const float v1 = lane + 32 < E ? logits[tt][lane + 32] : -INFINITY;
+    select_topk_store(v0, v1, E, k, score_mode, renorm, idx + size_t(t) * k, wout + size_t(t) * k, cnt_s);
     if (lane == 0) {
-      float wsum = 0.f;
-      float wj[rt::kMaxK];
-      for (int j = 0; j < k; ++j) {
-        wj[j] = expf(sel_v[j] - mx) / denom;
-        wsum += wj[j];
-      }
-      for (int j = 0; j < k; ++j) {
-        idx[size_t(t) * k + j] = sel_i[j];
-        wout[size_t(t) * k + j] = (score_mode == 1 && renorm) ? wj[j] / wsum : wj[j];
-        atomicAdd(&cnt_s[sel_i[j]], 1);
-      }
       if (has_gate && shared_gate != nullptr) {
         const float g = logits[tt][E];
         shared_gate[t] = 1.0f / (1.0f + expf(-g));
@@ -408,6 +420,47 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
   if (tid == 0) *ticket = 0u;  // ready for the next launch (stream-ordered)
 }
 
+// Logits-in parity variant of K1's selection stage: the same warp top-k, gate
+// weights and block-aggregated histogram, from caller-given fp32 logits [T][ld]
+// (+ bias).  One warp per token, 8 tokens per CTA.
+__global__ void __launch_bounds__(256) router_logits_kernel(const float* __restrict__ logits, int ld,
+                                                            const float* __restrict__ bias, int T, int E, int k,
+                                                            int score_mode, int renorm, int32_t* __restrict__ idx,
+                                                            float* __restrict__ wout, uint32_t* __restrict__ hist) {
+  __shared__ int cnt_s[rt::kMaxE];
+  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
+  __syncthreads();
+  const int t = blockIdx.x * (blockDim.x / 32) + warp;
+  if (t < T) {
+    const float* row = logits + size_t(t) * ld;
+    float v0 = lane < E ? row[lane] : -INFINITY;
+    float v1 = lane + 32 < E ? row[lane + 32] : -INFINITY;
+    if (bias != nullptr) {
+      if (lane < E) v0 = __fadd_rn(v0, bias[lane]);
+      if (lane + 32 < E) v1 = __fadd_rn(v1, bias[lane + 32]);
+    }
+    select_topk_store(v0, v1, E, k, score_mode, renorm, idx + size_t(t) * k, wout + size_t(t) * k, cnt_s);
+  }
+  __syncthreads();
+  if (hist != nullptr)
+    for (int e = tid; e < E; e += blockDim.x)
+      if (cnt_s[e]) atomicAdd(&hist[e], uint32_t(cnt_s[e]));
+}
+
+int launch_router_logits(const float* logits, int ld, const float* bias, int T, int E, int k, int score_mode,
+                         int renorm, int32_t* idx, float* w, uint32_t* hist, cudaStream_t stream) {
+  if (E < 1 || E > rt::kMaxE) return set_error(MP_E_SHAPE, "router: E=%d outside [1, %d]", E, rt::kMaxE);
+  if (k < 1 || k > E || k > rt::kMaxK) return set_error(MP_E_SHAPE, "router: top_k=%d invalid for E=%d", k, E);
+  if (ld < E) return set_error(MP_E_SHAPE, "router: logits row stride %d < E=%d", ld, E);
+  if (score_mode != 0 && score_mode != 1) return set_error(MP_E_ARG, "router: score_mode %d", score_mode);
+  if (T <= 0) return MP_OK;
+  router_logits_kernel<<<unsigned((T + 7) / 8), 256, 0, stream>>>(logits, ld, bias, T, E, k, score_mode, renorm,
+                                                                   idx, w, hist);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_logits_kernel launch");
+}
+
 int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
@@ -445,12 +498,9 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   const bool xsmem = variant >= 2;
   const int warps = (variant == 1 || variant == 2) ? kMaxWarps : kQuads;
   const size_t smem = std::max(bc_bytes, xsmem ? x_bytes : size_t(0));
-  static size_t smem_set[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const int slot = variant + (use32 ? 4 : 0);
-  if (smem > 48 * 1024 && smem > smem_set[slot]) {
-    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (ea != cudaSuccess) return set_cuda_error(ea, "cudaFuncSetAttribute(router)");
-    smem_set[slot] = smem;
+  {
+    const int ra = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(router)");
+    if (ra != MP_OK) return ra;
   }
   // small batches: split each block's expert passes over a cluster of up to 8 CTAs so the
   // grid covers the SMs (one CTA per SM for the register-heavy variants)

@@ -81,7 +81,7 @@ class B200MoELayer:
         dev = self.device
         self.n_phys_slots = n_phys
         self.slot_elems = int(p.slot_bytes) // 2
-        self.pool = _view(p.w13_pool, (n_phys, self.slot_elems), torch.bfloat16, dev) if n_phys else None
+        self.pool = _view(p.pool, (n_phys, self.slot_elems), torch.bfloat16, dev) if n_phys else None
         self.wg = _view(p.wg, (E + shape.shared_gate, d), torch.bfloat16, dev)
         self.bias = _view(p.bias, (E,), torch.float32, dev)
         self.idx = _view(p.idx, (T, k), torch.int32, dev)

@@ -12,6 +12,7 @@ import numpy as np
 import pytest
 
 from oracle import moe_oracle as orc
+from tolerance import check_gemm_close
 
 torch = pytest.importorskip("torch")
 
@@ -79,11 +80,7 @@ def test_grouped_gemm_matches_torch(swiglu, ms, K, N, pair, monkeypatch):
     ref = _ref_gemm(a, b, ms, slots, N, swiglu)
     got = out[:rows].float()
     assert torch.isfinite(got).all()
-    err = (got - ref).abs().max().item()
-    scale = ref.abs().max().item()
-    assert err <= 2e-2 * scale + 1e-3, (err, scale)
-    rel = ((got - ref).norm() / ref.norm()).item()
-    assert rel < 1e-2, rel
+    check_gemm_close(got.cpu().numpy(), ref.cpu().numpy())
     # rows outside every group are untouched
     assert torch.isnan(out[rows:].float()).all()
 
@@ -108,7 +105,9 @@ def test_grouped_gemm_large_k_many_tiles(pair, monkeypatch):
     assert rel < 1e-2, rel
 
 
-def _run_router(x, wg, bias, E, k, mode, gate):
+def _run_router(x, wg, bias, E, k, mode, gate, w32=0):
+    """mp_router_topk_hist (bf16 Wg operand) or, w32 = 1, mp_router_topk_hist_f32w (the fp32
+    consumption-order operand mp_layer_forward uses)."""
     L, lib = _lib()
     T, d = x.shape
     xt = torch.from_numpy(x).cuda().bfloat16()
@@ -120,19 +119,27 @@ def _run_router(x, wg, bias, E, k, mode, gate):
     w = torch.empty(T, k, dtype=torch.float32, device="cuda")
     go = torch.empty(T, dtype=torch.float32, device="cuda")
     hist = torch.zeros(E, dtype=torch.int32, device="cuda")
-    L.check(lib.mp_router_topk_hist(_vp(xt), _vp(packed), _vp(bt), T, d, E, gate, k, mode, 0, _vp(idx), _vp(w),
-                                    _vp(go) if gate else None, _vp(hist), _stream()))
+    if w32:
+        p32 = torch.empty((E + gate + 7) // 8 * 8 * d, device="cuda", dtype=torch.float32)
+        L.check(lib.mp_router_pack32(_vp(wgt), E + gate, d, _vp(p32), _stream()))
+        L.check(lib.mp_router_topk_hist_f32w(_vp(xt), _vp(packed), _vp(p32), _vp(bt), T, d, E, gate, k, mode, 0,
+                                             _vp(idx), _vp(w), _vp(go) if gate else None, _vp(hist), _stream()))
+    else:
+        L.check(lib.mp_router_topk_hist(_vp(xt), _vp(packed), _vp(bt), T, d, E, gate, k, mode, 0, _vp(idx), _vp(w),
+                                        _vp(go) if gate else None, _vp(hist), _stream()))
     torch.cuda.synchronize()
-    return idx.cpu().numpy(), w.cpu().numpy(), hist.cpu().numpy()
+    return idx.cpu().numpy(), w.cpu().numpy(), hist.cpu().numpy(), go.cpu().numpy()
 
 
+@pytest.mark.parametrize("w32", [0, 1], ids=["wg_bf16", "wg_f32"])
 @pytest.mark.parametrize("split", ["", "1", "2", "4", "8"])
 @pytest.mark.parametrize("variant", ["", "0", "1", "2", "3"])
 @pytest.mark.parametrize("E,k,mode,d", [(8, 2, 0, 512), (64, 6, 1, 256), (16, 4, 0, 4096)])
-def test_router_ties_go_to_the_lower_expert(E, k, mode, d, variant, split, monkeypatch):
+def test_router_ties_go_to_the_lower_expert(E, k, mode, d, variant, split, w32, monkeypatch):
     """Exact logit ties (duplicated router rows + biases, all-zero tokens whose logits are the
     biases alone) resolve to the lower expert id, bit-exact with the oracle -- in every router
-    variant (8 or 16 warps, x from HBM or staged in smem; "" = the shape's default)."""
+    variant (8 or 16 warps, x from HBM or staged in smem; "" = the shape's default), with the
+    bf16 Wg operand and with the fp32 consumption-order operand the layer runs."""
     if variant:
         monkeypatch.setenv("MP_ROUTER_VARIANT", variant)
     if split:  # passes split over a cluster of CTAs, logits gathered in the leader's smem
@@ -148,7 +155,7 @@ def test_router_ties_go_to_the_lower_expert(E, k, mode, d, variant, split, monke
     bias[3] = bias[4] = bias[6] = np.float32(bias.max())   # three-way tie among the biases
     lg = orc.router_logits(x, wg, bias)
     idx_ref, w_ref = orc.topk_route(lg, E, k, mode)
-    idx, w, hist = _run_router(x, wg, bias, E, k, mode, 0)
+    idx, w, hist, _ = _run_router(x, wg, bias, E, k, mode, 0, w32)
     assert np.array_equal(idx, idx_ref)
     assert np.array_equal(hist, orc.histogram(idx_ref, E))
     np.testing.assert_allclose(w, w_ref, rtol=1e-5, atol=1e-6)
@@ -159,32 +166,52 @@ def test_router_ties_go_to_the_lower_expert(E, k, mode, d, variant, split, monke
                 assert pos[lo] < pos[hi], row
 
 
+@pytest.mark.parametrize("w32", [0, 1], ids=["wg_bf16", "wg_f32"])
 @pytest.mark.parametrize("E,k,mode,gate,d,T", [(8, 2, 0, 0, 512, 333), (64, 6, 1, 0, 256, 200), (60, 4, 1, 1, 512, 64),
                                                (8, 2, 0, 0, 4096, 48), (16, 4, 0, 0, 4096, 100)])
-def test_router_bit_exact(E, k, mode, gate, d, T):
-    L, lib = _lib()
+def test_router_bit_exact(E, k, mode, gate, d, T, w32):
     x = orc.synthetic_tokens(0, T, d, seed=3)
     wg = orc.synthetic_router(E + gate, d, seed=3)
     bias = orc.origin_bias(1, E, seed=3)
     lg = orc.router_logits(x, wg, bias)
     idx_ref, w_ref = orc.topk_route(lg, E, k, mode)
     hist_ref = orc.histogram(idx_ref, E)
+    idx, w, hist, go = _run_router(x, wg, bias, E, k, mode, gate, w32)
+    assert np.array_equal(idx, idx_ref)
+    assert np.array_equal(hist, hist_ref)
+    np.testing.assert_allclose(w, w_ref, rtol=1e-5, atol=1e-6)
+    if gate:
+        g_ref = 1.0 / (1.0 + np.exp(-lg[:, E].astype(np.float64)))
+        np.testing.assert_allclose(go, g_ref, rtol=1e-5, atol=1e-6)
 
-    xt = torch.from_numpy(x).cuda().bfloat16()
-    wgt = torch.from_numpy(wg).cuda().bfloat16()
-    packed = torch.empty((E + gate + 7) // 8 * 8 * d, device="cuda", dtype=torch.bfloat16)
-    L.check(lib.mp_router_pack(_vp(wgt), E + gate, d, _vp(packed), _stream()))
+
+@pytest.mark.parametrize("E,k,mode,renorm", [(8, 2, 0, 0), (64, 6, 1, 0), (60, 4, 1, 1), (33, 8, 1, 0), (1, 1, 0, 0)])
+def test_router_logits_in_selection(E, k, mode, renorm):
+    """mp_router_topk_logits: K1's selection stage from given logits -- random logits plus rows
+    of exact ties (all equal, pairs, a tied top) -- indices and histogram bit-exact, weights to
+    fp32 rounding, against the oracle's selection rule."""
+    L, lib = _lib()
+    rng = np.random.default_rng(E * 10 + k)
+    T = 257
+    lg = rng.standard_normal((T, E)).astype(np.float32)
+    lg[1] = 0.5                                  # all tied: lowest ids first
+    lg[2, 1::2] = lg[2, 0::2][: lg[2, 1::2].size]  # adjacent pairs tied
+    lg[3, -1] = lg[3, 0] = np.float32(lg[3].max() + 1)  # tied top: 0 before E-1
+    bias = rng.standard_normal(E).astype(np.float32) * np.float32(0.1)
+    bias[-1] = bias[0]
+    ref_lg = (lg + bias[None, :]).astype(np.float32)
+    idx_ref, w_ref = orc.topk_route(ref_lg, E, k, mode, renorm)
+    ld = E + 3
+    buf = np.zeros((T, ld), np.float32)
+    buf[:, :E] = lg
+    lt = torch.from_numpy(buf).cuda()
     bt = torch.from_numpy(bias).cuda()
     idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
     w = torch.empty(T, k, dtype=torch.float32, device="cuda")
-    go = torch.empty(T, dtype=torch.float32, device="cuda")
     hist = torch.zeros(E, dtype=torch.int32, device="cuda")
-    L.check(lib.mp_router_topk_hist(_vp(xt), _vp(packed), _vp(bt), T, d, E, gate, k, mode, 0, _vp(idx), _vp(w),
-                                    _vp(go) if gate else None, _vp(hist), _stream()))
+    L.check(lib.mp_router_topk_logits(_vp(lt), ld, _vp(bt), T, E, k, mode, renorm, _vp(idx), _vp(w), _vp(hist),
+                                      _stream()))
     torch.cuda.synchronize()
     assert np.array_equal(idx.cpu().numpy(), idx_ref)
-    assert np.array_equal(hist.cpu().numpy(), hist_ref)
+    assert np.array_equal(hist.cpu().numpy(), orc.histogram(idx_ref, E))
     np.testing.assert_allclose(w.cpu().numpy(), w_ref, rtol=1e-5, atol=1e-6)
-    if gate:
-        g_ref = 1.0 / (1.0 + np.exp(-lg[:, E].astype(np.float64)))
-        np.testing.assert_allclose(go.cpu().numpy(), g_ref, rtol=1e-5, atol=1e-6)

@@ -1,8 +1,9 @@
 """Single-GPU parity of the whole MoE-layer forward (G = 1) against the oracle.
 
 Bit-exact: routed indices, histogram, per-pair receive positions, count table.
-Tolerance (floating point, stated): per element |out - ref| <= 2e-2 * max|ref|
-+ 1e-3 and relative Frobenius error <= 1e-2 (bf16 intermediates on both sides).
+Tolerance (floating point, stated in tests/tolerance.py): per element
+|out - ref| <= 2^-6 * sum_j |w_j y_j| + 1e-5 * max|ref| (two to four bf16 ulps of
+the contributing terms) and relative Frobenius error <= 3e-3.
 """
 
 import numpy as np
@@ -13,7 +14,7 @@ from oracle import moe_oracle as orc
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-ATOL_SCALE, ATOL, RTOL_FRO = 2e-2, 1e-3, 1e-2
+from tolerance import check_layer_close
 
 
 def _shape(name):
@@ -47,12 +48,8 @@ def _build_layer(shape, T, experts, shared, wg, bias, cap=None):
     return layer
 
 
-def _check_close(got, ref):
-    err = np.abs(got - ref).max()
-    scale = np.abs(ref).max()
-    assert err <= ATOL_SCALE * scale + ATOL, (err, scale)
-    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
-    assert rel <= RTOL_FRO, rel
+def _check_close(got, ref, mag):
+    check_layer_close(got, ref, mag)
 
 
 @pytest.mark.parametrize("pair", ["0", "1"], ids=["cta1", "cta_pair"])
@@ -82,7 +79,7 @@ def test_layer_g1_matches_oracle(name, T, pair, monkeypatch):
     rows = ref.pos_row[0].ravel()
     recv = layer.recv[: rows.max() + 1].float().cpu().numpy()
     np.testing.assert_array_equal(recv[rows], np.repeat(x, shape.k, axis=0))
-    _check_close(out.float().cpu().numpy(), ref.out[0])
+    _check_close(out.float().cpu().numpy(), ref.out[0], ref.mag[0])
     acc = layer.dispatch_accounting()
     assert acc["remote_invocations"] == 0 and acc["local_ratio"] == 1.0
     layer.close()
@@ -174,5 +171,5 @@ def test_large_batch_block_scan_from_global():
     assert np.array_equal(layer.idx[:T].cpu().numpy(), ref.idx[0])
     assert np.array_equal(layer.read_counts(), ref.counts)
     assert np.array_equal(layer.pos_row[:T].cpu().numpy(), ref.pos_row[0])
-    _check_close(out.float().cpu().numpy(), ref.out[0])
+    _check_close(out.float().cpu().numpy(), ref.out[0], ref.mag[0])
     layer.close()

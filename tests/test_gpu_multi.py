@@ -1,7 +1,8 @@
-"""Multi-GPU parity (G = 2 / 3 / 4 / 8): one torchrun process per rank running tests/mgpu_worker.py.
+"""Multi-GPU parity (G = 2 / 3 / 4 / 8): one torchrun process per GPU running tests/mgpu_worker.py.
 
-G = 8 also runs on a 4-GPU box with two ranks per GPU (co-resident processes time-slice
-the GPU): it checks the 8-rank flag protocol, layouts and migration, not speed."""
+A case runs only when the box has at least G GPUs: the layer kernels spin on flags their
+peers' kernels raise, so two ranks must never share one GPU.  The 8-rank host logic
+(layouts, route tables, migration rounds) is covered on CPU by tests/test_dist_gloo.py."""
 
 import socket
 import subprocess
@@ -26,9 +27,8 @@ def _free_port():
 
 @pytest.mark.parametrize("G", [2, 3, 4, 8])
 def test_multi_gpu_layer_matches_oracle(G):
-    need = 4 if G == 8 else G
-    if torch.cuda.device_count() < need:
-        pytest.skip(f"needs {need} GPUs, have {torch.cuda.device_count()}")
+    if torch.cuda.device_count() < G:
+        pytest.skip(f"needs {G} GPUs, have {torch.cuda.device_count()}")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(REPO / "tests" / "mgpu_worker.py")]
     res = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=900)
