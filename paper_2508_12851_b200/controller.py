@@ -58,39 +58,28 @@ class MigrationController:
 
     # ---------------------------------------------------------------- execution
     def migrate(self, candidate, side_stream: torch.cuda.Stream | None = None, while_copying=None) -> dict:
-        """Execute an adopted plan: NVLink pulls on `side_stream`, `while_copying()` (e.g. a few
-        forwards on the old placement) overlapped with them, then the route swap on every GPU
-        (`migration_complete`) and a fresh statistics window.  Returns copy accounting."""
+        """Execute an adopted plan: NVLink pulls on `side_stream` in cap-respecting rounds
+        (migration.plan_rounds: at most cap + 1 resident experts per GPU, every expert covered at
+        every instant), `while_copying()` (e.g. a few forwards on the current placement) overlapped
+        with each round's copies, the route swap after each round (`migration_complete`), then a
+        fresh statistics window.  Returns copy accounting."""
         import torch.distributed as dist
 
         layer = self.layer
         world = layer.world
         old_sets = gpu_expert_sets(self.placement, 0)
         new_sets = gpu_expert_sets(candidate, 0)
-        slot_maps = [None] * world
-        if world > 1:
-            dist.all_gather_object(slot_maps, layer.slot_of.tolist(), group=self.group)
-        else:
-            slot_maps = [layer.slot_of.tolist()]
-        side = side_stream or torch.cuda.Stream(layer.device)
-        cur = torch.cuda.current_stream(layer.device)
-        t0, done = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        side.wait_stream(cur)
-        t0.record(side)
-        adds = layer.migrate_async(old_sets, new_sets, slot_maps, side, done)
-        n_overlap = 0
-        if while_copying is not None:
-            n_overlap = while_copying() or 0
-        done.synchronize()
-        copy_ms = t0.elapsed_time(done)
-        if world > 1:
-            dist.barrier(group=self.group)  # every GPU's copies landed before any route swaps
+        # physical slots of every GPU: the reference's per-GPU cap (packable_capacity,
+        # domain.py:395-401) plus the staging slot(s) every layer reserves
+        phys = [int(self.mp.packable_capacity(self.cluster, n, self.model)) + layer.staging_slots
+                for n in range(world)]
         lat = np.asarray(self.cluster.link_latency, dtype=float)
         bw = np.asarray(self.cluster.link_bandwidth, dtype=float)
-        layer.finish_migration(new_sets, adds, lat, bw)
+        res = layer.migrate(old_sets, new_sets, phys_slots=phys, stream=side_stream, while_copying=while_copying,
+                            link_latency=lat, link_bandwidth=bw, group=self.group)
         self.placement = candidate
         self.reset_window()
-        n_add, t_copy = len(adds), copy_ms
+        n_add, t_copy = len(res["adds"]), res["copy_ms"]
         if world > 1:
             dev = layer.device if dist.get_backend(self.group) == "nccl" else "cpu"
             a = torch.tensor([float(n_add)], dtype=torch.float64, device=dev)
@@ -99,7 +88,7 @@ class MigrationController:
             dist.all_reduce(b, op=dist.ReduceOp.MAX, group=self.group)
             n_add, t_copy = int(a.item()), float(b.item())
         rec = {"slots_copied": n_add, "bytes_copied": n_add * layer.shape.expert_bytes, "copy_ms_max_gpu": t_copy,
-               "forwards_during_copy": n_overlap}
+               "rounds": res["rounds"], "forwards_during_copy": res["forwards_during_copy"]}
         self.history.append(rec)
         return rec
 

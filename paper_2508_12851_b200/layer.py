@@ -12,8 +12,9 @@ One object per (process, GPU).  It owns an `mp_layer` of the C ABI
 * `dispatch_accounting()` -- remote invocations / bytes of the last forward in
   the reference's accounting (sim.py:452-456);
 * `migrate(...)` -- executes `migration_cost`'s slot diff (cost.py:186-187)
-  with NVLink peer copies on a side stream, then swaps routes after
-  completion (sim.py:520-525).
+  with NVLink peer copies on a side stream, in rounds that keep every GPU
+  within its cap + one staging slot and every expert covered, swapping routes
+  only after each round's copies landed (sim.py:520-525).
 
 PyTorch is used for device memory views, streams and `torch.distributed`
 plumbing only; every kernel on the path lives in the CUDA library.
@@ -29,8 +30,8 @@ import torch
 
 from . import _lib
 from .errors import InfeasibleError
-from .migration import plan_pulls
-from .routing import dispatch_accounting, gpu_expert_sets, route_table, route_table_for
+from .migration import Round, plan_rounds
+from .routing import dispatch_accounting, gpu_expert_sets, route_table, route_table_for, uniform_links
 from .shapes import LayerShape
 
 
@@ -56,17 +57,18 @@ def interleave_w13(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
 
 class B200MoELayer:
     def __init__(self, shape: LayerShape, *, rank: int = 0, world: int = 1, device: int | None = None,
-                 max_tokens: int = 4096, cap_slots: int | None = None, staging_slots: int | None = None):
-        """cap_slots = floor(GpuSpec.memory / m_e) (domain.py:395-401); staging slots (default =
-        cap) hold incoming experts while a migration is in flight, so old copies retire only after
-        new ones land."""
+                 max_tokens: int = 4096, cap_slots: int | None = None, staging_slots: int = 1):
+        """cap_slots = floor(GpuSpec.memory / m_e) (domain.py:395-401) expert slots plus
+        `staging_slots` (default ONE) that hold incoming experts while a migration is in flight,
+        so old copies retire only after new ones land -- the physical pool is
+        cap + 1 slots; `migrate` orders the copies into rounds within that bound."""
         self.lib = _lib.load()
         self.shape = shape
         self.rank, self.world = rank, world
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.max_tokens = max_tokens
         self.cap_slots = shape.E if cap_slots is None else int(cap_slots)
-        self.staging_slots = self.cap_slots if staging_slots is None else int(staging_slots)
+        self.staging_slots = int(staging_slots)
         n_phys = self.cap_slots + self.staging_slots
         desc = _lib.LayerDesc(rank=rank, world=world, device=self.device.index, max_tokens=max_tokens, d=shape.d,
                               f=shape.f, E=shape.E, top_k=shape.k, score_mode=shape.score_mode, renorm=shape.renorm,
@@ -201,11 +203,8 @@ class B200MoELayer:
     def set_placement_sets(self, gpu_sets, weight_source, link_latency=None, link_bandwidth=None) -> None:
         """Same as set_placement from plain per-GPU expert lists (uniform links by default)."""
         G, E = self.world, self.shape.E
-        if link_latency is None:
-            link_latency = np.full((G, G), 3e-6)
-            np.fill_diagonal(link_latency, 0.0)
-        if link_bandwidth is None:
-            link_bandwidth = np.full((G, G), 770e9)
+        if link_latency is None or link_bandwidth is None:
+            link_latency, link_bandwidth = uniform_links(G)
         route = route_table([frozenset(s) for s in gpu_sets], E, link_latency, link_bandwidth, self.shape.d)
         slot_of = self.load_experts(gpu_sets[self.rank], weight_source)
         torch.cuda.synchronize(self.device)
@@ -291,45 +290,86 @@ class B200MoELayer:
         return dispatch_accounting(self.read_counts(), self.route, self.shape.d)
 
     # ------------------------------------------------------------------ migration
-    def plan_migration(self, old_sets, new_sets):
-        """Copy ops for this GPU: every expert added here pulls from the lowest-id old holder
-        (the slot diff `new.slots - old.slots` of migration_cost, cost.py:186-187)."""
-        pulls = plan_pulls(self.rank, old_sets, new_sets, self._free)
-        return [(p.src_rank, p.expert, p.dst_slot) for p in pulls], [(p.expert, p.dst_slot) for p in pulls]
+    def plan_migration(self, old_sets, new_sets, phys_slots=None) -> list[Round]:
+        """Rounds of the slot diff `new.slots - old.slots` (migration_cost, cost.py:186-187) that keep
+        every GPU within its physical slots (cap + staging) and every expert covered
+        (migration.plan_rounds).  Every rank computes the same plan; phys_slots defaults to this
+        layer's own count on every GPU."""
+        phys = phys_slots if phys_slots is not None else [self.n_phys_slots] * self.world
+        return plan_rounds(old_sets, new_sets, phys)
 
-    def migrate_async(self, old_sets, new_sets, peer_slot_of, stream: torch.cuda.Stream, event: torch.cuda.Event):
-        """Issue this GPU's weight pulls on `stream`; `peer_slot_of[n][e]` = slot of e on GPU n."""
-        ops, adds = self.plan_migration(old_sets, new_sets)
-        arr = (_lib.CopyOp * max(1, len(ops)))()
-        for i, (src, e, dst) in enumerate(ops):
-            arr[i] = _lib.CopyOp(src, int(peer_slot_of[src][e]), dst)
+    def migrate_round_async(self, rnd: Round, peer_slot_of, stream: torch.cuda.Stream, event: torch.cuda.Event):
+        """Issue this GPU's pulls of one round on `stream` (peer_slot_of[n][e] = slot of e on GPU n);
+        returns [(expert, destination slot)]."""
+        mine = [p for p in rnd.pulls if p.dst_rank == self.rank]
+        if len(mine) > len(self._free):
+            raise InfeasibleError(f"GPU {self.rank}: {len(mine)} pulls but {len(self._free)} free slots")
+        arr = (_lib.CopyOp * max(1, len(mine)))()
+        adds = []
+        for i, p in enumerate(mine):
+            dst = self._free[i]
+            arr[i] = _lib.CopyOp(p.src_rank, int(peer_slot_of[p.src_rank][p.expert]), dst)
+            adds.append((p.expert, dst))
         with torch.cuda.stream(stream):
-            _lib.check(self.lib.mp_layer_migrate(self._h, arr, len(ops), c_void_p(stream.cuda_stream), None),
+            _lib.check(self.lib.mp_layer_migrate(self._h, arr, len(mine), c_void_p(stream.cuda_stream), None),
                        "mp_layer_migrate")
             event.record(stream)  # torch-side record: the CUDA event is created lazily by torch
         for _, dst in adds:
             self._free.remove(dst)
         return adds
 
-    def finish_migration(self, new_sets, adds, link_latency=None, link_bandwidth=None) -> None:
-        """After the copies landed everywhere: swap routes, retire evicted slots (migration_complete)."""
+    def finish_round(self, rnd: Round, adds, link_latency=None, link_bandwidth=None) -> None:
+        """After every GPU's copies of the round landed: the added experts become resident, the
+        experts this GPU drops in the round's placement retire, routes swap to that placement
+        (migration_complete, sim.py:520-525, one round at a time)."""
         G, E = self.world, self.shape.E
         slot_of = self.slot_of.copy()
         for e, dst in adds:
             slot_of[e] = dst
-        keep = set(new_sets[self.rank])
+        keep = set(rnd.sets_after[self.rank])
         for e in range(E):
             if slot_of[e] >= 0 and e not in keep:
                 self._free.append(int(slot_of[e]))
                 slot_of[e] = -1
         self._free.sort()
-        if link_latency is None:
-            link_latency = np.full((G, G), 3e-6)
-            np.fill_diagonal(link_latency, 0.0)
-        if link_bandwidth is None:
-            link_bandwidth = np.full((G, G), 770e9)
-        route = route_table([frozenset(s) for s in new_sets], E, link_latency, link_bandwidth, self.shape.d)
+        if link_latency is None or link_bandwidth is None:
+            link_latency, link_bandwidth = uniform_links(G)
+        route = route_table([frozenset(s) for s in rnd.sets_after], E, link_latency, link_bandwidth, self.shape.d)
         self.set_routes(route, slot_of)
+
+    def migrate(self, old_sets, new_sets, *, phys_slots=None, stream: torch.cuda.Stream | None = None,
+                while_copying=None, link_latency=None, link_bandwidth=None, group=None) -> dict:
+        """Execute an adopted plan (SPMD: every rank calls it): per round, NVLink pulls on the side
+        `stream` while `while_copying()` (e.g. forwards on the current placement) keeps traffic
+        flowing, then -- after every GPU's copies landed -- the route swap.  Returns accounting
+        (this GPU's adds, rounds, copy time)."""
+        import torch.distributed as dist
+        rounds = self.plan_migration(old_sets, new_sets, phys_slots)
+        side = stream or torch.cuda.Stream(self.device)
+        main = torch.cuda.current_stream(self.device)
+        copy_ms, n_overlap, all_adds = 0.0, 0, []
+        for rnd in rounds:
+            if self.world > 1:
+                slot_maps = [None] * self.world
+                dist.all_gather_object(slot_maps, self.slot_of.tolist(), group=group)
+            else:
+                slot_maps = [self.slot_of.tolist()]
+            # the slots freed by the previous round may still be read by forwards queued before its swap
+            side.wait_stream(main)
+            t0, done = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(side)
+            adds = self.migrate_round_async(rnd, slot_maps, side, done)
+            if while_copying is not None:
+                n_overlap += while_copying() or 0
+            done.synchronize()
+            copy_ms += t0.elapsed_time(done)
+            if self.world > 1:
+                dist.barrier(group=group)  # every GPU's copies of this round landed
+            self.finish_round(rnd, adds, link_latency, link_bandwidth)
+            if self.world > 1:
+                dist.barrier(group=group)  # every GPU swapped before the next round overwrites slots
+            all_adds += adds
+        return {"rounds": len(rounds), "adds": all_adds, "copy_ms": copy_ms, "forwards_during_copy": n_overlap}
 
 
 class HostPipeline:

@@ -27,7 +27,7 @@ from paper_2508_12851_b200.routing import route_table, uniform_links
 from paper_2508_12851_b200.shapes import LayerShape
 
 
-def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None):
+def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None, expect_rounds=0, staging=1):
     """expect: K3 plan keys (B200MoELayer.exec_plan) the first forward must have run, so the
     production plans -- CTA-pair tiles with the NVLink-scatter GEMM2 epilogue; the split plan
     with the pair-fused shared expert and the small-group side chain -- meet the oracle at G > 1."""
@@ -41,7 +41,7 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None):
     lat, bw = uniform_links(G)
 
     cap = max(len(s) for s in sets + sets2) if caps is None else caps[rank]
-    layer = B200MoELayer(shape, rank=rank, world=G, max_tokens=max(T_list), cap_slots=cap)
+    layer = B200MoELayer(shape, rank=rank, world=G, max_tokens=max(T_list), cap_slots=cap, staging_slots=staging)
     layer.open_peers()
     layer.set_router(torch.from_numpy(wg[:E]), torch.from_numpy(biases[rank]),
                      torch.from_numpy(wg[E]) if shape.shared_gate else None)
@@ -90,22 +90,23 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None):
         shape, xs, wg[:E], biases, route1, experts, shared, wg[E] if shape.shared_gate else None).counts)
     del g
 
-    # ---- migration A -> B: gather every GPU's slot map, pull added experts over NVLink
-    slot_maps = [None] * G
-    dist.all_gather_object(slot_maps, layer.slot_of.tolist())
-    side = torch.cuda.Stream(dev)
-    done = torch.cuda.Event()
-    adds = layer.migrate_async(sets, sets2, slot_maps, side, done)
-    done.synchronize()
-    dist.barrier()  # every GPU's copies have landed
-    layer.finish_migration(sets2, adds)
+    # ---- migration A -> B in cap-respecting rounds (cap + 1 staging slot per GPU, coverage at
+    # every instant): NVLink pulls on a side stream with forwards in flight, route swap per round
+    phys = [(caps[g] if caps is not None else cap) + staging for g in range(G)]
+    fwd_out = torch.empty_like(x)
+    res = layer.migrate(sets, sets2, phys_slots=phys, stream=torch.cuda.Stream(dev),
+                        while_copying=lambda: (layer.forward(x, fwd_out), 1)[1])
     route2 = route_table([frozenset(s) for s in sets2], E, lat, bw, shape.d)
     assert np.array_equal(layer.route, route2)
+    assert int((layer.slot_of >= 0).sum()) == len(sets2[rank]) <= phys[rank] - staging
+    if expect_rounds:
+        assert res["rounds"] >= expect_rounds, res["rounds"]
     # migrated weights are bit-identical to the source copies
-    for e, dst in adds:
-        w1, w3, w2 = layer.read_slot(dst)
+    for e, _ in res["adds"]:
+        w1, w3, w2 = layer.read_slot(int(layer.slot_of[e]))
         assert np.array_equal(w1.float().cpu().numpy(), experts[e][0]), f"migrated W1 of expert {e}"
         assert np.array_equal(w2.float().cpu().numpy(), experts[e][2]), f"migrated W2 of expert {e}"
+    layer.check()
     check(route2, "placement B (after migration)")
     layer.close()
 
@@ -123,6 +124,7 @@ def main():
 
     if only != "prod":
         small_cases(G, rank)
+        tight_cap_case(G, rank)
     production_cases(G, rank)
 
     dist.barrier()
@@ -165,6 +167,22 @@ def production_cases(G, rank):
              expect={"pair_routed": 1, "split_m": 256, "small_grid": 20, "fuse_shared": 1})
 
 
+def tight_cap_case(G, rank):
+    """Heterogeneous, exactly-full caps (Qwen-like 60 experts, caps in the ratio of the Qwen
+    config's [12,10,8,8,8,6,6,6]): every GPU holds cap experts and swaps a block of them, so the
+    migration needs several rounds through the single staging slot."""
+    shape = LayerShape("qwen_tight", d=256, f=256, E=60, k=4, score_mode=1, shared_f=256, shared_gate=1)
+    het = np.array([12, 10, 8, 8, 8, 6, 6, 6][:G], dtype=float)
+    sizes = np.floor(60 * het / het.sum()).astype(int)
+    sizes[0] += 60 - int(sizes.sum())
+    starts = np.concatenate([[0], np.cumsum(sizes)[:-1]])
+    sets = [list(range(int(a), int(a + n))) for a, n in zip(starts, sizes)]
+    shift = max(3, 60 // (3 * G))
+    sets2 = [sorted((e + shift) % 60 for e in s) for s in sets]
+    run_case(shape, G, rank, sets, sets2, [160 + 8 * s for s in range(G)], seed=31, caps=[int(n) for n in sizes],
+             expect_rounds=2)
+
+
 def small_cases(G, rank):
     # case 1: toy-like shape, replicated experts; origins with different T (ragged)
     shape = LayerShape("toy_small", d=512, f=512, E=8, k=2)
@@ -200,7 +218,7 @@ def small_cases(G, rank):
     holders = list(range(G - 1))
     sets = [sorted(e for e in range(8) if e % len(holders) == g) if g < G - 1 else [] for g in range(G)]
     caps = [max(len(x) for x in sets)] * (G - 1) + [0]
-    run_case(shape, G, rank, sets, sets, [100 + 20 * s for s in range(G)], seed=5, caps=caps)
+    run_case(shape, G, rank, sets, sets, [100 + 20 * s for s in range(G)], seed=5, caps=caps, staging=0)
 
     # case 6: randomised shapes and placements (every rank draws the same ones): replicated
     # experts, ragged T including empty origins, migration between two random placements

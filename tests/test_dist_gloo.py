@@ -1,10 +1,13 @@
-"""N > 1 host logic on CPU with world_size-2 gloo process groups.
+"""N > 1 host logic on CPU with gloo process groups of 2 and 8 ranks.
 
 Covers what the ranks agree on before the NVLink kernels run: identical route
 tables from one placement, the handle all-gather of B200MoELayer.open_peers,
 the count all-gather feeding the reference solver, the receive layout each
 rank derives independently (must equal the oracle), and consistent migration
-plans (every pulled expert is held by its source in the old placement).
+plans (every rank derives the same cap-respecting migration rounds; every
+pulled expert is held by its source when its round starts).  The 8-rank case
+covers the G = 8 host side that no 4-GPU box can run (the layer's kernels must
+never share a GPU between ranks).
 """
 
 import os
@@ -32,7 +35,7 @@ def _worker(rank, world, port, q):
     try:
         from oracle import moe_oracle as orc
         from paper_2508_12851_b200 import routing
-        from paper_2508_12851_b200.migration import plan_pulls
+        from paper_2508_12851_b200.migration import plan_rounds
 
         E, k, d, T = 16, 2, 256, 64
         sets = [[e for e in range(E) if e % world == r or e == 0] for r in range(world)]
@@ -63,15 +66,22 @@ def _worker(rank, world, port, q):
         tot = mine_rows.clone()
         dist.all_reduce(tot)
         assert tot.tolist() == [int(M[D].sum()) for D in range(world)]
-        # 4. migration plans are consistent across ranks
+        # 4. migration rounds are identical on every rank and move exactly the slot diff
         new = [[e for e in range(E) if e % world == (r + 1) % world or e == 1] for r in range(world)]
-        pulls = plan_pulls(rank, sets, new, free_slots=list(range(100, 100 + E)))
+        phys = [max(len(a), len(b)) + 1 for a, b in zip(sets, new)]
+        rounds = plan_rounds(sets, new, phys)
+        plan = [[(p.expert, p.src_rank, p.dst_rank) for p in r.pulls] for r in rounds]
         allp = [None] * world
-        dist.all_gather_object(allp, [(p.expert, p.src_rank) for p in pulls])
-        for r, pl in enumerate(allp):
-            assert {e for e, _ in pl} == set(new[r]) - set(sets[r])
-            for e, src in pl:
-                assert e in sets[src]
+        dist.all_gather_object(allp, plan)
+        assert all(p == allp[0] for p in allp)
+        cur = [set(x) for x in sets]
+        for r in rounds:
+            for p in r.pulls:
+                assert p.expert in cur[p.src_rank]
+            cur = [set(x) for x in r.sets_after]
+        assert [sorted(c) for c in cur] == [sorted(x) for x in new]
+        mine = {p.expert for r in rounds for p in r.pulls if p.dst_rank == rank}
+        assert mine == set(new[rank]) - set(sets[rank])
         q.put((rank, "ok"))
     except Exception as ex:  # pragma: no cover - reported to the parent
         q.put((rank, repr(ex)))
@@ -79,8 +89,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_host_logic_gloo():
-    world = 2
+@pytest.mark.parametrize("world", [2, 8])
+def test_multi_rank_host_logic_gloo(world):
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     port = _port()

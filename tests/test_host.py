@@ -9,7 +9,7 @@ import pytest
 
 from paper_2508_12851_b200 import routing
 from paper_2508_12851_b200.errors import import_moeplace
-from paper_2508_12851_b200.migration import plan_pulls, slot_diff
+from paper_2508_12851_b200.migration import added_cells, plan_rounds
 from paper_2508_12851_b200.shapes import DEEPSEEK, MIXTRAL, QWEN, SHAPES, TOY, get_shape, slot_caps
 
 REPO = Path(__file__).resolve().parent.parent
@@ -73,20 +73,67 @@ def test_dispatch_accounting_reference_formula():
     assert acc["local_ratio"] == pytest.approx((8 + 2) / 14)
 
 
-def test_plan_pulls_uses_lowest_old_holder_and_free_slots():
+def test_plan_rounds_uses_lowest_current_holder():
     old = [[0, 1, 2], [2, 3], [0, 3]]
     new = [[0, 1, 3], [1, 2, 3], [0, 2]]
-    p0 = plan_pulls(0, old, new, free_slots=[7, 5])
-    assert [(p.expert, p.src_rank, p.dst_slot) for p in p0] == [(3, 1, 5)]
-    p1 = plan_pulls(1, old, new, free_slots=[4])
-    assert [(p.expert, p.src_rank, p.dst_slot) for p in p1] == [(1, 0, 4)]
-    p2 = plan_pulls(2, old, new, free_slots=[9])
-    assert [(p.expert, p.src_rank) for p in p2] == [(2, 0)]
-    added, removed = slot_diff(old, new)
-    assert len(added) == 3 and len(removed) == 2
+    rounds = plan_rounds(old, new, [4, 4, 4])
+    assert len(rounds) == 1
+    assert sorted((p.expert, p.src_rank, p.dst_rank) for p in rounds[0].pulls) == [(1, 0, 1), (2, 0, 2), (3, 1, 0)]
+    assert [list(s) for s in rounds[0].sets_after] == new
+    assert added_cells(rounds) == [(0, 0, 0, 3), (1, 0, 0, 1), (2, 0, 0, 2)]
+
+
+def _check_rounds(old, new, phys):
+    rounds = plan_rounds(old, new, phys)
+    cur = [set(s) for s in old]
+    E = set().union(*map(set, old))
+    for r in rounds:
+        for p in r.pulls:                       # sources hold the expert when the round starts
+            assert p.expert in cur[p.src_rank] and p.expert not in cur[p.dst_rank]
+        during = [cur[g] | {p.expert for p in r.pulls if p.dst_rank == g} for g in range(len(old))]
+        assert all(len(during[g]) <= phys[g] for g in range(len(old)))   # old copies retire after
+        after = [set(s) for s in r.sets_after]
+        assert set().union(*after) == E                                  # coverage at every swap
+        assert all(after[g] <= during[g] for g in range(len(old)))
+        cur = after
+    assert [sorted(c) for c in cur] == [sorted(s) for s in new]
+    return rounds
+
+
+def test_plan_rounds_full_gpus_swap_through_one_staging_slot():
+    # every GPU exactly full (cap = 3): swapping whole blocks takes one round per expert
+    old = [[0, 1, 2], [3, 4, 5]]
+    new = [[3, 4, 5], [0, 1, 2]]
+    rounds = _check_rounds(old, new, [4, 4])
+    assert len(rounds) == 3
+    assert all(len(r.pulls) == 2 for r in rounds)
+
+
+def test_plan_rounds_random_heterogeneous_caps():
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        G = int(rng.integers(2, 9))
+        E = int(rng.choice([8, 16, 60, 64]))
+        caps = [-(-E // G) + int(rng.integers(0, 3)) for _ in range(G)]
+
+        def place():
+            sets = [set() for _ in range(G)]
+            for e in rng.permutation(E):
+                g = int(rng.choice([g for g in range(G) if len(sets[g]) < caps[g]]))
+                sets[g].add(int(e))
+            for g in range(G):
+                while len(sets[g]) < caps[g] and rng.random() < 0.6:
+                    sets[g].add(int(rng.integers(E)))
+            return [sorted(s) for s in sets]
+        _check_rounds(place(), place(), [c + 1 for c in caps])
+
+
+def test_plan_rounds_rejects_over_cap_and_unheld():
     from paper_2508_12851_b200 import InfeasibleError
     with pytest.raises(InfeasibleError):
-        plan_pulls(1, old, new, free_slots=[])
+        plan_rounds([[0, 1]], [[0, 1, 2]], [2])
+    with pytest.raises(InfeasibleError):
+        plan_rounds([[0], [1]], [[0, 2], [1]], [3, 3])
 
 
 def test_bench_placement_documents_are_valid():
