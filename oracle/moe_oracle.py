@@ -292,12 +292,16 @@ def silu(x):
     return x / (1.0 + np.exp(-x))
 
 
-def swiglu_ffn(xrows: np.ndarray, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray) -> np.ndarray:
-    """bf16( bf16(silu(x W1^T) * (x W3^T)) W2^T ), fp32 accumulation."""
+def swiglu_ffn(xrows: np.ndarray, w1: np.ndarray, w3: np.ndarray, w2: np.ndarray, with_terms: bool = False):
+    """bf16( bf16(silu(x W1^T) * (x W3^T)) W2^T ), fp32 accumulation.  with_terms: also return
+    |h| |W2|^T, the magnitude of GEMM2's terms (what a one-ulp change of every h can move y by)."""
     g = xrows @ w1.T
     u = xrows @ w3.T
     h = bf16_round((silu(g) * u).astype(np.float32))
-    return bf16_round((h @ w2.T).astype(np.float32))
+    y = bf16_round((h @ w2.T).astype(np.float32))
+    if with_terms:
+        return y, (np.abs(h) @ np.abs(w2).T).astype(np.float32)
+    return y
 
 
 # ----------------------------------------------------------------------------- full layer
@@ -315,8 +319,9 @@ class OracleResult:
     pos_row: list = field(default_factory=list)
     recv_M: np.ndarray | None = None
     shared_gate: list = field(default_factory=list)
-    mag: list = field(default_factory=list)  # per origin [T, d]: sum_j |w_j y_j| (+ |g ysh|), the
-                                             # magnitude the per-element tolerance is relative to
+    mag: list = field(default_factory=list)   # per origin [T, d]: sum_j |w_j y_j| (+ |g ysh|)
+    mag2: list = field(default_factory=list)  # per origin [T, d]: sum_j |w_j| (|h_j| |W2|^T) (+ shared):
+                                              # GEMM2 term magnitude (tests/tolerance.py's bound)
 
 
 def moe_layer_forward(shape: LayerShape, xs, wg, biases, route, experts, shared=None, wsg=None) -> OracleResult:
@@ -350,26 +355,31 @@ def moe_layer_forward(shape: LayerShape, xs, wg, biases, route, experts, shared=
         pos_dst.append(dst)
         pos_row.append(rows)
     # expert outputs per (origin, token, slot)
-    outs, mags = [], []
+    outs, mags, mags2 = [], [], []
     for s in range(G):
         T = xs[s].shape[0]
         y = np.zeros((T, k, shape.d), dtype=np.float32)
+        yt = np.zeros((T, k, shape.d), dtype=np.float32)
         for e in np.unique(idxs[s]):
             sel = np.nonzero(idxs[s] == e)
-            y[sel] = swiglu_ffn(xs[s][sel[0]], *experts[int(e)])
+            y[sel], yt[sel] = swiglu_ffn(xs[s][sel[0]], *experts[int(e)], with_terms=True)
         acc = np.zeros((T, shape.d), dtype=np.float32)
         mag = np.zeros((T, shape.d), dtype=np.float32)
+        mag2 = np.zeros((T, shape.d), dtype=np.float32)
         for j in range(k):
             acc = acc + ws[s][:, j:j + 1] * y[:, j, :]
             mag = mag + np.abs(ws[s][:, j:j + 1] * y[:, j, :])
+            mag2 = mag2 + np.abs(ws[s][:, j:j + 1]) * yt[:, j, :]
         if shared is not None:
-            ysh = swiglu_ffn(xs[s], *shared)
+            ysh, ysht = swiglu_ffn(xs[s], *shared, with_terms=True)
             g = gates[s][:, None] if wsg is not None else np.float32(1.0)
             acc = acc + g * ysh
             mag = mag + np.abs(g * ysh)
+            mag2 = mag2 + np.abs(g) * ysht
         outs.append(bf16_round(acc.astype(np.float32)))
         mags.append(mag)
-    return OracleResult(outs, idxs, ws, hists, counts, route, pos_dst, pos_row, M, gates, mags)
+        mags2.append(mag2)
+    return OracleResult(outs, idxs, ws, hists, counts, route, pos_dst, pos_row, M, gates, mags, mags2)
 
 
 # ----------------------------------------------------------------------------- accounting

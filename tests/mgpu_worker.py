@@ -65,7 +65,7 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None, 
         assert np.array_equal(layer.pos_row[:T].cpu().numpy(), ref.pos_row[rank]), f"{tag}: pos_row"
         acc = layer.dispatch_accounting()
         assert acc["remote_bytes"] == orc.reference_remote_bytes(ref.counts, route, shape.d), f"{tag}: bytes"
-        check_layer_close(out.float().cpu().numpy(), ref.out[rank], ref.mag[rank], tag)
+        check_layer_close(out.float().cpu().numpy(), ref.out[rank], ref.mag[rank], ref.mag2[rank], tag)
         return out
 
     route1 = route_table([frozenset(s) for s in sets], E, lat, bw, shape.d)

@@ -71,8 +71,9 @@ def _run(shape, T, seed=0):
     rows_d = torch.from_numpy(rows.ravel()).long().to(dev)
     assert torch.equal(layer.recv[rows_d], x.repeat_interleave(k, dim=0))
     # every output element against the GPU fp32 restatement
-    ref, mag = layer_reference(x, idx_ref, w_ref, src, shared, gate)
-    stats = check_layer_close(out.float().cpu().numpy(), ref.cpu().numpy(), mag.cpu().numpy(), shape.name)
+    ref, mag, mag2 = layer_reference(x, idx_ref, w_ref, src, shared, gate)
+    stats = check_layer_close(out.float().cpu().numpy(), ref.cpu().numpy(), mag.cpu().numpy(), mag2.cpu().numpy(),
+                              shape.name)
     print(f"{shape.name} T={T} plan={layer.exec_plan()} {stats}")
     layer.close()
 

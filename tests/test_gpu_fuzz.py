@@ -70,5 +70,5 @@ def test_random_layer_matches_oracle(seed):
     rows = ref.pos_row[0].ravel()
     recv = layer.recv[: rows.max() + 1].float().cpu().numpy()
     np.testing.assert_array_equal(recv[rows], np.repeat(x, shape.k, axis=0))
-    check_layer_close(out.float().cpu().numpy(), ref.out[0], ref.mag[0], tag)
+    check_layer_close(out.float().cpu().numpy(), ref.out[0], ref.mag[0], ref.mag2[0], tag)
     layer.close()

@@ -14,18 +14,21 @@ from __future__ import annotations
 import torch
 
 
-def _ffn(x: torch.Tensor, w1: torch.Tensor, w3: torch.Tensor, w2: torch.Tensor) -> torch.Tensor:
+def _ffn(x: torch.Tensor, w1: torch.Tensor, w3: torch.Tensor, w2: torch.Tensor):
+    """(y, |h| |W2|^T): the output and the magnitude of GEMM2's terms."""
     g = x @ w1.float().T
     u = x @ w3.float().T
     h = (torch.nn.functional.silu(g) * u).bfloat16().float()
-    return (h @ w2.float().T).bfloat16().float()
+    w2f = w2.float()
+    return (h @ w2f.T).bfloat16().float(), h.abs() @ w2f.abs().T
 
 
 def layer_reference(x: torch.Tensor, idx, w, expert_src, shared=None, gate=None):
     """x [T, d] bf16 (device); idx [T, k] int, w [T, k] fp32 (numpy or torch); expert_src(e) ->
     (W1 [f, d], W3 [f, d], W2 [d, f]) bf16 device tensors; shared (W1, W3, W2) or None; gate [T]
-    (sigmoid shared gate) or None.  Returns (out [T, d] fp32 bf16-exact, mag [T, d]) with
-    mag = sum_j |w_j y_j| (+ |g y_sh|), the magnitude tests/tolerance.py is relative to."""
+    (sigmoid shared gate) or None.  Returns (out [T, d] fp32 bf16-exact, mag, mag2) with
+    mag = sum_j |w_j y_j| (+ |g y_sh|) and mag2 = sum_j |w_j| (|h_j| |W2|^T) (+ shared), the
+    magnitudes tests/tolerance.py's bound is relative to."""
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = False
     try:
@@ -35,20 +38,24 @@ def layer_reference(x: torch.Tensor, idx, w, expert_src, shared=None, gate=None)
         T, k = idx.shape
         xf = x.float()
         y = torch.zeros(T, k, x.shape[1], device=dev)
+        yt = torch.zeros_like(y)
         for e in torch.unique(idx).tolist():
             t, j = torch.nonzero(idx == e, as_tuple=True)
-            y[t, j] = _ffn(xf[t], *expert_src(e))
+            y[t, j], yt[t, j] = _ffn(xf[t], *expert_src(e))
         acc = torch.zeros(T, x.shape[1], device=dev)
         mag = torch.zeros_like(acc)
+        mag2 = torch.zeros_like(acc)
         for j in range(k):
             term = w[:, j:j + 1] * y[:, j]
             acc = acc + term
             mag = mag + term.abs()
+            mag2 = mag2 + w[:, j:j + 1].abs() * yt[:, j]
         if shared is not None:
-            ysh = _ffn(xf, *shared)
+            ysh, ysht = _ffn(xf, *shared)
             g = torch.as_tensor(gate, device=dev).float()[:, None] if gate is not None else 1.0
             acc = acc + g * ysh
             mag = mag + (g * ysh).abs()
-        return acc.bfloat16().float(), mag
+            mag2 = mag2 + (g.abs() if gate is not None else 1.0) * ysht
+        return acc.bfloat16().float(), mag, mag2
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
