@@ -144,6 +144,7 @@ typedef struct mp_layer_ptrs {
   uint32_t* hist;    /* [E] cumulative activation histogram (this origin)        */
   int32_t* counts;   /* [2][G][E] exchanged batch counts C[src][e] (parity halves) */
   float* shared_gate;/* [max_tokens] or NULL                                     */
+  int32_t* batch_counts; /* [E] this origin's counts of the last routed batch      */
   int64_t recv_cap;  /* rows                                                     */
   int64_t slot_bytes;/* bytes of one expert slot (w13 + w2) = ModelSpec.expert_size */
 } mp_layer_ptrs;
@@ -188,6 +189,29 @@ int mp_layer_forward(mp_layer* layer, const void* x, void* out, int T, void* str
  *   11 side chain start | 12 side chain end                                   */
 #define MP_NUM_STAGE_EVENTS 13
 int mp_layer_forward_timed(mp_layer* layer, const void* x, void* out, int T, void* stream, void* const* events);
+
+/* ---- The same forward as separate stages, for a host-driven transport (the
+ * NCCL all-to-all-v arm: paper_2508_12851_b200/nccl_path.py) and for standalone
+ * K1 / K2 / K3 / K5 parity tests.  Between the stages the caller moves rows:
+ *   mp_layer_route     K1 only: idx, w, gate, histogram and this origin's batch
+ *                      counts (ptrs.batch_counts); no peer exchange.
+ *   mp_layer_permute   K2 against a caller-assembled count table counts_all
+ *                      [G][E] (device): rows for this GPU go into recv, rows
+ *                      for GPU D != rank into `staging` + (D * recv_cap + r) * d,
+ *                      r = the row in D's receive layout (pos_row) -- so every
+ *                      (source, expert) chunk has the same offsets in the
+ *                      sender's image and in D's receive buffer.
+ *   mp_layer_experts   K3 over recv (groups from counts_all and the routes);
+ *                      the expert outputs overwrite their received rows.
+ *   mp_layer_combine_gather
+ *                      K5 reading pair (t, j)'s output from recv (own GPU) or
+ *                      `ret_stage` + (D * recv_cap + pos_row) * d (GPU D's
+ *                      rows, returned into the same image layout).
+ * staging / ret_stage: G * recv_cap * d bf16 (device), unused when G == 1. */
+int mp_layer_route(mp_layer* layer, const void* x, int T, void* stream);
+int mp_layer_permute(mp_layer* layer, const void* x, int T, const int32_t* counts_all, void* staging, void* stream);
+int mp_layer_experts(mp_layer* layer, const void* x, int T, const int32_t* counts_all, void* stream);
+int mp_layer_combine_gather(mp_layer* layer, const void* ret_stage, int T, void* out, void* stream);
 
 /* Number of kernels the last mp_layer_forward launched. */
 int mp_layer_last_launches(mp_layer* layer);

@@ -43,7 +43,7 @@ EXPORTED_SYMBOLS = (
     "mp_router_topk_hist_f32w", "mp_router_topk_logits", "mp_grouped_gemm",
     "mp_layer_create", "mp_layer_destroy", "mp_layer_get_ptrs", "mp_layer_export_handles",
     "mp_layer_open_peers", "mp_layer_set_routes", "mp_layer_prepare_router", "mp_layer_forward",
-    "mp_layer_forward_timed",
+    "mp_layer_forward_timed", "mp_layer_route", "mp_layer_permute", "mp_layer_experts", "mp_layer_combine_gather",
     "mp_layer_last_launches", "mp_layer_config", "mp_layer_read_counts", "mp_layer_check", "mp_layer_migrate",
 )
 
@@ -64,7 +64,7 @@ class LayerPtrs(Structure):
         ("pos_dst", c_void_p), ("pos_row", c_void_p), ("recv", c_void_p), ("h", c_void_p), ("ret", c_void_p),
         ("recv_src", c_void_p),
         ("hist", c_void_p), ("counts", c_void_p),
-        ("shared_gate", c_void_p), ("recv_cap", c_int64), ("slot_bytes", c_int64),
+        ("shared_gate", c_void_p), ("batch_counts", c_void_p), ("recv_cap", c_int64), ("slot_bytes", c_int64),
     ]
 
 
@@ -108,6 +108,10 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         "mp_layer_prepare_router": ([V, V], I),
         "mp_layer_forward": ([V, V, V, I, V], I),
         "mp_layer_forward_timed": ([V, V, V, I, V, POINTER(c_void_p)], I),
+        "mp_layer_route": ([V, V, I, V], I),
+        "mp_layer_permute": ([V, V, I, V, V, V], I),
+        "mp_layer_experts": ([V, V, I, V, V], I),
+        "mp_layer_combine_gather": ([V, V, I, V, V], I),
         "mp_layer_last_launches": ([V], I),
         "mp_layer_config": ([V, I], I),
         "mp_layer_read_counts": ([V, V, V], I),

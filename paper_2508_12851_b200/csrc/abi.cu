@@ -120,6 +120,11 @@ struct mp_layer {
   uint32_t* err_host_d = nullptr;
   uint32_t *perm_ticket = nullptr, *ret_ticket = nullptr;  // arrival counters of the raising kernels
   void** ptr_arrays = nullptr;  // device: recv[8], ret[8], flags[8], counts0[8], counts1[8], recv_src[8]
+  // stage entries (host-driven transport): device [recv images 8 | recv_src images 8 | combine bases 8]
+  void** stage_ptrs = nullptr;
+  void* stage_host[24] = {};
+  bool stage_uploaded = false;
+  int32_t* src_image = nullptr;  // [G][recv_cap] recv_src images of the peers' layouts (never read)
 
   uint8_t* peer_window[8] = {};
   uint8_t* peer_pool[8] = {};
@@ -344,6 +349,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       L->ret_ticket = cv.take<uint32_t>(4);
       L->sync_state = cv.take<uint32_t>(4);
       L->ptr_arrays = cv.take<void*>(6 * 8);
+      L->stage_ptrs = cv.take<void*>(3 * 8);
       if (D.shared_f > 0) {
         L->w13s = cv.take<__nv_bfloat16>(size_t(2) * D.shared_f * D.d);
         L->w2s = cv.take<__nv_bfloat16>(size_t(D.d) * D.shared_f);
@@ -459,6 +465,7 @@ int mp_layer_destroy(mp_layer* L) {
   if (L->side) cudaStreamDestroy(L->side);
   if (L->scratch) cudaFree(L->scratch);
   if (L->err_host) cudaFreeHost(const_cast<uint32_t*>(L->err_host));
+  if (L->src_image) cudaFree(L->src_image);
   if (L->window) cudaFree(L->window);
   if (L->pool) cudaFree(L->pool);
   delete L;
@@ -484,6 +491,7 @@ int mp_layer_get_ptrs(mp_layer* L, mp_layer_ptrs* o) {
   o->hist = L->hist;
   o->counts = L->counts;
   o->shared_gate = L->sgate;
+  o->batch_counts = L->batch_counts;
   o->recv_cap = L->recv_cap;
   o->slot_bytes = int64_t(L->slot_bytes);
   return MP_OK;
@@ -578,89 +586,62 @@ int mp_layer_prepare_router(mp_layer* L, void* stream) {
   return MP_OK;
 }
 
-static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream, void* const* events) {
-  if (!L) return set_error(MP_E_ARG, "mp_layer_forward: null layer");
-  if ((!x || !out) && T > 0) return set_error(MP_E_ARG, "mp_layer_forward: null x/out with T=%d", T);
+namespace {
+
+// Stage-boundary events of mp_layer_forward_timed (NULL entries skipped).
+struct Marker {
+  void* const* events;
+  cudaStream_t st;
+  int i = 0;
+  int mark() {
+    if (events && events[i]) {
+      cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(events[i]), st);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaEventRecord(stage)");
+    }
+    ++i;
+    return MP_OK;
+  }
+  int mark_on(int idx, cudaStream_t s) {
+    if (events && events[idx]) {
+      cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(events[idx]), s);
+      if (e != cudaSuccess) return set_cuda_error(e, "cudaEventRecord(stage)");
+    }
+    return MP_OK;
+  }
+};
+
+int check_forward_args(mp_layer* L, const void* x, const void* out, int T, const char* who) {
+  if (!L) return set_error(MP_E_ARG, "%s: null layer", who);
+  if ((!x || !out) && T > 0) return set_error(MP_E_ARG, "%s: null x/out with T=%d", who, T);
   const mp_layer_desc& D = L->desc;
   if (T < 0 || T > D.max_tokens) return set_error(MP_E_SHAPE, "T=%d exceeds max_tokens=%d", T, D.max_tokens);
-  if (!L->routes_set) return set_error(MP_E_UNPLACED, "mp_layer_forward: route table not set");
-  if (!L->router_ready) return set_error(MP_E_ARG, "mp_layer_forward: router weights not prepared");
-  if (!L->peers_open) return set_error(MP_E_PEER, "mp_layer_forward: peers not opened (G=%d)", L->G);
+  if (!L->routes_set) return set_error(MP_E_UNPLACED, "%s: route table not set", who);
+  if (!L->router_ready) return set_error(MP_E_ARG, "%s: router weights not prepared", who);
   // a peer wait of an earlier forward timed out: its outputs were garbage and the
   // protocol is out of step -- refuse to run (read from mapped host memory, no sync)
   if (const uint32_t bad = *L->err_host)
     return set_error(MP_E_PEER, "an earlier forward timed out waiting for NVLink peers (ranks mask 0x%x)", bad);
-  DeviceGuard dg(D.device);
-  MP_CUDA(dg.status);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int G = L->G, E = D.E, k = D.top_k, rank = L->rank;
-  auto** recv_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 0 * 8);
-  auto** ret_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 1 * 8);
-  auto** src_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + 5 * 8);
-  auto** flag_ptrs = reinterpret_cast<uint32_t**>(L->ptr_arrays + 2 * 8);
-  auto** count_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + 3 * 8);  // [parity][peer]
-  int launches = 0;
-  int ev_i = 0;
-  auto mark = [&]() -> int {
-    if (events && events[ev_i]) {
-      cudaError_t e = cudaEventRecord(static_cast<cudaEvent_t>(events[ev_i]), st);
-      if (e != cudaSuccess) return set_cuda_error(e, "cudaEventRecord(stage)");
-    }
-    ++ev_i;
-    return MP_OK;
-  };
+  return MP_OK;
+}
 
-  if (D.shared_f > 0 && T > 0 && (L->tm_x_ptr != x || L->tm_x_rows != T)) {
-    MP_TRY(encode_tmap_bf16_2d(&L->tm_x, x, uint64_t(std::max(T, 1)), uint64_t(D.d), 128));
+// The shared expert's dense tensor map over this forward's x.
+int bind_x(mp_layer* L, const void* x, int T) {
+  if (L->desc.shared_f > 0 && T > 0 && (L->tm_x_ptr != x || L->tm_x_rows != T)) {
+    MP_TRY(encode_tmap_bf16_2d(&L->tm_x, x, uint64_t(std::max(T, 1)), uint64_t(L->desc.d), 128));
     L->tm_x_ptr = x;
     L->tm_x_rows = T;
   }
+  return MP_OK;
+}
 
-  // NVLink flag protocol (G > 1), folded into the kernels: router tail raises A
-  // (counts published), permute waits A and its tail raises B (rows sent), GEMM1
-  // producers wait B, the GEMM2 tails raise C (rows returned), combine waits C
-  PeerSync ps0;
-  if (G > 1) {
-    ps0.flag_ptrs = flag_ptrs;
-    ps0.count_ptrs = count_ptrs;
-    ps0.state = L->sync_state;
-    ps0.err = L->err;
-    ps0.err_host = L->err_host_d;
-    ps0.G = G;
-    ps0.rank = rank;
-  }
-  PeerSync ps_wait = ps0, ps_perm = ps0, ps_ret = ps0;
-  ps_wait.wait = 1;
-  ps_perm.wait = 1;
-  ps_perm.ticket = L->perm_ticket;
-  ps_perm.total = 1;  // launch_permute sets its grid
-  ps_ret.ticket = L->ret_ticket;
-
-  MP_TRY(mark());  // 0
-  if (T > 0) {
-    MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
-                         D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
-                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr, L->wg32));
-    ++launches;
-  } else if (G > 1) {
-    // no router / permute on this origin: publish zero counts, raise A and B
-    MP_TRY(launch_peer_sync(ps0, L->batch_counts, E, 2, st));
-    ++launches;
-  } else {
-    MP_CUDA(cudaMemsetAsync(L->batch_counts, 0, size_t(E) * 4, st));
-  }
-  MP_TRY(mark());  // 1 router (+ per-batch counts, count exchange)
-  const int32_t* counts_all = G > 1 ? L->counts : L->batch_counts;
-  const uint32_t* parity = G > 1 ? L->sync_state + 2 : nullptr;
-  MP_TRY(mark());  // 2 (count exchange: folded into the router tail / permute prologue)
-  MP_TRY(mark());  // 3 (layout: folded into permute / GEMM prologues)
-  if (T > 0) {
-    MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, parity,
-                          L->blk_prefix, src_ptrs, rank, G, T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st,
-                          G > 1 ? &ps_perm : nullptr));
-    ++launches;
-  }
-  MP_TRY(mark());  // 4 permute + dispatch
+// K3: the local experts' grouped SwiGLU GEMMs over the receive buffer, groups derived from
+// the count table (counts_all [+ parity half]) and the route table; the shared expert rides in
+// the routed launches when the plan fuses it.  GEMM2 writes each row to ret_ptrs[origin][pair]
+// (scatter, the fused NVLink return) or, ret_ptrs == nullptr, in place of its received row.
+int stage_experts(mp_layer* L, int T, const int32_t* counts_all, const uint32_t* parity, cudaStream_t st,
+                  Marker& mk, const PeerSync* sw, PeerSync* ps_ret, __nv_bfloat16* const* ret_ptrs, int& launches) {
+  const mp_layer_desc& D = L->desc;
+  const int G = L->G, E = D.E, k = D.top_k;
   // Per-forward K3 plan.  With few rows per expert (small batches) every group is
   // weight-bound: stream all of them over every SM on the 1-CTA kernel instead of
   // confining them to the small-group side chain (the shared expert rides along as
@@ -683,8 +664,8 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
                                st, ps));
     launches += 2;
   }
-  MP_TRY(mark());  // 5 shared expert
-  MP_TRY(mark());  // 6 (dispatch barrier: folded into the permute tail / GEMM1 producers)
+  MP_TRY(mk.mark());  // 5 shared expert
+  MP_TRY(mk.mark());  // 6 (dispatch barrier: folded into the permute tail / GEMM1 producers)
   if (D.n_slots > 0) {
     GroupSpec gs;
     gs.mode = 1;
@@ -694,7 +675,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     gs.slot_of = L->slot_of_d;
     gs.G = G;
     gs.E = E;
-    gs.rank = rank;
+    gs.rank = L->rank;
     const int pr = stream_plan ? 0 : L->pair_routed;
     // side-chain SMs: with many rows per expert (G*T*k/E >= 1024, e.g. 4+ GPUs) few groups
     // stay below split_m, so the chain gets 8 SMs instead of 20 (measured: +3-5% at G = 4)
@@ -702,9 +683,9 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     L->last_small_grid = small_grid;
     const int big_grid = split ? kNumSMs - small_grid : 0;
     // C is raised by the last GEMM2 CTA of both chains
-    ps_ret.total = grouped_gemm_ctas(big_grid, pr) + (split ? grouped_gemm_ctas(small_grid, 0) : 0);
-    const PeerSync* sw = G > 1 ? &ps_wait : nullptr;
-    const PeerSync* sr = G > 1 ? &ps_ret : nullptr;
+    if (ps_ret) ps_ret->total = grouped_gemm_ctas(big_grid, pr) + (split ? grouped_gemm_ctas(small_grid, 0) : 0);
+    const int32_t* scatter_src = ret_ptrs ? L->recv_src : nullptr;
+    __nv_bfloat16* out2 = ret_ptrs ? L->ret : L->recv;
     if (split) {
       // fork: small groups (weight-bound) on the side stream over small_grid SMs, large
       // groups (compute-bound) on the main stream over the rest, then join
@@ -713,13 +694,13 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
       gs.m_lo = L->split_m;
       MP_CUDA(cudaEventRecord(L->ev_fork, st));
       MP_CUDA(cudaStreamWaitEvent(L->side, L->ev_fork, 0));
-      if (events && events[11]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[11]), L->side));
+      MP_TRY(mk.mark_on(11, L->side));
       // (no PDL on the split chains: early-scheduled CTAs would contend for the other chain's SMs)
       MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, gsmall, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
                                  small_grid, L->side, 0, nullptr, nullptr, false, nullptr, sw));
-      MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, gsmall, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                                 small_grid, L->side, 0, L->recv_src, ret_ptrs, false, nullptr, sr));
-      if (events && events[12]) MP_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(events[12]), L->side));
+      MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, gsmall, D.d, D.f, 3 * D.d, 2 * D.d, out2, D.d, 0,
+                                 small_grid, L->side, 0, scatter_src, ret_ptrs, false, nullptr, ps_ret));
+      MP_TRY(mk.mark_on(12, L->side));
       MP_CUDA(cudaEventRecord(L->ev_join, L->side));
       launches += 2;
     }
@@ -744,28 +725,97 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     }
     MP_TRY(launch_grouped_gemm(L->tm_recv, pr ? L->tm_w13_p : L->tm_w13, gs, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
                                big_grid, st, pr, nullptr, nullptr, pdl, fused ? &aux1 : nullptr, sw));
-    MP_TRY(mark());  // 7 GEMM1 (SwiGLU)
+    MP_TRY(mk.mark());  // 7 GEMM1 (SwiGLU)
     // GEMM2 epilogue returns every output row to its origin GPU (NVLink stores)
-    MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, L->ret, D.d, 0,
-                               big_grid, st, pr, L->recv_src, ret_ptrs, pdl, fused ? &aux2 : nullptr, sr));
+    MP_TRY(launch_grouped_gemm(L->tm_h, pr ? L->tm_w2_p : L->tm_w2, gs, D.d, D.f, 3 * D.d, 2 * D.d, out2, D.d, 0,
+                               big_grid, st, pr, scatter_src, ret_ptrs, pdl, fused ? &aux2 : nullptr, ps_ret));
     if (split) MP_CUDA(cudaStreamWaitEvent(st, L->ev_join, 0));
     launches += 2;
   } else {
-    MP_TRY(mark());
-    if (G > 1) {  // no GEMM2 here to raise C
-      MP_TRY(launch_peer_sync(ps0, nullptr, E, 1, st));
+    MP_TRY(mk.mark());
+    if (ps_ret && G > 1) {  // no GEMM2 here to raise C
+      MP_TRY(launch_peer_sync(*ps_ret, nullptr, E, 1, st));
       ++launches;
     }
   }
-  MP_TRY(mark());  // 8 GEMM2
-  MP_TRY(mark());  // 9 (return barrier: folded into the GEMM2 tails / combine prologue)
+  MP_TRY(mk.mark());  // 8 GEMM2
+  return MP_OK;
+}
+
+}  // namespace
+
+static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream, void* const* events) {
+  MP_TRY(check_forward_args(L, x, out, T, "mp_layer_forward"));
+  if (!L->peers_open) return set_error(MP_E_PEER, "mp_layer_forward: peers not opened (G=%d)", L->G);
+  const mp_layer_desc& D = L->desc;
+  DeviceGuard dg(D.device);
+  MP_CUDA(dg.status);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int G = L->G, E = D.E, k = D.top_k, rank = L->rank;
+  auto** recv_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 0 * 8);
+  auto** ret_ptrs = reinterpret_cast<__nv_bfloat16**>(L->ptr_arrays + 1 * 8);
+  auto** src_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + 5 * 8);
+  auto** flag_ptrs = reinterpret_cast<uint32_t**>(L->ptr_arrays + 2 * 8);
+  auto** count_ptrs = reinterpret_cast<int32_t**>(L->ptr_arrays + 3 * 8);  // [parity][peer]
+  int launches = 0;
+  Marker mk{events, st};
+  MP_TRY(bind_x(L, x, T));
+
+  // NVLink flag protocol (G > 1), folded into the kernels: router tail raises A
+  // (counts published), permute waits A and its tail raises B (rows sent), GEMM1
+  // producers wait B, the GEMM2 tails raise C (rows returned), combine waits C
+  PeerSync ps0;
+  if (G > 1) {
+    ps0.flag_ptrs = flag_ptrs;
+    ps0.count_ptrs = count_ptrs;
+    ps0.state = L->sync_state;
+    ps0.err = L->err;
+    ps0.err_host = L->err_host_d;
+    ps0.G = G;
+    ps0.rank = rank;
+  }
+  PeerSync ps_wait = ps0, ps_perm = ps0, ps_ret = ps0;
+  ps_wait.wait = 1;
+  ps_perm.wait = 1;
+  ps_perm.ticket = L->perm_ticket;
+  ps_perm.total = 1;  // launch_permute sets its grid
+  ps_ret.ticket = L->ret_ticket;
+
+  MP_TRY(mk.mark());  // 0
+  if (T > 0) {
+    MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
+                         D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
+                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr, L->wg32));
+    ++launches;
+  } else if (G > 1) {
+    // no router / permute on this origin: publish zero counts, raise A and B
+    MP_TRY(launch_peer_sync(ps0, L->batch_counts, E, 2, st));
+    ++launches;
+  } else {
+    MP_CUDA(cudaMemsetAsync(L->batch_counts, 0, size_t(E) * 4, st));
+  }
+  MP_TRY(mk.mark());  // 1 router (+ per-batch counts, count exchange)
+  const int32_t* counts_all = G > 1 ? L->counts : L->batch_counts;
+  const uint32_t* parity = G > 1 ? L->sync_state + 2 : nullptr;
+  MP_TRY(mk.mark());  // 2 (count exchange: folded into the router tail / permute prologue)
+  MP_TRY(mk.mark());  // 3 (layout: folded into permute / GEMM prologues)
+  if (T > 0) {
+    MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, parity,
+                          L->blk_prefix, src_ptrs, rank, G, T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st,
+                          G > 1 ? &ps_perm : nullptr));
+    ++launches;
+  }
+  MP_TRY(mk.mark());  // 4 permute + dispatch
+  MP_TRY(stage_experts(L, T, counts_all, parity, st, mk, G > 1 ? &ps_wait : nullptr, G > 1 ? &ps_ret : nullptr,
+                       ret_ptrs, launches));
+  MP_TRY(mk.mark());  // 9 (return barrier: folded into the GEMM2 tails / combine prologue)
   if (T > 0) {
     MP_TRY(launch_combine(L->ret, L->w, T, D.d, k, D.shared_f > 0 ? L->ys : nullptr,
                           D.shared_gate ? L->sgate : nullptr, static_cast<__nv_bfloat16*>(out), st,
                           G > 1 ? &ps_wait : nullptr));
     ++launches;
   }
-  MP_TRY(mark());  // 10 combine + return
+  MP_TRY(mk.mark());  // 10 combine + return
   L->last_launches = launches;
   return MP_OK;
 }
@@ -777,6 +827,90 @@ int mp_layer_forward(mp_layer* L, const void* x, void* out, int T, void* stream)
 int mp_layer_forward_timed(mp_layer* L, const void* x, void* out, int T, void* stream, void* const* events) {
   if (!events) return set_error(MP_E_ARG, "mp_layer_forward_timed: null events");
   return layer_forward(L, x, out, T, stream, events);
+}
+
+// ---- stage entries (host-driven transport, e.g. NCCL all-to-all-v; standalone K1 / K2 / K3 / K5)
+namespace {
+// Points the permute's destinations / the combine's sources at receive-layout images:
+// slot 8*a + D (a = 0 permute rows, 1 permute recv_src, 2 combine rows) = own buffer for
+// D == rank, else image D of the caller's staging buffer.
+int upload_stage_ptrs(mp_layer* L, int which, void* base, size_t elem_bytes, void* own, cudaStream_t st) {
+  bool changed = !L->stage_uploaded;
+  for (int D = 0; D < 8; ++D) {
+    void* p = nullptr;
+    if (D < L->G)
+      p = D == L->rank ? own
+                       : (base ? static_cast<uint8_t*>(base) + size_t(D) * size_t(L->recv_cap) * elem_bytes : nullptr);
+    changed |= L->stage_host[8 * which + D] != p;
+    L->stage_host[8 * which + D] = p;
+  }
+  if (!changed) return MP_OK;
+  MP_CUDA(cudaMemcpyAsync(L->stage_ptrs, L->stage_host, sizeof(L->stage_host), cudaMemcpyHostToDevice, st));
+  MP_CUDA(cudaStreamSynchronize(st));
+  L->stage_uploaded = true;
+  return MP_OK;
+}
+}  // namespace
+
+int mp_layer_route(mp_layer* L, const void* x, int T, void* stream) {
+  MP_TRY(check_forward_args(L, x, x, T, "mp_layer_route"));
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
+  const mp_layer_desc& D = L->desc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (T == 0) {
+    MP_CUDA(cudaMemsetAsync(L->batch_counts, 0, size_t(D.E) * 4, st));
+    return MP_OK;
+  }
+  return launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, D.E, D.shared_gate,
+                       D.top_k, D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts,
+                       L->batch_counts, L->ticket, L->blk_prefix, st, nullptr, L->wg32);
+}
+
+int mp_layer_permute(mp_layer* L, const void* x, int T, const int32_t* counts_all, void* staging, void* stream) {
+  MP_TRY(check_forward_args(L, x, x, T, "mp_layer_permute"));
+  if (!counts_all) return set_error(MP_E_ARG, "mp_layer_permute: null count table");
+  if (L->G > 1 && !staging) return set_error(MP_E_ARG, "mp_layer_permute: G=%d needs a staging buffer", L->G);
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
+  const mp_layer_desc& D = L->desc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (L->G > 1 && !L->src_image) {
+    cudaError_t e = cudaMalloc(&L->src_image, size_t(L->G) * size_t(L->recv_cap) * 4);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaMalloc(recv_src images)");
+  }
+  MP_TRY(upload_stage_ptrs(L, 0, staging, size_t(D.d) * 2, L->recv, st));
+  MP_TRY(upload_stage_ptrs(L, 1, L->src_image, 4, L->recv_src, st));
+  if (T == 0) return MP_OK;
+  return launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, nullptr, L->blk_prefix,
+                        reinterpret_cast<int32_t* const*>(L->stage_ptrs + 8), L->rank, L->G, T, D.d, D.E, D.top_k,
+                        reinterpret_cast<__nv_bfloat16* const*>(L->stage_ptrs), L->pos_dst, L->pos_row, st, nullptr);
+}
+
+int mp_layer_experts(mp_layer* L, const void* x, int T, const int32_t* counts_all, void* stream) {
+  MP_TRY(check_forward_args(L, x, x, T, "mp_layer_experts"));
+  if (!counts_all) return set_error(MP_E_ARG, "mp_layer_experts: null count table");
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
+  MP_TRY(bind_x(L, x, T));
+  Marker mk{nullptr, static_cast<cudaStream_t>(stream)};
+  int launches = 0;
+  return stage_experts(L, T, counts_all, nullptr, static_cast<cudaStream_t>(stream), mk, nullptr, nullptr, nullptr,
+                       launches);
+}
+
+int mp_layer_combine_gather(mp_layer* L, const void* ret_stage, int T, void* out, void* stream) {
+  MP_TRY(check_forward_args(L, out, out, T, "mp_layer_combine_gather"));
+  if (L->G > 1 && !ret_stage) return set_error(MP_E_ARG, "mp_layer_combine_gather: G=%d needs the return images", L->G);
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
+  const mp_layer_desc& D = L->desc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  MP_TRY(upload_stage_ptrs(L, 2, const_cast<void*>(ret_stage), size_t(D.d) * 2, L->recv, st));
+  if (T == 0) return MP_OK;
+  return launch_combine(nullptr, L->w, T, D.d, D.top_k, D.shared_f > 0 ? L->ys : nullptr,
+                        D.shared_gate ? L->sgate : nullptr, static_cast<__nv_bfloat16*>(out), st, nullptr,
+                        reinterpret_cast<const __nv_bfloat16* const*>(L->stage_ptrs + 16), L->pos_dst, L->pos_row);
 }
 
 int mp_layer_last_launches(mp_layer* L) { return L ? L->last_launches : 0; }

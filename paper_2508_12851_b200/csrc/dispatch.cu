@@ -200,11 +200,16 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
 // this GPU's return buffer by the (local or remote) GEMM2 epilogues, at rows
 // t*k .. t*k+k-1, so the combine is a local, fully coalesced read:
 // out[t] = bf16( sum_{j<k} w[t,j] * ret[t*k+j] (+ g[t] * ysh[t]) ), fp32, ascending j.
+// Gather form (bases != nullptr; the host-driven NCCL transport): pair (t, j)'s row
+// is bases[pos_dst[t,j]] + pos_row[t,j] * d -- the expert output left in the
+// receive-layout image of the GPU that computed it.
 template <int K>
 __global__ void __launch_bounds__(256)
     combine_kernel(const __nv_bfloat16* __restrict__ ret, const float* __restrict__ w, int T, int d,
                    const __nv_bfloat16* __restrict__ shared_y, const float* __restrict__ shared_gate,
-                   __nv_bfloat16* __restrict__ out, const PeerSync sync) {
+                   __nv_bfloat16* __restrict__ out, const PeerSync sync,
+                   const __nv_bfloat16* const* __restrict__ bases, const int32_t* __restrict__ pos_dst,
+                   const int32_t* __restrict__ pos_row) {
   griddep_launch_dependents();
   griddep_wait();
   // every rank's GEMM2 stored its rows of our tokens into ret (epoch C)
@@ -213,6 +218,11 @@ __global__ void __launch_bounds__(256)
   if (t >= T) return;
   const int lane = lane_id();
   const __nv_bfloat16* src = ret + size_t(t) * K * d;
+  const __nv_bfloat16* rows[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    rows[j] = bases ? bases[pos_dst[size_t(t) * K + j]] + size_t(pos_row[size_t(t) * K + j]) * d
+                    : src + size_t(j) * d;
   float wj[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) wj[j] = w[size_t(t) * K + j];
@@ -229,7 +239,7 @@ __global__ void __launch_bounds__(256)
       const int c = c0 + 32 * u;
       if (c < nvec) {
 #pragma unroll
-        for (int j = 0; j < K; ++j) v[u][j] = ld_cg_v4(src + size_t(j) * d + 8 * c);  // peer-written: L2
+        for (int j = 0; j < K; ++j) v[u][j] = ld_cg_v4(rows[j] + 8 * c);  // peer-written: L2
         if (shared_y) sv[u] = ld_nc_v4(shared_y + size_t(t) * d + 8 * c);
       }
     }
@@ -268,7 +278,8 @@ __global__ void __launch_bounds__(256)
 }
 
 int launch_combine(const __nv_bfloat16* ret, const float* w, int T, int d, int k, const __nv_bfloat16* shared_y,
-                   const float* shared_gate, __nv_bfloat16* out, cudaStream_t stream, const PeerSync* sync) {
+                   const float* shared_gate, __nv_bfloat16* out, cudaStream_t stream, const PeerSync* sync,
+                   const __nv_bfloat16* const* bases, const int32_t* pos_dst, const int32_t* pos_row) {
   if (d % 8 != 0) return set_error(MP_E_SHAPE, "combine: d=%d not a multiple of 8", d);
   if (k < 1 || k > 8) return set_error(MP_E_SHAPE, "combine: top_k=%d outside [1, 8]", k);
   if (T <= 0) return MP_OK;
@@ -277,7 +288,10 @@ int launch_combine(const __nv_bfloat16* ret, const float* w, int T, int d, int k
   cudaError_t e = cudaSuccess;
   switch (k) {
 #define MP_COMBINE_CASE(N) \
-  case N: e = launch_pdl(combine_kernel<N>, dim3(grid), dim3(256), 0, stream, ret, w, T, d, shared_y, shared_gate, out, ps); break;
+  case N:                                                                                                  \
+    e = launch_pdl(combine_kernel<N>, dim3(grid), dim3(256), 0, stream, ret, w, T, d, shared_y, shared_gate, out, ps, \
+                   bases, pos_dst, pos_row);                                                                \
+    break;
     MP_COMBINE_CASE(1) MP_COMBINE_CASE(2) MP_COMBINE_CASE(3) MP_COMBINE_CASE(4)
     MP_COMBINE_CASE(5) MP_COMBINE_CASE(6) MP_COMBINE_CASE(7) MP_COMBINE_CASE(8)
 #undef MP_COMBINE_CASE

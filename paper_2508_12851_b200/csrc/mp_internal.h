@@ -140,7 +140,9 @@ int grouped_gemm_ctas(int grid, int pair);
 // ---- K5 combine (the expert outputs are already back in this GPU's return buffer)
 int launch_combine(const __nv_bfloat16* ret /*[T][k][d]*/, const float* w, int T, int d, int k,
                    const __nv_bfloat16* shared_y, const float* shared_gate, __nv_bfloat16* out,
-                   cudaStream_t stream, const PeerSync* sync = nullptr);
+                   cudaStream_t stream, const PeerSync* sync = nullptr,
+                   const __nv_bfloat16* const* bases = nullptr, const int32_t* pos_dst = nullptr,
+                   const int32_t* pos_row = nullptr);
 
 // ---- stand-in flag raises over NVLink peer memory (exchange.cu)
 // Stand-ins when a raising kernel does not run (T == 0: no router / permute;

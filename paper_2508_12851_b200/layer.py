@@ -94,6 +94,7 @@ class B200MoELayer:
         self.ret = _view(p.ret, (T * k, d), torch.bfloat16, dev)          # expert outputs, (token, slot) order
         self.recv_src = _view(p.recv_src, (p.recv_cap,), torch.int32, dev)
         self.hist = _view(p.hist, (E,), torch.int32, dev)
+        self.batch_counts = _view(p.batch_counts, (E,), torch.int32, dev)
         self.w13_shared = _view(p.w13_shared, (2 * shape.shared_f, d), torch.bfloat16, dev) if shape.shared_f else None
         self.w2_shared = _view(p.w2_shared, (d, shape.shared_f), torch.bfloat16, dev) if shape.shared_f else None
         self.shared_gate = _view(p.shared_gate, (T,), torch.float32, dev) if shape.shared_gate else None

@@ -27,6 +27,9 @@ from paper_2508_12851_b200.routing import route_table, uniform_links
 from paper_2508_12851_b200.shapes import LayerShape
 
 
+NCCL_GROUP = None
+
+
 def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None, expect_rounds=0, staging=1):
     """expect: K3 plan keys (B200MoELayer.exec_plan) the first forward must have run, so the
     production plans -- CTA-pair tiles with the NVLink-scatter GEMM2 epilogue; the split plan
@@ -66,11 +69,12 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None, 
         acc = layer.dispatch_accounting()
         assert acc["remote_bytes"] == orc.reference_remote_bytes(ref.counts, route, shape.d), f"{tag}: bytes"
         check_layer_close(out.float().cpu().numpy(), ref.out[rank], ref.mag[rank], ref.mag2[rank], tag)
-        return out
+        return out, ref
 
     route1 = route_table([frozenset(s) for s in sets], E, lat, bw, shape.d)
     assert np.array_equal(layer.route, route1)
-    out_a = check(route1, "placement A").clone()
+    out_a, ref_a = check(route1, "placement A")
+    out_a = out_a.clone()
     if expect:
         plan = layer.exec_plan()
         assert all(plan[k] == v for k, v in expect.items()), f"{shape.name}: plan {plan}, expected {expect}"
@@ -86,6 +90,14 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None, 
     layer.check()
     dist.barrier()
     assert torch.equal(gout, out_a), "graph replay differs from eager forward"
+    # the NCCL all-to-all-v transport (the K4 A/B arm) runs the same kernels as stages with NCCL
+    # moving the rows: bit-identical outputs and routing
+    from paper_2508_12851_b200.nccl_path import NcclForward
+    nf = NcclForward(layer, group=NCCL_GROUP)
+    out_n = nf.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(out_n, out_a), "NCCL transport differs from the fused NVLink forward"
+    assert np.array_equal(layer.pos_row[:T_list[rank]].cpu().numpy(), ref_a.pos_row[rank]), "NCCL path pos_row"
     assert np.array_equal(layer.read_counts(), orc.moe_layer_forward(
         shape, xs, wg[:E], biases, route1, experts, shared, wg[E] if shape.shared_gate else None).counts)
     del g
@@ -120,6 +132,8 @@ def main():
     if local >= torch.cuda.device_count():
         raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but only {torch.cuda.device_count()} GPUs")
     torch.cuda.set_device(local)
+    global NCCL_GROUP
+    NCCL_GROUP = dist.new_group(backend="nccl")
     only = os.environ.get("MGPU_CASES")  # optional subset, e.g. "prod" (production plans only)
 
     if only != "prod":

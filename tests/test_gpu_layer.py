@@ -173,3 +173,23 @@ def test_large_batch_block_scan_from_global():
     assert np.array_equal(layer.pos_row[:T].cpu().numpy(), ref.pos_row[0])
     _check_close(out.float().cpu().numpy(), ref.out[0], ref.mag[0], ref.mag2[0])
     layer.close()
+
+
+@pytest.mark.parametrize("name,T", [("toy", 200), ("ds_small", 300), ("qwen_small", 150)])
+def test_stage_entries_match_fused_forward(name, T):
+    """The stage entries (mp_layer_route / _permute / _experts / _combine_gather, the kernels of
+    the host-driven NCCL transport) reproduce the fused forward bit for bit at G = 1."""
+    from paper_2508_12851_b200.nccl_path import NcclForward
+    shape = _shape(name)
+    experts, shared, wg = _weights(shape)
+    x = orc.synthetic_tokens(0, T, shape.d, seed=6)
+    bias = orc.origin_bias(0, shape.E, seed=6)
+    layer = _build_layer(shape, T, experts, shared, wg, bias)
+    xt = torch.from_numpy(x).cuda().bfloat16()
+    fused = layer.forward(xt).clone()
+    pos = layer.pos_row[:T].clone()
+    staged = NcclForward(layer).forward(xt)
+    torch.cuda.synchronize()
+    assert torch.equal(staged, fused)
+    assert torch.equal(layer.pos_row[:T], pos)
+    layer.close()
