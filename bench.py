@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--stages", action="store_true", help="print the per-stage table on stderr")
     ap.add_argument("--layers", type=int, default=4, help="--scenario stack: MoE layers in the stack")
-    ap.add_argument("--scenario", default="steady", choices=["steady", "shift", "stack"],
+    ap.add_argument("--scenario", default="steady", choices=["steady", "shift", "stack", "transport"],
                     help="shift: BASELINE config 5, drifting routing + expert migration vs static placement")
     return ap.parse_args()
 
@@ -279,7 +279,9 @@ def time_cpu_baseline(shape, seed, T_cpu, budget_s, weights_cpu, wg_np, bias_np,
 
 
 # ----------------------------------------------------------------------------- main (B200 arm)
-def main_b200(args):
+def setup_bench_layer(args):
+    """Process group, weights, the reference solver's placement on GPU-measured counts, the layer
+    and its warm-up (shared by the steady and transport scenarios)."""
     import torch
     import torch.distributed as dist
     from paper_2508_12851_b200 import _lib, workload as wl
@@ -351,6 +353,24 @@ def main_b200(args):
         layer.forward(xs[i % N_ROTATE], out)
     torch.cuda.synchronize()
     layer.check()
+    from types import SimpleNamespace
+    return SimpleNamespace(torch=torch, dist=dist, _lib=_lib, rank=rank, local=local, world=world, dev=dev,
+                           shape=shape, T=T, G=G, seed=seed, layer=layer, xs=xs, out=out, stream=stream,
+                           barrier=barrier, sets=sets, caps=caps, solver=solver, wg=wg, bias=bias,
+                           expert_src=expert_src, lib=lib)
+
+
+def main_b200(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2508_12851_b200 import _lib
+    from paper_2508_12851_b200.layer import HostPipeline
+    from paper_2508_12851_b200.routing import dispatch_accounting, route_table, uniform_links
+
+    b = setup_bench_layer(args)
+    rank, local, world, dev = b.rank, b.local, b.world, b.dev
+    shape, T, G, seed, layer, xs, out, stream, barrier = b.shape, b.T, b.G, b.seed, b.layer, b.xs, b.out, b.stream, b.barrier
+    sets, caps, solver, wg, bias, expert_src = b.sets, b.caps, b.solver, b.wg, b.bias, b.expert_src
 
     # ---- timed region (device time, CUDA events).  Inside it only the K3 (grouped GEMM)
     # boundaries are recorded per step -- the roofline's kernel duration; the full per-stage
@@ -951,6 +971,77 @@ def main_stack(args):
         layer.close()
 
 
+def main_transport(args):
+    """K4 A/B (north star (4)): the same layer, placement and inputs run through the
+    fused NVLink transport (B200MoELayer.forward: peer stores inside the permute kernel and the
+    GEMM2 epilogue, flag protocol inside the kernels) and through the NCCL all-to-all-v transport
+    (nccl_path.NcclForward: the same kernels as stages, NCCL send/recv of every (source, expert)
+    chunk, one host sync for the chunk sizes).  Reports tokens/s of both (max over ranks), the
+    NCCL dispatch / return wire rates, and the measured peer-copy bandwidth."""
+    from paper_2508_12851_b200.nccl_path import NcclForward
+    b = setup_bench_layer(args)
+    torch, dist = b.torch, b.dist
+    layer, xs, out, stream, G, T, rank, dev = b.layer, b.xs, b.out, b.stream, b.G, b.T, b.rank, b.dev
+
+    def timed(fn, steps):
+        for i in range(args.warmup):
+            fn(xs[i % N_ROTATE])
+        torch.cuda.synchronize()
+        b.barrier()
+        a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for i in range(steps):
+            fn(xs[i % N_ROTATE])
+        z.record(stream)
+        torch.cuda.synchronize()
+        b.barrier()
+        ms = torch.tensor([a.elapsed_time(z)], dtype=torch.float64, device=dev)
+        if G > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return ms.item()
+
+    fused_ms = timed(lambda x: layer.forward(x, out), args.steps)
+    fused_out = out.clone()
+    layer.check()
+    nf = NcclForward(layer, group=None)
+    nccl_ms = timed(lambda x: nf.forward(x, out), args.steps)
+    same = bool(torch.equal(out, fused_out))
+    nf.timing = True
+    for i in range(min(args.steps, 20)):
+        nf.forward(xs[i % N_ROTATE], out)
+    st_ms = nf.stage_ms()
+    vals = torch.tensor([st_ms.get(k, 0.0) for k in NcclForward.STAGES] +
+                        [nf.last["dispatch_bytes"], nf.last["return_bytes"]], dtype=torch.float64, device=dev)
+    parts = [torch.zeros_like(vals) for _ in range(G)]
+    if G > 1:
+        dist.all_gather(parts, vals)
+    else:
+        parts = [vals]
+    per_rank = [p.tolist() for p in parts]
+    peer_bw = measure_peer_copy(layer, G, rank) if G > 1 else None
+    if rank == 0:
+        ns = len(NcclForward.STAGES)
+        disp = [p[ns] / (p[2] * 1e-3) / 1e9 if p[2] > 0 else None for p in per_rank]
+        retr = [p[ns + 1] / (p[4] * 1e-3) / 1e9 if p[4] > 0 else None for p in per_rank]
+        line = {"scenario": "transport A/B (K4: fused NVLink peer stores vs NCCL all-to-all-v)", "metric": METRIC,
+                "unit": UNIT, "n_gpus": G, "steps": args.steps,
+                "config": {"model": b.shape.name, "tokens_per_gpu": T, "placement": b.solver, "slot_caps": b.caps},
+                "fused": {"value": G * T * args.steps / (fused_ms * 1e-3), "ms_per_step": fused_ms / args.steps},
+                "nccl": {"value": G * T * args.steps / (nccl_ms * 1e-3), "ms_per_step": nccl_ms / args.steps,
+                         "stages_ms_per_rank": [dict(zip(NcclForward.STAGES, p[:ns])) for p in per_rank],
+                         "dispatch_bytes_per_rank": [int(p[ns]) for p in per_rank],
+                         "return_bytes_per_rank": [int(p[ns + 1]) for p in per_rank],
+                         "dispatch_GBps_per_rank": disp, "return_GBps_per_rank": retr},
+                "fused_over_nccl": nccl_ms / fused_ms, "outputs_bit_identical": same,
+                "peer_copy_GBps": peer_bw / 1e9 if peer_bw else None, "nvlink_peak_GBps": 770.0,
+                "decision": "fused" if fused_ms <= nccl_ms else "nccl"}
+        print(json.dumps(line), flush=True)
+    if G > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    layer.close()
+
+
 def measure_peer_copy(layer, world, rank):
     """NVLink pull bandwidth: copy one expert slot from the next GPU into a free staging slot."""
     import torch
@@ -1004,6 +1095,9 @@ if __name__ == "__main__":
         raise SystemExit(0)
     if a.scenario == "stack" and a.impl != "reference":
         main_stack(a)
+        raise SystemExit(0)
+    if a.scenario == "transport" and a.impl != "reference":
+        main_transport(a)
         raise SystemExit(0)
     if a.impl == "reference":
         # keep the whole --steps K run within minutes: clamp the sample size for the big shapes

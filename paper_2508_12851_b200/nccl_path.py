@@ -34,8 +34,12 @@ from .routing import receive_layout
 
 
 class NcclForward:
-    def __init__(self, layer, group=None):
+    STAGES = ("route+counts", "permute", "dispatch", "experts", "return", "combine")
+
+    def __init__(self, layer, group=None, timing: bool = False):
         self.layer = layer
+        self.timing = timing
+        self.events = []
         self.group = group
         self.lib = layer.lib
         G, E, d = layer.world, layer.shape.E, layer.shape.d
@@ -59,37 +63,42 @@ class NcclForward:
         if out is None:
             out = torch.empty_like(x)
         st = self._stream()
+        ev = []
+
+        def mark():
+            if self.timing:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                ev.append(e)
+        mark()
         _lib.check(lib.mp_layer_route(layer._h, x.data_ptr(), T, st), "mp_layer_route")
         if G > 1:
             dist.all_gather_into_tensor(self.counts, self.batch_counts, group=self.group)
         else:
             self.counts.copy_(self.batch_counts)
         counts = self.counts.view(G, E).cpu().numpy()          # host sync: NCCL needs the sizes
-        route = layer.route
-        _, send = receive_layout(counts, route)                # send[s][e]: row in route[s][e]'s layout
+        mark()
         stg = self.staging.data_ptr() if G > 1 else None
         _lib.check(lib.mp_layer_permute(layer._h, x.data_ptr(), T, self.counts.data_ptr(), stg, st),
                    "mp_layer_permute")
-        chunks_out, chunks_in = [], []   # (peer, first row, rows)
+        mark()
+        # (peer, first row in the receive layout, rows) per (source, expert) chunk
+        chunks_out, chunks_in = chunk_plan(counts, layer.route, rank) if G > 1 else ([], [])
         if G > 1:
-            for e in range(E):
-                D = int(route[rank, e])
-                if D != rank and counts[rank, e] > 0:
-                    chunks_out.append((D, int(send[rank, e]), int(counts[rank, e])))
-            for s in range(G):
-                if s == rank:
-                    continue
-                for e in range(E):
-                    if route[s, e] == rank and counts[s, e] > 0:
-                        chunks_in.append((s, int(send[s, e]), int(counts[s, e])))
             self._exchange([(self.staging, D * self.cap + a, n, D) for D, a, n in chunks_out],
                            [(layer.recv, a, n, s) for s, a, n in chunks_in])
+        mark()
         _lib.check(lib.mp_layer_experts(layer._h, x.data_ptr(), T, self.counts.data_ptr(), st), "mp_layer_experts")
+        mark()
         if G > 1:
             self._exchange([(layer.recv, a, n, s) for s, a, n in chunks_in],
                            [(self.ret_stage, D * self.cap + a, n, D) for D, a, n in chunks_out])
+        mark()
         rs = self.ret_stage.data_ptr() if G > 1 else None
         _lib.check(lib.mp_layer_combine_gather(layer._h, rs, T, out.data_ptr(), st), "mp_layer_combine_gather")
+        mark()
+        if self.timing:
+            self.events.append(ev)
         row_b = layer.shape.d * 2
         self.last = {"chunks_out": len(chunks_out), "chunks_in": len(chunks_in),
                      "dispatch_bytes": sum(n for _, _, n in chunks_out) * row_b,
@@ -97,6 +106,15 @@ class NcclForward:
         return out
 
     __call__ = forward
+
+    def stage_ms(self) -> dict:
+        """Mean per-stage milliseconds of the timed forwards (timing=True; synchronises)."""
+        torch.cuda.synchronize(self.layer.device)
+        if not self.events:
+            return {}
+        per = np.array([[ev[i].elapsed_time(ev[i + 1]) for i in range(len(ev) - 1)] for ev in self.events])
+        self.events = []
+        return dict(zip(self.STAGES, per.mean(axis=0).tolist()))
 
     def _exchange(self, sends, recvs):
         """One NCCL group of point-to-point ops; chunks to / from one peer are posted in the
@@ -110,8 +128,9 @@ class NcclForward:
 
 
 def chunk_plan(counts: np.ndarray, route: np.ndarray, rank: int):
-    """(outgoing, incoming) chunk lists of one rank: (peer, first row in the peer's / own receive
-    layout, rows) per (source, expert) with rows on another GPU -- host mirror used by tests."""
+    """(outgoing, incoming) chunk lists of one rank: (peer, first row in the receiving GPU's layout
+    (routing.receive_layout), rows) per (source, expert) pair whose rows cross GPUs, expert
+    ascending per peer -- the order both sides post their NCCL ops in."""
     G, E = counts.shape
     _, send = receive_layout(counts, route)
     out = [(int(route[rank, e]), int(send[rank, e]), int(counts[rank, e])) for e in range(E)
