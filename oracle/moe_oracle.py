@@ -33,11 +33,13 @@ and what is not:
                            the stated tolerance for activations.
 
 Numerics contract shared with the CUDA kernels:
-  logits[t,e] = 32 lane partials (lane l: sequential fp32 accumulation over
-                k in [256 s + 8 l, +8), s ascending) combined by the butterfly
-                tree p[l] += p[l + o], o = 16..1 (bf16 inputs: each product is
-                exact in fp32, so the GPU's FMA chain and this add chain round
-                identically), then + bias[e].
+  logits[t,e] = 32 * n_lg lane partials (lane (g, l): sequential fp32
+                accumulation over k in [8 L s + 8 (32 g + l), +8), s ascending,
+                L = 32 n_lg, n_lg = router_lane_groups(d) in {1, 2, 4}) combined
+                by the butterfly tree p[l] += p[l + o], o = 16..1 inside each
+                group, then q[g] += q[g + o], o = n_lg/2..1 across groups (bf16
+                inputs: each product is exact in fp32, so the GPU's FMA chain
+                and this add chain round identically), then + bias[e].
   top-k       = k largest logits, descending, ties -> lower expert id.
   h           = bf16( silu(g) * u ) with g, u the fp32 GEMM accumulators.
   y           = bf16( h @ W2^T ) (fp32 accumulate).
@@ -187,14 +189,26 @@ def slot_assignment(gpu_experts) -> dict:
 # ----------------------------------------------------------------------------- router
 
 
+def router_lane_groups(d: int) -> int:
+    """Lane groups of the router contract: 4 for d >= 4096 (d % 1024 == 0), 2 for d >= 2048
+    (d % 512 == 0), else 1 -- the same function as csrc/router.cu router_lane_groups."""
+    if d >= 4096 and d % 1024 == 0:
+        return 4
+    if d >= 2048 and d % 512 == 0:
+        return 2
+    return 1
+
+
 def router_logits(x: np.ndarray, wg: np.ndarray, bias: np.ndarray | None = None) -> np.ndarray:
     """Router logits under the kernel's numerics contract (csrc/router.cu).
 
-    Lane l of 32 owns k in [256 s + 8 l, 256 s + 8 l + 8) for s = 0..d/256-1; its
-    partial is a sequential fp32 accumulation over those k ascending (bf16
-    inputs: products exact, one rounding per add == the GPU's FMA).  The 32
-    partials are combined by the butterfly tree p[l] <- p[l] + p[l + o],
-    o = 16, 8, 4, 2, 1; then + bias[e].
+    L = 32 * n_lg logical lanes, n_lg = router_lane_groups(d).  Logical lane
+    (g, l) -- group g, lane l of 32 -- owns k in [8 L s + 8 (32 g + l), +8) for
+    s = 0..d/(8 L)-1; its partial is a sequential fp32 accumulation over those k
+    ascending (bf16 inputs: products exact, one rounding per add == the GPU's
+    FMA).  Inside each group the 32 partials are combined by the butterfly tree
+    p[l] <- p[l] + p[l + o], o = 16, 8, 4, 2, 1; then the group sums by
+    q[g] <- q[g] + q[g + o], o = n_lg/2 .. 1; then + bias[e].
     """
     x = np.asarray(x, dtype=np.float32)
     wg = np.asarray(wg, dtype=np.float32)
@@ -202,17 +216,23 @@ def router_logits(x: np.ndarray, wg: np.ndarray, bias: np.ndarray | None = None)
     E = wg.shape[0]
     if d % 256:
         raise ValueError("router contract needs d % 256 == 0")
-    S = d // 256
-    xr = x.reshape(T, S, 32, 8)
-    wr = wg.reshape(E, S, 32, 8)
-    acc = np.zeros((T, E, 32), dtype=np.float32)
+    G = router_lane_groups(d)
+    S = d // (256 * G)
+    xr = x.reshape(T, S, G, 32, 8)
+    wr = wg.reshape(E, S, G, 32, 8)
+    acc = np.zeros((T, E, G, 32), dtype=np.float32)
     for s in range(S):
         for j in range(8):
-            acc += xr[:, None, s, :, j] * wr[None, :, s, :, j]   # exact products, one fp32 rounding per add
+            acc += xr[:, None, s, :, :, j] * wr[None, :, s, :, :, j]   # exact products, one fp32 rounding per add
     p = acc
     for o in (16, 8, 4, 2, 1):
         p = p[..., :o] + p[..., o:2 * o]
-    logits = np.ascontiguousarray(p[..., 0])
+    q = p[..., 0]
+    o = G // 2
+    while o >= 1:
+        q = q[..., :o] + q[..., o:2 * o]
+        o //= 2
+    logits = np.ascontiguousarray(q[..., 0])
     if bias is not None:
         logits[:, :bias.shape[0]] += np.asarray(bias, dtype=np.float32)[None, :]
     return logits

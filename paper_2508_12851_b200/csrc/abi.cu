@@ -45,7 +45,7 @@ int set_cuda_error(cudaError_t e, const char* what) {
 }
 
 int ensure_max_dyn_smem(const void* kernel, size_t bytes, const char* what) {
-  if (bytes <= 48 * 1024) return MP_OK;
+  if (bytes == 0) return MP_OK;  // the 48 KB default covers static + dynamic: set it for any dynamic size
   struct Entry {
     const void* fn;
     int dev;
@@ -110,6 +110,7 @@ struct mp_layer {
   __nv_bfloat16 *h = nullptr, *wg = nullptr, *w13s = nullptr, *w2s = nullptr, *hs = nullptr, *ys = nullptr;
   __nv_bfloat16* wg_packed = nullptr;
   float* wg32 = nullptr;  // Wg in fp32, router consumption order
+  float* partial = nullptr;  // router lane-group partial logits [n_lg][max_tokens][E_pad]
   float *bias = nullptr, *w = nullptr, *sgate = nullptr;
   int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr, *blk_prefix = nullptr,
           *batch_counts = nullptr, *route_d = nullptr,
@@ -331,6 +332,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       L->wg = cv.take<__nv_bfloat16>(size_t(E_tot) * D.d);
       L->wg_packed = cv.take<__nv_bfloat16>(size_t(router_e_pad(E_tot)) * D.d);
       L->wg32 = cv.take<float>(size_t(router_e_pad(E_tot)) * D.d);
+      L->partial = cv.take<float>(router_partial_floats(T, D.d, E_tot));
       L->bias = cv.take<float>(E);
       L->w = cv.take<float>(size_t(T) * k);
       L->sgate = D.shared_gate ? cv.take<float>(T) : nullptr;
@@ -785,7 +787,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   if (T > 0) {
     MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
                          D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
-                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr, L->wg32));
+                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr, L->wg32, L->partial));
     ++launches;
   } else if (G > 1) {
     // no router / permute on this origin: publish zero counts, raise A and B
@@ -864,7 +866,7 @@ int mp_layer_route(mp_layer* L, const void* x, int T, void* stream) {
   }
   return launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, D.E, D.shared_gate,
                        D.top_k, D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts,
-                       L->batch_counts, L->ticket, L->blk_prefix, st, nullptr, L->wg32);
+                       L->batch_counts, L->ticket, L->blk_prefix, st, nullptr, L->wg32, L->partial);
 }
 
 int mp_layer_permute(mp_layer* L, const void* x, int T, const int32_t* counts_all, void* staging, void* stream) {

@@ -88,7 +88,10 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
                   int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync = nullptr,
-                  const float* w32 = nullptr);
+                  const float* w32 = nullptr, float* partial = nullptr);
+// Partial-logit scratch the router needs for T tokens ([lane groups][T][E_pad] floats).
+size_t router_partial_floats(int T, int d, int E_tot);
+__host__ __device__ int router_lane_groups(int d);
 // Wg pre-converted to fp32 in the router's consumption order (E_pad * d floats).
 int launch_router_pack32(const __nv_bfloat16* wg, int E_tot, int d, float* w32, cudaStream_t stream);
 int launch_router_logits(const float* logits, int ld, const float* bias, int T, int E, int k, int score_mode,

@@ -13,21 +13,28 @@
 //   hist[e]    += #tokens whose top-k contains e   (token_count = 1 per token)
 //
 // Bit-exactness contract (restated by oracle/moe_oracle.py:router_logits):
-//   * lane l of 32 owns the k-slices [256 s + 8 l, 256 s + 8 l + 8), s = 0..d/256-1;
-//     its partial is ONE sequential fp32 FMA chain over those k ascending, from 0;
-//     x and Wg are bf16, so each product is exact and fma == rn(acc + x*w);
-//   * the 32 partials are combined by the butterfly tree
-//     p[l] <- p[l] + p[l + o] for o = 16, 8, 4, 2, 1 (fp add is commutative, so
-//     a warp reduce-scatter yields exactly this tree), then + bias[e];
+//   * L = 32 n_lg logical lanes, n_lg = router_lane_groups(d) in {1, 2, 4}; lane
+//     (g, l) owns the k-slices [8 L s + 8 (32 g + l), +8), s = 0..d/(8L)-1 -- i.e.
+//     the 256-k steps g, g + n_lg, g + 2 n_lg, ... at offset 8 l; its partial is ONE
+//     sequential fp32 FMA chain over those k ascending, from 0; x and Wg are bf16, so
+//     each product is exact and fma == rn(acc + x*w);
+//   * inside a group the 32 partials are combined by the butterfly tree
+//     p[l] <- p[l] + p[l + o] for o = 16, 8, 4, 2, 1 (fp add is commutative, so a
+//     warp reduce-scatter yields exactly this tree); the group sums by
+//     q[g] <- q[g] + q[g + o], o = n_lg/2 .. 1; then + bias[e];
 //   * selection compares logits only (independent of the exp implementation).
 //
-// Mapping: a CTA owns 32 tokens (8 warps x 4 tokens).  A warp keeps 4 tokens x
-// 8 experts = 32 accumulators per lane (16 FFMA2 chains) while its lanes walk d;
-// x rows are read straight from HBM (512 B coalesced per token per step), the
-// padded bf16 Wg [E_pad][d] through L1/L2.  One reduce-scatter per 8-expert pass
-// leaves lane l holding logit (token l/8, expert l%8).
+// Two kernels.  router_chain_kernel: persistent over every SM, one warp per unit =
+// (8-expert pass, lane group, 4-token quad) -- 4 x 8 = 32 accumulators per lane as
+// 16 FFMA2 chains while the lanes walk the group's k-steps (x straight from HBM,
+// 512 B coalesced per token per step; Wg fp32 in consumption order through L1/L2);
+// a reduce-scatter leaves lane l holding (token l/8, expert l%8), stored as a group
+// partial.  Lane groups split d so that even one expert pass (Mixtral) yields enough
+// units to fill the SMs.  router_select_kernel: one CTA per 32-token block combines
+// the partials by the contract's tree and runs top-k, weights and the histogram.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "mp_internal.h"
@@ -43,6 +50,12 @@ constexpr int kMaxK = 8;
 
 int router_block_tokens() { return rt::kTokens; }
 __host__ __device__ int router_e_pad(int E_tot) { return (E_tot + 7) / 8 * 8; }
+
+#define MP_TRY_R(call)             \
+  do {                             \
+    const int _r = (call);         \
+    if (_r != MP_OK) return _r;    \
+  } while (0)
 
 // packed[E_pad][d] bf16 = Wg (zero rows pad E_tot up to a multiple of 8)
 __global__ void router_pack_kernel(const __nv_bfloat16* __restrict__ wg, int E_tot, int E_pad, int d,
@@ -153,97 +166,62 @@ MP_DEV void select_topk_store(float v0, float v1, int E, int k, int score_mode, 
   }
 }
 
-#ifndef MP_ROUTER_MIN_BLOCKS
-#define MP_ROUTER_MIN_BLOCKS 1
-#endif
-constexpr int kQuads = 8;      // 8 token quads x 4 tokens = rt::kTokens
-constexpr int kMaxWarps = 16;  // 2 warps per quad when there are >= 2 expert passes
-constexpr int kTokPerWarp = 4;
+constexpr int kTokPerWarp = 4;  // a chain unit: 4 tokens (one quad) x 8 experts (one pass)
 constexpr int kExpPerPass = 8;
+constexpr int kChainWarps = 16;  // warps per CTA of the chain kernel
 
-// kWarpsT = 8: one warp per quad, 255-register budget, two k-steps of loads in
-// flight per warp (Mixtral: one expert pass; x read once, straight from HBM
-// after an L2 bulk prefetch of the CTA's rows).  kWarpsT = 16: two warps per
-// quad on alternate passes, 128 registers -- twice the warps to hide latency
-// when there are >= 2 passes (E_pad >= 16); with kXSmem the CTA's 32 x rows
-// (contiguous, 32 d bf16) are bulk-copied into shared memory once and every
-// pass reads them from there.
-template <int kWarpsT, bool kXSmem, bool kW32>
-__global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
-    router_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wp,
-                  const float4* __restrict__ w32,
-                  const float* __restrict__ bias, int T, int d, int E, int has_gate, int k, int score_mode,
-                  int renorm, int32_t* __restrict__ idx, float* __restrict__ wout, float* __restrict__ shared_gate,
-                  uint32_t* __restrict__ hist, int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
-                  uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix, const PeerSync sync,
-                  int stage_counts, int csplit) {
-  __shared__ float logits[rt::kTokens][rt::kMaxE + 9];
-  __shared__ int cnt_s[rt::kMaxE];
-  __shared__ uint64_t xbar;
-  // kXSmem: the CTA's x rows [32][d]; afterwards (last CTA) the [nb][E] block counts
-  extern __shared__ __align__(128) uint8_t dsm[];
-  int* bc = reinterpret_cast<int*>(dsm);
+// Lane groups of the numerics contract (oracle.router_lane_groups): with n_lg groups
+// of 32 logical lanes, the chain of lane (g, l) walks the 256-k steps g, g + n_lg, ...
+// so every unit of work is one 32-lane warp over d / n_lg of the k range.
+__host__ __device__ int router_lane_groups(int d) {
+  if (d >= 4096 && d % 1024 == 0) return 4;
+  if (d >= 2048 && d % 512 == 0) return 2;
+  return 1;
+}
 
-  const int E_tot = E + has_gate;
-  const int E_pad = router_e_pad(E_tot);
-  // csplit > 1: a cluster of csplit CTAs shares one 32-token block, CTA r computing the
-  // expert passes r, r + csplit, ... and storing its logits into the leader's smem (DSMEM);
-  // the leader does the rest.  Small batches get csplit x the CTAs on the chains.
-  const int blk = blockIdx.x / csplit, crank = blockIdx.x - blk * csplit;
-  const int n_blk = gridDim.x / csplit;
-  const int t0 = blk * rt::kTokens;
-  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
-  const int n_tok = min(rt::kTokens, T - t0);
-  for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
-  if (kXSmem && tid == 0) {
-    mbar_init(&xbar, 1);
-    fence_barrier_init();
-  }
+// Stage 1 (chains).  Unit = (expert pass p, lane group g, token quad q): one warp keeps
+// 4 tokens x 8 experts = 16 FFMA2 accumulator pairs per lane while its lanes walk the
+// group's k-steps (x: 512 B coalesced per token per step, straight from HBM; Wg: the
+// fp32 consumption-order operand or the bf16 rows, through L1/L2).  A reduce-scatter
+// butterfly leaves lane l holding the group partial of (token l/8, expert l%8), stored
+// to partial[g][t][E_pad].  Persistent: warps stride over the units, quads fastest.
+template <bool kW32>
+__global__ void __launch_bounds__(kChainWarps * 32, 1)
+    router_chain_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wp,
+                        const float4* __restrict__ w32, int T, int d, int E_pad, int n_lg,
+                        float* __restrict__ partial) {
   griddep_launch_dependents();
-  __syncthreads();
   griddep_wait();
-  const __nv_bfloat16* xblk = x + size_t(t0) * d;  // n_tok contiguous rows
-  if (tid == 0) {
-    const uint32_t bytes = uint32_t(n_tok) * d * 2;
-    if (kXSmem) {
-      mbar_arrive_expect_tx(&xbar, bytes);
-      for (uint32_t off = 0; off < bytes; off += 32768u)
-        bulk_load(dsm + off, reinterpret_cast<const uint8_t*>(xblk) + off, min(32768u, bytes - off), &xbar);
-    } else {
-      for (uint32_t off = 0; off < bytes; off += 32768u)
-        bulk_prefetch_l2(reinterpret_cast<const uint8_t*>(xblk) + off, min(32768u, bytes - off));
-    }
-  }
-
-  // this warp's 4 tokens (rows past T are never loaded and are discarded); with
-  // 16 warps, warp w and w + 8 share a quad and take alternate expert passes
-  const int quad = warp % kQuads, n_pg = (blockDim.x >> 5) / kQuads;
-  const __nv_bfloat16* xr[kTokPerWarp];
+  const int lane = lane_id();
+  const int n_quads = (T + kTokPerWarp - 1) / kTokPerWarp;
+  const int n_pass = E_pad / kExpPerPass;
+  const int S_all = d / 256;          // 256-k steps in d
+  const int S = S_all / n_lg;         // steps of one lane group's chain
+  const int n_units = n_quads * n_pass * n_lg;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp_id();
+  const int n_warps = gridDim.x * (blockDim.x >> 5);
+  for (int u = gw; u < n_units; u += n_warps) {
+    const int q = u % n_quads, pg = u / n_quads;
+    const int g = pg % n_lg, pass = pg / n_lg;
+    const int t0 = q * kTokPerWarp;
+    const __nv_bfloat16* xr[kTokPerWarp];
 #pragma unroll
-  for (int i = 0; i < kTokPerWarp; ++i) {
-    const int r = quad * kTokPerWarp + i;
-    xr[i] = kXSmem ? reinterpret_cast<const __nv_bfloat16*>(dsm) + size_t(r) * d + 8 * lane
-                   : x + size_t(t0 + (r < n_tok ? r : 0)) * d + 8 * lane;
-  }
-  if (kXSmem) mbar_wait(&xbar, 0);
-  const int S = d / 256;
-
-  for (int e0 = kExpPerPass * (crank * n_pg + warp / kQuads); e0 < E_pad; e0 += kExpPerPass * n_pg * csplit) {
+    for (int i = 0; i < kTokPerWarp; ++i)
+      xr[i] = x + size_t(t0 + i < T ? t0 + i : 0) * d + 256 * g + 8 * lane;  // rows past T: discarded
     unsigned long long acc[kTokPerWarp][kExpPerPass / 2];
 #pragma unroll
     for (int i = 0; i < kTokPerWarp; ++i)
 #pragma unroll
       for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
-    const __nv_bfloat16* wr = wp + size_t(e0) * d + 8 * lane;
     if (kW32) {
-      // fp32 pairs straight from the pre-converted Wg (two halves of 4 k each)
-      const float4* w4 = w32 + size_t(e0 / kExpPerPass) * S * 16 * 32 + lane;
+      // fp32 pairs straight from the pre-converted Wg (two halves of 4 k each); the
+      // step of this group's chain number s is the 256-k step g + n_lg * s
+      const float4* w4 = w32 + (size_t(pass) * S_all + g) * 16 * 32 + lane;
 #pragma unroll 1
-      for (int s = 0; s < S; ++s, w4 += 16 * 32) {
+      for (int s = 0; s < S; ++s, w4 += size_t(n_lg) * 16 * 32) {
         uint4 xv[kTokPerWarp];
 #pragma unroll
-        for (int i = 0; i < kTokPerWarp; ++i)
-          xv[i] = kXSmem ? *reinterpret_cast<const uint4*>(xr[i] + 256 * s) : ld_nc_v4(xr[i] + 256 * s);
+        for (int i = 0; i < kTokPerWarp; ++i) xv[i] = ld_nc_v4(xr[i] + size_t(256) * n_lg * s);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float4 wv[8];
@@ -251,12 +229,12 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
           for (int t2 = 0; t2 < 8; ++t2) wv[t2] = __ldg(w4 + (8 * h + t2) * 32);
 #pragma unroll
           for (int qq = 0; qq < 4; ++qq) {  // strictly ascending k inside the lane's slice
-            const int q = 4 * h + qq;
+            const int qk = 4 * h + qq;
             float xs[kTokPerWarp];
 #pragma unroll
             for (int i = 0; i < kTokPerWarp; ++i) {
-              const uint32_t u = (&xv[i].x)[q >> 1];
-              xs[i] = (q & 1) ? bf16_hi(u) : bf16_lo(u);
+              const uint32_t uu = (&xv[i].x)[qk >> 1];
+              xs[i] = (qk & 1) ? bf16_hi(uu) : bf16_lo(uu);
             }
             const float4 a = wv[2 * qq], b = wv[2 * qq + 1];
             const unsigned long long w2[4] = {pack2(a.x, a.y), pack2(a.z, a.w), pack2(b.x, b.y), pack2(b.z, b.w)};
@@ -267,31 +245,32 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
           }
         }
       }
-    } else
-#pragma unroll(kWarpsT == kQuads ? 2 : 1)
-    for (int s = 0; s < S; ++s) {
-      uint4 xv[kTokPerWarp], wv[kExpPerPass];
+    } else {
+      const __nv_bfloat16* wr = wp + size_t(kExpPerPass) * pass * d + 256 * g + 8 * lane;
+#pragma unroll 1
+      for (int s = 0; s < S; ++s) {
+        const size_t ko = size_t(256) * n_lg * s;
+        uint4 xv[kTokPerWarp], wv[kExpPerPass];
 #pragma unroll
-      for (int i = 0; i < kTokPerWarp; ++i)
-        xv[i] = kXSmem ? *reinterpret_cast<const uint4*>(xr[i] + 256 * s) : ld_nc_v4(xr[i] + 256 * s);
+        for (int i = 0; i < kTokPerWarp; ++i) xv[i] = ld_nc_v4(xr[i] + ko);
 #pragma unroll
-      for (int j = 0; j < kExpPerPass; ++j)
-        wv[j] = __ldg(reinterpret_cast<const uint4*>(wr + size_t(j) * d + 256 * s));
+        for (int j = 0; j < kExpPerPass; ++j) wv[j] = __ldg(reinterpret_cast<const uint4*>(wr + size_t(j) * d + ko));
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {  // strictly ascending k inside the lane's slice
-        float xs[kTokPerWarp];
+        for (int qk = 0; qk < 8; ++qk) {  // strictly ascending k inside the lane's slice
+          float xs[kTokPerWarp];
 #pragma unroll
-        for (int i = 0; i < kTokPerWarp; ++i) {
-          const uint32_t u = (&xv[i].x)[q >> 1];
-          xs[i] = (q & 1) ? bf16_hi(u) : bf16_lo(u);
-        }
+          for (int i = 0; i < kTokPerWarp; ++i) {
+            const uint32_t uu = (&xv[i].x)[qk >> 1];
+            xs[i] = (qk & 1) ? bf16_hi(uu) : bf16_lo(uu);
+          }
 #pragma unroll
-        for (int j = 0; j < kExpPerPass / 2; ++j) {
-          const uint32_t u0 = (&wv[2 * j].x)[q >> 1], u1 = (&wv[2 * j + 1].x)[q >> 1];
-          const unsigned long long w2 =
-              (q & 1) ? pack2(bf16_hi(u0), bf16_hi(u1)) : pack2(bf16_lo(u0), bf16_lo(u1));
+          for (int j = 0; j < kExpPerPass / 2; ++j) {
+            const uint32_t u0 = (&wv[2 * j].x)[qk >> 1], u1 = (&wv[2 * j + 1].x)[qk >> 1];
+            const unsigned long long w2 =
+                (qk & 1) ? pack2(bf16_hi(u0), bf16_hi(u1)) : pack2(bf16_lo(u0), bf16_lo(u1));
 #pragma unroll
-          for (int i = 0; i < kTokPerWarp; ++i) ffma2(acc[i][j], xs[i], w2);
+            for (int i = 0; i < kTokPerWarp; ++i) ffma2(acc[i][j], xs[i], w2);
+          }
         }
       }
     }
@@ -315,19 +294,47 @@ __global__ void __launch_bounds__(kWarpsT * 32, MP_ROUTER_MIN_BLOCKS)
         v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
       }
     }
-    const int tt = quad * kTokPerWarp + (lane >> 3), e = e0 + (lane & 7);
-    if (e < E_tot) {
-      float val = v[0];
-      if (bias != nullptr && e < E) val = __fadd_rn(val, bias[e]);
-      if (csplit > 1)
-        st_cluster_f32(&logits[tt][e], 0, val);
-      else
-        logits[tt][e] = val;
-    }
+    const int tt = t0 + (lane >> 3);
+    if (tt < T) partial[(size_t(g) * T + tt) * E_pad + kExpPerPass * pass + (lane & 7)] = v[0];
   }
-  if (csplit > 1) {
-    cluster_sync();  // every CTA's logits are in the leader's smem
-    if (crank != 0) return;
+}
+
+// Stage 2 (selection).  CTA = one router block of 32 tokens (the histogram / permute
+// block), 8 warps: logits = the lane groups' partials combined by the contract's tree
+// (q[g] += q[g + o], o = n_lg/2..1) + bias; then top-k, gate weights, block-aggregated
+// histogram, and -- in the last CTA -- the batch counts, the block prefix and (G > 1) the
+// count exchange with epoch A.
+__global__ void __launch_bounds__(256)
+    router_select_kernel(const float* __restrict__ partial, int n_lg, int E_pad, const float* __restrict__ bias,
+                         int T, int E, int has_gate, int k, int score_mode, int renorm, int32_t* __restrict__ idx,
+                         float* __restrict__ wout, float* __restrict__ shared_gate, uint32_t* __restrict__ hist,
+                         int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
+                         uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix, const PeerSync sync,
+                         int stage_counts) {
+  __shared__ float logits[rt::kTokens][rt::kMaxE + 9];
+  __shared__ int cnt_s[rt::kMaxE];
+  extern __shared__ __align__(128) uint8_t dsm[];  // last CTA: the [nb][E] block counts
+  int* bc = reinterpret_cast<int*>(dsm);
+  const int E_tot = E + has_gate;
+  const int blk = blockIdx.x, n_blk = gridDim.x;
+  const int t0 = blk * rt::kTokens;
+  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
+  griddep_launch_dependents();
+  griddep_wait();
+  for (int i = tid; i < rt::kTokens * E_tot; i += blockDim.x) {
+    const int tt = i / E_tot, e = i - tt * E_tot, t = t0 + tt;
+    if (t >= T) continue;
+    const float* pp = partial + size_t(t) * E_pad + e;
+    const size_t gs = size_t(T) * E_pad;  // stride between lane groups
+    float val = __ldcg(pp);
+    if (n_lg == 2) {
+      val = val + __ldcg(pp + gs);
+    } else if (n_lg == 4) {  // q[g] += q[g + 2], then q[0] += q[1]
+      val = (val + __ldcg(pp + 2 * gs)) + (__ldcg(pp + gs) + __ldcg(pp + 3 * gs));
+    }
+    if (bias != nullptr && e < E) val = __fadd_rn(val, bias[e]);
+    logits[tt][e] = val;
   }
   __syncthreads();
 
@@ -461,10 +468,33 @@ int launch_router_logits(const float* logits, int ld, const float* bias, int T, 
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_logits_kernel launch");
 }
 
+// Partial-logit scratch of the stateless entries (the layer passes its own): per device,
+// grown on demand, never freed.
+static float* stateless_partial(size_t floats) {
+  static std::mutex mu;
+  static float* buf[16] = {};
+  static size_t cap[16] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (cap[dev] < floats) {
+    if (buf[dev]) cudaFree(buf[dev]);
+    buf[dev] = nullptr;
+    cap[dev] = 0;
+    if (cudaMalloc(&buf[dev], floats * sizeof(float)) != cudaSuccess) return nullptr;
+    cap[dev] = floats;
+  }
+  return buf[dev];
+}
+
+size_t router_partial_floats(int T, int d, int E_tot) {
+  return size_t(router_lane_groups(d)) * size_t(T) * size_t(router_e_pad(E_tot));
+}
+
 int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
-                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync, const float* w32) {
+                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync, const float* w32, float* partial) {
   if (batch_counts && !ticket) return set_error(MP_E_ARG, "router: batch counts need a ticket word");
   if (E < 1 || E > rt::kMaxE) return set_error(MP_E_SHAPE, "router: E=%d outside [1, %d]", E, rt::kMaxE);
   if (k < 1 || k > E || k > rt::kMaxK) return set_error(MP_E_SHAPE, "router: top_k=%d invalid for E=%d", k, E);
@@ -474,68 +504,38 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   if (sync && sync->G > 1 && (!batch_counts || !blk_counts))
     return set_error(MP_E_ARG, "router: the count exchange needs the batch counts");
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return set_error(MP_E_ARG, "router: x not 16-byte aligned");
-  const int grid = (T + rt::kTokens - 1) / rt::kTokens;
-  size_t bc_bytes = blk_counts && batch_counts ? size_t(grid) * E * 4 : 0;
-  const bool stage_counts = bc_bytes <= 200 * 1024;  // larger T: the last CTA scans from global memory
-  if (!stage_counts) bc_bytes = 0;
-  // variant: 0 = 8 warps, x from HBM (one expert pass); 1 = 16 warps, x from HBM;
-  // 2 = 16 warps, x rows in smem; 3 = 8 warps, x rows in smem (MP_ROUTER_VARIANT overrides)
-  const char* venv = getenv("MP_ROUTER_VARIANT");
-  const int variant_env = venv ? atoi(venv) : -1;
-  const size_t x_bytes = size_t(rt::kTokens) * d * 2;
-  const bool multi_pass = router_e_pad(E + (has_gate ? 1 : 0)) >= 2 * kExpPerPass;
-  int variant = multi_pass ? (x_bytes <= 160 * 1024 ? 2 : 1) : 0;
-  if (variant_env >= 0 && variant_env <= 3) variant = variant_env;
-  if ((variant == 2 || variant == 3) && x_bytes > 160 * 1024) variant = variant == 2 ? 1 : 0;
-  using KernT = decltype(&router_kernel<kQuads, false, false>);
-  const KernT kerns[4] = {router_kernel<kQuads, false, false>, router_kernel<kMaxWarps, false, false>,
-                          router_kernel<kMaxWarps, true, false>, router_kernel<kQuads, true, false>};
-  const KernT kerns32[4] = {router_kernel<kQuads, false, true>, router_kernel<kMaxWarps, false, true>,
-                            router_kernel<kMaxWarps, true, true>, router_kernel<kQuads, true, true>};
+  const int E_tot = E + (has_gate ? 1 : 0), E_pad = router_e_pad(E_tot), n_lg = router_lane_groups(d);
+  if (!partial) partial = stateless_partial(router_partial_floats(T, d, E_tot));
+  if (!partial) return set_error(MP_E_CUDA, "router: cannot allocate the partial-logit scratch");
   const char* w32env = getenv("MP_ROUTER_W32");
   const bool use32 = w32 != nullptr && (w32env == nullptr || atoi(w32env) != 0);
-  const KernT kern = use32 ? kerns32[variant] : kerns[variant];
-  const bool xsmem = variant >= 2;
-  const int warps = (variant == 1 || variant == 2) ? kMaxWarps : kQuads;
-  const size_t smem = std::max(bc_bytes, xsmem ? x_bytes : size_t(0));
-  {
-    const int ra = ensure_max_dyn_smem(reinterpret_cast<const void*>(kern), smem, "cudaFuncSetAttribute(router)");
-    if (ra != MP_OK) return ra;
-  }
-  // small batches: split each block's expert passes over a cluster of up to 8 CTAs so the
-  // grid covers the SMs (one CTA per SM for the register-heavy variants)
-  const int n_pass = router_e_pad(E + (has_gate ? 1 : 0)) / kExpPerPass;
-  const int n_pg = warps / kQuads;
-  int csplit = 1;
-  while (csplit * 2 <= 8 && csplit * 2 * n_pg <= n_pass && grid * csplit * 2 <= kNumSMs) csplit *= 2;
-  if (const char* cs = getenv("MP_ROUTER_SPLIT")) csplit = std::max(1, std::min(8, atoi(cs)));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid * csplit);
-  cfg.blockDim = dim3(warps * 32);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[2];
-  int na = 0;
-  if (csplit > 1) {
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = csplit;
-    attr[na].val.clusterDim.y = 1;
-    attr[na].val.clusterDim.z = 1;
-    ++na;
-  }
-  if (pdl_enabled()) {
-    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
-  cfg.attrs = attr;
-  cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, x, wg_packed, reinterpret_cast<const float4*>(w32), bias, T, d, E,
-                                     has_gate ? 1 : 0, k, score_mode,
-                                     renorm, idx, w, shared_gate, hist, blk_counts, batch_counts, ticket, blk_prefix,
-                                     sync ? *sync : PeerSync(), stage_counts ? 1 : 0, csplit);
+
+  // stage 1: the chains, persistent over every SM (MP_ROUTER_GRID overrides, for tests)
+  const int n_units = ((T + kTokPerWarp - 1) / kTokPerWarp) * (E_pad / kExpPerPass) * n_lg;
+  int grid1 = std::min(kNumSMs, (n_units + kChainWarps - 1) / kChainWarps);
+  if (const char* ge = getenv("MP_ROUTER_GRID")) grid1 = std::max(1, atoi(ge));
+  cudaError_t e;
+  if (use32)
+    e = launch_pdl(router_chain_kernel<true>, dim3(grid1), dim3(kChainWarps * 32), 0, stream, x, wg_packed,
+                   reinterpret_cast<const float4*>(w32), T, d, E_pad, n_lg, partial);
+  else
+    e = launch_pdl(router_chain_kernel<false>, dim3(grid1), dim3(kChainWarps * 32), 0, stream, x, wg_packed,
+                   static_cast<const float4*>(nullptr), T, d, E_pad, n_lg, partial);
   if (e == cudaSuccess) e = cudaGetLastError();
-  return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_kernel launch");
+  if (e != cudaSuccess) return set_cuda_error(e, "router_chain_kernel launch");
+
+  // stage 2: selection per 32-token block (+ last-CTA scan and count exchange)
+  const int grid2 = (T + rt::kTokens - 1) / rt::kTokens;
+  size_t bc_bytes = blk_counts && batch_counts ? size_t(grid2) * E * 4 : 0;
+  const bool stage_counts = bc_bytes <= 200 * 1024;  // larger T: the last CTA scans from global memory
+  if (!stage_counts) bc_bytes = 0;
+  MP_TRY_R(ensure_max_dyn_smem(reinterpret_cast<const void*>(router_select_kernel), bc_bytes,
+                               "cudaFuncSetAttribute(router_select)"));
+  e = launch_pdl(router_select_kernel, dim3(grid2), dim3(256), bc_bytes, stream, static_cast<const float*>(partial),
+                 n_lg, E_pad, bias, T, E, has_gate ? 1 : 0, k, score_mode, renorm, idx, w, shared_gate, hist,
+                 blk_counts, batch_counts, ticket, blk_prefix, sync ? *sync : PeerSync(), stage_counts ? 1 : 0);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_select_kernel launch");
 }
 
 }  // namespace mp

@@ -132,18 +132,16 @@ def _run_router(x, wg, bias, E, k, mode, gate, w32=0):
 
 
 @pytest.mark.parametrize("w32", [0, 1], ids=["wg_bf16", "wg_f32"])
-@pytest.mark.parametrize("split", ["", "1", "2", "4", "8"])
-@pytest.mark.parametrize("variant", ["", "0", "1", "2", "3"])
-@pytest.mark.parametrize("E,k,mode,d", [(8, 2, 0, 512), (64, 6, 1, 256), (16, 4, 0, 4096)])
-def test_router_ties_go_to_the_lower_expert(E, k, mode, d, variant, split, w32, monkeypatch):
+@pytest.mark.parametrize("grid", ["", "1", "7", "148"])
+@pytest.mark.parametrize("E,k,mode,d", [(8, 2, 0, 512), (64, 6, 1, 256), (16, 4, 0, 4096), (60, 4, 1, 2048),
+                                        (8, 2, 0, 3072)])
+def test_router_ties_go_to_the_lower_expert(E, k, mode, d, grid, w32, monkeypatch):
     """Exact logit ties (duplicated router rows + biases, all-zero tokens whose logits are the
-    biases alone) resolve to the lower expert id, bit-exact with the oracle -- in every router
-    variant (8 or 16 warps, x from HBM or staged in smem; "" = the shape's default), with the
-    bf16 Wg operand and with the fp32 consumption-order operand the layer runs."""
-    if variant:
-        monkeypatch.setenv("MP_ROUTER_VARIANT", variant)
-    if split:  # passes split over a cluster of CTAs, logits gathered in the leader's smem
-        monkeypatch.setenv("MP_ROUTER_SPLIT", split)
+    biases alone) resolve to the lower expert id, bit-exact with the oracle -- for 1, 2 and 4
+    lane groups (d = 512 / 2048 / 4096), every chain-kernel grid ("" = the default; 1 CTA walks
+    every unit), with the bf16 Wg operand and the fp32 consumption-order operand the layer runs."""
+    if grid:
+        monkeypatch.setenv("MP_ROUTER_GRID", grid)
     T = 96
     x = orc.synthetic_tokens(0, T, d, seed=7)
     x[::3] = 0.0                       # every third token: logits == bias
