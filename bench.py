@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--stages", action="store_true", help="print the per-stage table on stderr")
     ap.add_argument("--layers", type=int, default=4, help="--scenario stack: MoE layers in the stack")
-    ap.add_argument("--scenario", default="steady", choices=["steady", "shift", "stack", "transport"],
+    ap.add_argument("--scenario", default="steady", choices=["steady", "shift", "stack", "transport", "calibrate"],
                     help="shift: BASELINE config 5, drifting routing + expert migration vs static placement")
     return ap.parse_args()
 
@@ -840,8 +840,15 @@ def main_shift(args):
     # remote penalty per token-unit: wire time of one remote invocation (activations out, results
     # back, comm_time's bandwidth term cost.py:148) at the measured peer bandwidth (probe copy below)
     bw_probe = measure_peer_copy(layer, world, rank) if world > 1 else 770e9
-    from paper_2508_12851_b200.calibrate import remote_penalty_seconds
-    penalty = remote_penalty_seconds(shape.d, bw_probe)
+    from paper_2508_12851_b200.calibrate import observed_remote_penalty, remote_penalty_seconds
+    # observed per-invocation penalty (sim.py:455-456, 469): the step-time difference of phase A
+    # and static phase B (same batch size, placement A) over their remote-invocation difference
+    penalty_analytic = remote_penalty_seconds(shape.d, bw_probe)
+    per_step = lambda tps: G * T / tps
+    penalty = observed_remote_penalty(per_step(tps_a), acc_a["remote_invocations"] / args.steps,
+                                      per_step(tps_b_static), acc_b_static["remote_invocations"] / args.steps)
+    if penalty <= 0.0:
+        penalty = penalty_analytic
     cluster = cluster_spec(shape, G, caps, link_bandwidth=bw_probe, load_bandwidth=bw_probe)
     from paper_2508_12851_b200.controller import MigrationController
     ctl = MigrationController(layer, cluster, model, pa, strategy="ours", seed=seed, mode="loads-only",
@@ -850,6 +857,8 @@ def main_shift(args):
     mig = {"decision": ledger["decision"], "cost_current_seconds": ledger["cost_current_seconds"],
            "cost_candidate_seconds": ledger["cost_candidate_seconds"],
            "migration_seconds_model": ledger["migration_seconds"], "penalty_seconds_per_token": penalty,
+           "penalty_source": "observed: (step_B_static - step_A) / (remote_B - remote_A) per step",
+           "penalty_analytic_2dbpe_over_bw": penalty_analytic,
            "peer_copy_GBps": bw_probe / 1e9}
     tps_b_mig, acc_b_mig = None, None
     if adopt:
@@ -1042,6 +1051,134 @@ def main_transport(args):
     layer.close()
 
 
+def measure_peer_latency(rank, world, reps: int = 200) -> float:
+    """Seconds per small (4 KB) copy to the next GPU over NVLink -- the link latency term of
+    comm_time (cost.py:139-149), measured with CUDA events on this rank's stream."""
+    import torch
+    import torch.distributed as dist
+    peer = (rank + 1) % world
+    src = torch.zeros(4096, dtype=torch.uint8, device=torch.cuda.current_device())
+    dst = torch.empty(4096, dtype=torch.uint8, device=torch.device("cuda", peer))
+    for _ in range(10):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        dst.copy_(src, non_blocking=True)
+    z.record()
+    torch.cuda.synchronize()
+    lat = torch.tensor([a.elapsed_time(z) * 1e-3 / reps], dtype=torch.float64, device=src.device)
+    dist.all_reduce(lat, op=dist.ReduceOp.MAX)
+    del dst
+    return float(lat.item())
+
+
+def main_calibrate(args):
+    """F1: measured-cost feedback into the reference's decision layer.  The analytic TimeModel
+    (cost.py:39-85: comp_base 2 ms, comp_per_token 50 us, link matrices) and the remote penalty of
+    CostSnapshot (cost.py:195-214, accumulated per remote invocation at sim.py:455-456, 469) get
+    their numbers from this box: a batch-size sweep of the expert GEMMs (K3 time vs routed rows per
+    GPU, least squares per GPU), the measured NVLink peer-copy bandwidth and small-copy latency, and
+    the observed penalty (step time of the same batch under the uniform vs the activation-aware
+    placement over their remote-invocation difference).  The reference's layer model
+    (`layer_latency`, cost.py:152-168) then predicts the measured forward."""
+    import numpy as np
+    from paper_2508_12851_b200 import calibrate as cal
+    from paper_2508_12851_b200.errors import import_moeplace
+    from paper_2508_12851_b200.routing import dispatch_accounting
+    from paper_2508_12851_b200.shapes import cluster_spec, model_spec
+    b = setup_bench_layer(args)
+    torch, dist, _lib = b.torch, b.dist, b._lib
+    layer, xs, out, stream, G, T, rank, dev, shape = b.layer, b.xs, b.out, b.stream, b.G, b.T, b.rank, b.dev, b.shape
+    mp = import_moeplace()
+    NS = _lib.NUM_STAGE_EVENTS
+
+    def run(Tn, steps):
+        """(mean step ms max over ranks, this GPU's mean K3 ms, rows this GPU computed, counts)"""
+        evs = []
+        for _ in range(steps):
+            row = [torch.cuda.Event(enable_timing=True) if j in (0, _lib.GEMM_START, _lib.GEMM_END,
+                                                                  _lib.MAIN_STAGE_EVENTS - 1) else None
+                   for j in range(NS)]
+            for ev in row:
+                if ev is not None:
+                    ev.record(stream)
+            evs.append(row)
+        for i in range(args.warmup):
+            layer.forward(xs[i % N_ROTATE][:Tn], out[:Tn])
+        torch.cuda.synchronize()
+        b.barrier()
+        for i in range(steps):
+            layer.forward(xs[i % N_ROTATE][:Tn], out[:Tn], events=evs[i])
+        torch.cuda.synchronize()
+        b.barrier()
+        layer.check()
+        step = float(np.median([e[0].elapsed_time(e[_lib.MAIN_STAGE_EVENTS - 1]) for e in evs]))
+        k3 = float(np.mean([e[_lib.GEMM_START].elapsed_time(e[_lib.GEMM_END]) for e in evs]))
+        st = torch.tensor([step], dtype=torch.float64, device=dev)
+        if G > 1:
+            dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        counts = layer.read_counts()
+        rows = int(sum(counts[s, e] for s in range(G) for e in range(shape.E) if layer.route[s, e] == rank))
+        return st.item(), k3, rows, counts
+
+    sweep = sorted({max(256, T // 8), max(256, T // 4), max(256, T // 2), T})
+    samples = []
+    for Tn in sweep:
+        step_ms, k3_ms, rows, counts = run(Tn, args.steps)
+        samples.append((rows, k3_ms * 1e-3))
+    allsamp = [None] * G
+    if G > 1:
+        dist.all_gather_object(allsamp, samples)
+    else:
+        allsamp = [samples]
+    step_ours, _, _, counts_ours = run(T, args.steps)
+    acc_ours = dispatch_accounting(counts_ours, layer.route, shape.d)
+    penalty, step_uni, acc_uni = None, None, None
+    bw, lat = 770e9, 3e-6
+    if G > 1:
+        bw = measure_peer_copy(layer, G, rank)
+        lat = measure_peer_latency(rank, G)
+        uni = uniform_sets(shape, G)
+        if all(len(uni[g]) <= layer.cap_slots for g in range(G)):
+            layer.set_placement_sets(uni, b.expert_src)
+            step_uni, _, _, counts_uni = run(T, args.steps)
+            acc_uni = dispatch_accounting(counts_uni, layer.route, shape.d)
+            penalty = cal.observed_remote_penalty(step_ours * 1e-3, acc_ours["remote_invocations"],
+                                                  step_uni * 1e-3, acc_uni["remote_invocations"])
+            layer.set_placement_sets(b.sets, b.expert_src)
+    pred = None
+    if rank == 0 and mp is not None:
+        cluster = cluster_spec(shape, G, b.caps, link_bandwidth=bw, link_latency=lat, load_bandwidth=bw)
+        model = model_spec(shape)
+        tm = cal.calibrated_time_model(cluster, allsamp, link_bandwidth=bw, link_latency=lat)
+        placement = mp.placement_from_server_sets([[s] for s in b.sets], cluster, model)
+        pred = cal.predicted_layer_latency(tm, placement, model, counts_ours, layer.route)
+        default_tm = mp.TimeModel.from_cluster(cluster)
+        pred_default = cal.predicted_layer_latency(default_tm, placement, model, counts_ours, layer.route)
+        line = {"scenario": "calibration (F1: measured TimeModel / CostSnapshot inputs)", "n_gpus": G,
+                "config": {"model": shape.name, "tokens_per_gpu": T, "sweep_tokens": sweep, "steps": args.steps},
+                "comp_fit": {"comp_base_s": tm.comp_base.tolist(), "comp_per_token_s": tm.comp_per_token.tolist(),
+                             "samples_rows_seconds": allsamp},
+                "link": {"peer_copy_GBps": bw / 1e9, "small_copy_latency_s": lat},
+                "penalty": {"observed_s_per_remote_invocation": penalty,
+                            "analytic_2dbpe_over_bw_s": cal.remote_penalty_seconds(shape.d, bw),
+                            "step_ms_ours": step_ours, "step_ms_uniform": step_uni,
+                            "remote_invocations_ours": acc_ours["remote_invocations"],
+                            "remote_invocations_uniform": acc_uni["remote_invocations"] if acc_uni else None},
+                "measured_step_ms": step_ours,
+                "predicted_calibrated": {k: (v * 1e3 if k.endswith("_s") else v) for k, v in pred.items()},
+                "predicted_reference_defaults": {k: (v * 1e3 if k.endswith("_s") else v)
+                                                 for k, v in pred_default.items()},
+                "units": "predicted_* latencies in ms (reference layer_latency, cost.py:152-168)"}
+        print(json.dumps(line), flush=True)
+    if G > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    layer.close()
+
+
 def measure_peer_copy(layer, world, rank):
     """NVLink pull bandwidth: copy one expert slot from the next GPU into a free staging slot."""
     import torch
@@ -1098,6 +1235,9 @@ if __name__ == "__main__":
         raise SystemExit(0)
     if a.scenario == "transport" and a.impl != "reference":
         main_transport(a)
+        raise SystemExit(0)
+    if a.scenario == "calibrate" and a.impl != "reference":
+        main_calibrate(a)
         raise SystemExit(0)
     if a.impl == "reference":
         # keep the whole --steps K run within minutes: clamp the sample size for the big shapes
