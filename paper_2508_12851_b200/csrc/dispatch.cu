@@ -16,6 +16,9 @@
 // of that source.  M[D][e] = sum_s [route[s][e]==D] * C[s][e].  The offsets are
 // recomputed where they are needed (permute CTAs, GEMM prologues) from the
 // exchanged count table -- there is no separate layout kernel.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "mp_internal.h"
 #include "peer_sync.cuh"
@@ -172,10 +175,13 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   if (G < 1 || G > 8 || E < 1 || E > 64) return set_error(MP_E_SHAPE, "permute: G=%d E=%d", G, E);
   if (T <= 0) return MP_OK;
   const int grid = (T + 31) / 32;
-  // small batches: split each block's row copies into column slices so that the
-  // grid reaches about one CTA per SM (the copies are bound by per-SM store rate)
+  // split each block's row copies into column slices until the grid holds about two CTAs
+  // per SM (they are small: 8 warps, no dynamic smem, so several are co-resident) -- the
+  // copies are bound by the memory-level parallelism of the warps in flight per SM
   int ny = 1;
-  while (ny < 16 && grid * ny * 2 <= kNumSMs && (d / 8) % (ny * 2) == 0 && (d / 8) / (ny * 2) >= 32) ny *= 2;
+  while (ny < 16 && grid * ny < 2 * kNumSMs && (d / 8) % (ny * 2) == 0 && (d / 8) / (ny * 2) >= 32) ny *= 2;
+  if (const char* env = getenv("MP_PERMUTE_SLICES")) ny = std::max(1, atoi(env));
+  if ((d / 8) % ny != 0) return set_error(MP_E_SHAPE, "permute: %d column slices do not divide d=%d", ny, d);
   const int vpl = ((d / 8) / ny + 31) / 32;
   PeerSync ps = sync ? *sync : PeerSync();
   if (ps.total > 0) ps.total = grid * ny;
