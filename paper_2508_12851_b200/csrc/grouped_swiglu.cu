@@ -673,7 +673,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
     if (ra != MP_OK) return ra;
     if (grid <= 0) grid = kNumSMs;
     grid &= ~1;
-    cudaError_t e = launch_pdl_if(pdl, grouped_gemm_2sm_kernel, dim3(grid), dim3(gg::kThreads), g2::kSmemBytes, stream, tmA,
+    cudaError_t e = launch_pdl_if(pdl && pdl_enabled(), grouped_gemm_2sm_kernel, dim3(grid), dim3(gg::kThreads), g2::kSmemBytes, stream, tmA,
                                tmB, gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src,
                                scatter_ptrs, ax, ps);
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -684,7 +684,7 @@ int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const Gr
                                      "cudaFuncSetAttribute(grouped_gemm)");
   if (ra != MP_OK) return ra;
   if (grid <= 0) grid = kNumSMs;
-  cudaError_t e = launch_pdl_if(pdl, grouped_gemm_kernel, dim3(grid), dim3(gg::kThreads), gg::kSmemBytes, stream, tmA, tmB,
+  cudaError_t e = launch_pdl_if(pdl && pdl_enabled(), grouped_gemm_kernel, dim3(grid), dim3(gg::kThreads), gg::kSmemBytes, stream, tmA, tmB,
                              gs, N, K, b_slot_stride, b_offset, out, out_ld, swiglu, scatter_src, scatter_ptrs, ps,
                              ax);
   if (e == cudaSuccess) e = cudaGetLastError();

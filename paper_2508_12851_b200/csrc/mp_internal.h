@@ -27,13 +27,13 @@ cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 bl
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                        Args&&... args) {
-  return launch_pdl_if(true, kernel, grid, block, smem, stream, static_cast<Args&&>(args)...);
+  return launch_pdl_if(pdl_enabled(), kernel, grid, block, smem, stream, static_cast<Args&&>(args)...);
 }
 
 // NVLink synchronisation folded into the layer's own kernels (G > 1).  Each

@@ -116,14 +116,16 @@ MP_DEV bool better(float a, int ia, float b, int ib) { return a > b || (a == b &
 // Warp-collective top-k + gate weights of one token from its logits (lane l holds
 // experts l and l + 32): k rounds of a warp arg-max (larger logit, ties -> lower
 // id), then softmax over the k (mode 0) or over all E (mode 1, optional
-// renormalisation).  Lane 0 writes idx_row / w_row and bumps cnt_s.
+// renormalisation).  Lane j < k writes idx_row[j] / w_row[j] and bumps cnt_s.
 MP_DEV void select_topk_store(float v0, float v1, int E, int k, int score_mode, int renorm, int32_t* idx_row,
                               float* w_row, int* cnt_s) {
   const int lane = lane_id();
   bool taken0 = lane >= E, taken1 = lane + 32 >= E;
-  float sel_v[rt::kMaxK];
-  int sel_i[rt::kMaxK];
-  for (int j = 0; j < k; ++j) {
+  float my_v = -INFINITY, mx = 0.f;  // lane j < k keeps the j-th selected logit and expert
+  int my_i = 0;
+#pragma unroll
+  for (int j = 0; j < rt::kMaxK; ++j) {
+    if (j >= k) break;
     float bv = -INFINITY;
     int bi = 0x7fffffff;
     if (!taken0) { bv = v0; bi = lane; }
@@ -134,35 +136,35 @@ MP_DEV void select_topk_store(float v0, float v1, int E, int k, int score_mode, 
       const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
       if (oi != 0x7fffffff && (bi == 0x7fffffff || better(ov, oi, bv, bi))) { bv = ov; bi = oi; }
     }
-    sel_v[j] = bv;
-    sel_i[j] = bi;
+    if (j == 0) mx = bv;  // every lane holds the arg-max after the xor butterfly
+    if (lane == j) { my_v = bv; my_i = bi; }
     if (bi == lane) taken0 = true;
     if (bi == lane + 32) taken1 = true;
   }
-  // weights
-  const float mx = sel_v[0];
+  // weights: lane j < k owns w_j
+  const float ej = lane < k ? expf(my_v - mx) : 0.f;
   float denom;
   if (score_mode == 0) {
-    denom = 0.f;
-    for (int j = 0; j < k; ++j) denom += expf(sel_v[j] - mx);
-  } else {
-    float s = (lane < E ? expf(v0 - mx) : 0.f) + (lane + 32 < E ? expf(v1 - mx) : 0.f);
+    denom = ej;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    denom = s;
+    for (int off = 16; off > 0; off >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, off);
+  } else {
+    float sum = (lane < E ? expf(v0 - mx) : 0.f) + (lane + 32 < E ? expf(v1 - mx) : 0.f);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    denom = sum;
   }
-  if (lane == 0) {
-    float wsum = 0.f;
-    float wj[rt::kMaxK];
-    for (int j = 0; j < k; ++j) {
-      wj[j] = expf(sel_v[j] - mx) / denom;
-      wsum += wj[j];
-    }
-    for (int j = 0; j < k; ++j) {
-      idx_row[j] = sel_i[j];
-      w_row[j] = (score_mode == 1 && renorm) ? wj[j] / wsum : wj[j];
-      atomicAdd(&cnt_s[sel_i[j]], 1);
-    }
+  float wj = ej / denom;
+  if (score_mode == 1 && renorm) {
+    float wsum = wj;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, off);
+    wj = wj / wsum;
+  }
+  if (lane < k) {
+    idx_row[lane] = my_i;
+    w_row[lane] = wj;
+    atomicAdd(&cnt_s[my_i], 1);
   }
 }
 
@@ -217,11 +219,16 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1)
       // fp32 pairs straight from the pre-converted Wg (two halves of 4 k each); the
       // step of this group's chain number s is the 256-k step g + n_lg * s
       const float4* w4 = w32 + (size_t(pass) * S_all + g) * 16 * 32 + lane;
+      uint4 xv[kTokPerWarp], xn[kTokPerWarp];
+#pragma unroll
+      for (int i = 0; i < kTokPerWarp; ++i) xv[i] = ld_nc_v4(xr[i]);
 #pragma unroll 1
       for (int s = 0; s < S; ++s, w4 += size_t(n_lg) * 16 * 32) {
-        uint4 xv[kTokPerWarp];
+        // the next step's x rows are in flight while this step's FFMA2 chains run
+        if (s + 1 < S) {
 #pragma unroll
-        for (int i = 0; i < kTokPerWarp; ++i) xv[i] = ld_nc_v4(xr[i] + size_t(256) * n_lg * s);
+          for (int i = 0; i < kTokPerWarp; ++i) xn[i] = ld_nc_v4(xr[i] + size_t(256) * n_lg * (s + 1));
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           float4 wv[8];
@@ -244,6 +251,8 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1)
               for (int i = 0; i < kTokPerWarp; ++i) ffma2(acc[i][j], xs[i], w2[j]);
           }
         }
+#pragma unroll
+        for (int i = 0; i < kTokPerWarp; ++i) xv[i] = xn[i];
       }
     } else {
       const __nv_bfloat16* wr = wp + size_t(kExpPerPass) * pass * d + 256 * g + 8 * lane;
@@ -300,10 +309,23 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1)
 }
 
 // Stage 2 (selection).  CTA = one router block of 32 tokens (the histogram / permute
-// block), 8 warps: logits = the lane groups' partials combined by the contract's tree
-// (q[g] += q[g + o], o = n_lg/2..1) + bias; then top-k, gate weights, block-aggregated
-// histogram, and -- in the last CTA -- the batch counts, the block prefix and (G > 1) the
-// count exchange with epoch A.
+// block), 8 warps, one warp per token (4 each): lane l reads the partials of experts l
+// and l + 32 straight from L2 (all of a warp's loads issued before any is used),
+// combines them by the contract's tree (q[g] += q[g + o], o = n_lg/2..1) + bias, then
+// top-k, gate weights and the block-aggregated histogram; the last CTA produces the
+// batch counts, the block prefix and (G > 1) the count exchange with epoch A.
+MP_DEV float combine_groups(const float* pp, size_t gs, int n_lg) {
+  // pp: the partial of (token, expert) in group 0; gs: stride between groups
+  float v = __ldcg(pp);
+  if (n_lg == 2) {
+    v = v + __ldcg(pp + gs);
+  } else if (n_lg == 4) {  // q[g] += q[g + 2], then q[0] += q[1]
+    const float a1 = __ldcg(pp + gs), a2 = __ldcg(pp + 2 * gs), a3 = __ldcg(pp + 3 * gs);
+    v = (v + a2) + (a1 + a3);
+  }
+  return v;
+}
+
 __global__ void __launch_bounds__(256)
     router_select_kernel(const float* __restrict__ partial, int n_lg, int E_pad, const float* __restrict__ bias,
                          int T, int E, int has_gate, int k, int score_mode, int renorm, int32_t* __restrict__ idx,
@@ -311,46 +333,40 @@ __global__ void __launch_bounds__(256)
                          int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
                          uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix, const PeerSync sync,
                          int stage_counts) {
-  __shared__ float logits[rt::kTokens][rt::kMaxE + 9];
   __shared__ int cnt_s[rt::kMaxE];
   extern __shared__ __align__(128) uint8_t dsm[];  // last CTA: the [nb][E] block counts
   int* bc = reinterpret_cast<int*>(dsm);
-  const int E_tot = E + has_gate;
   const int blk = blockIdx.x, n_blk = gridDim.x;
   const int t0 = blk * rt::kTokens;
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
   for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
+  const float bz0 = (bias != nullptr && lane < E) ? bias[lane] : 0.f;
+  const float bz1 = (bias != nullptr && lane + 32 < E) ? bias[lane + 32] : 0.f;
   griddep_launch_dependents();
-  griddep_wait();
-  for (int i = tid; i < rt::kTokens * E_tot; i += blockDim.x) {
-    const int tt = i / E_tot, e = i - tt * E_tot, t = t0 + tt;
-    if (t >= T) continue;
-    const float* pp = partial + size_t(t) * E_pad + e;
-    const size_t gs = size_t(T) * E_pad;  // stride between lane groups
-    float val = __ldcg(pp);
-    if (n_lg == 2) {
-      val = val + __ldcg(pp + gs);
-    } else if (n_lg == 4) {  // q[g] += q[g + 2], then q[0] += q[1]
-      val = (val + __ldcg(pp + 2 * gs)) + (__ldcg(pp + gs) + __ldcg(pp + 3 * gs));
-    }
-    if (bias != nullptr && e < E) val = __fadd_rn(val, bias[e]);
-    logits[tt][e] = val;
-  }
+  griddep_wait();  // the chain kernel's partials
   __syncthreads();
 
-  // ---- top-k + weights: one warp per token
-  for (int tt = warp; tt < rt::kTokens; tt += blockDim.x / 32) {
-    const int t = t0 + tt;
+  // ---- logits, top-k + weights: one warp per token
+  const size_t gs = size_t(T) * E_pad;
+  constexpr int kPerWarp = rt::kTokens / 8;
+  float v0[kPerWarp], v1[kPerWarp], gl[kPerWarp];
+#pragma unroll
+  for (int i = 0; i < kPerWarp; ++i) {
+    const int t = min(t0 + warp + 8 * i, T - 1);
+    const float* pp = partial + size_t(t) * E_pad;
+    v0[i] = lane < E ? combine_groups(pp + lane, gs, n_lg) : -INFINITY;
+    v1[i] = lane + 32 < E ? combine_groups(pp + lane + 32, gs, n_lg) : -INFINITY;
+    gl[i] = has_gate ? combine_groups(pp + E, gs, n_lg) : 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < kPerWarp; ++i) {
+    const int t = t0 + warp + 8 * i;
     if (t >= T) break;
-    const float v0 = lane < E ? logits[tt][lane] : -INFINITY;
-    const float v1 = lane + 32 < E ? logits[tt][lane + 32] : -INFINITY;
-    select_topk_store(v0, v1, E, k, score_mode, renorm, idx + size_t(t) * k, wout + size_t(t) * k, cnt_s);
-    if (lane == 0) {
-      if (has_gate && shared_gate != nullptr) {
-        const float g = logits[tt][E];
-        shared_gate[t] = 1.0f / (1.0f + expf(-g));
-      }
-    }
+    const float a = lane < E ? __fadd_rn(v0[i], bz0) : -INFINITY;
+    const float c = lane + 32 < E ? __fadd_rn(v1[i], bz1) : -INFINITY;
+    select_topk_store(bias != nullptr ? a : v0[i], bias != nullptr ? c : v1[i], E, k, score_mode, renorm,
+                      idx + size_t(t) * k, wout + size_t(t) * k, cnt_s);
+    if (lane == 0 && has_gate && shared_gate != nullptr) shared_gate[t] = 1.0f / (1.0f + expf(-gl[i]));
   }
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) {
@@ -531,9 +547,16 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   if (!stage_counts) bc_bytes = 0;
   MP_TRY_R(ensure_max_dyn_smem(reinterpret_cast<const void*>(router_select_kernel), bc_bytes,
                                "cudaFuncSetAttribute(router_select)"));
-  e = launch_pdl(router_select_kernel, dim3(grid2), dim3(256), bc_bytes, stream, static_cast<const float*>(partial),
-                 n_lg, E_pad, bias, T, E, has_gate ? 1 : 0, k, score_mode, renorm, idx, w, shared_gate, hist,
-                 blk_counts, batch_counts, ticket, blk_prefix, sync ? *sync : PeerSync(), stage_counts ? 1 : 0);
+  // programmatic dependent launch: the selection grid is scheduled while the chains drain
+  // (its griddepcontrol.wait still orders every partial before use); MP_ROUTER_PDL=0 disables
+  static const bool sel_pdl = [] {
+    const char* env = getenv("MP_ROUTER_PDL");
+    return env == nullptr || atoi(env) != 0;
+  }();
+  e = launch_pdl_if(sel_pdl || pdl_enabled(), router_select_kernel, dim3(grid2), dim3(256), bc_bytes, stream,
+                    static_cast<const float*>(partial), n_lg, E_pad, bias, T, E, has_gate ? 1 : 0, k, score_mode,
+                    renorm, idx, w, shared_gate, hist, blk_counts, batch_counts, ticket, blk_prefix,
+                    sync ? *sync : PeerSync(), stage_counts ? 1 : 0);
   if (e == cudaSuccess) e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_select_kernel launch");
 }
