@@ -158,6 +158,16 @@ namespace {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// The router's fp32 consumption-order operand runs the quad chain kernel; the default is the
+// octet kernel over the bf16 rows (MP_ROUTER_CHAIN=4 selects the quad kernel with fp32 Wg).
+const float* router_w32(const mp_layer* L) {
+  static const bool quad = [] {
+    const char* env = getenv("MP_ROUTER_CHAIN");
+    return env != nullptr && atoi(env) == 4;
+  }();
+  return quad ? L->wg32 : nullptr;
+}
+
 struct Carver {
   uint8_t* base;
   size_t off = 0;
@@ -787,7 +797,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   if (T > 0) {
     MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
                          D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
-                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr, L->wg32, L->partial));
+                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr, router_w32(L), L->partial));
     ++launches;
   } else if (G > 1) {
     // no router / permute on this origin: publish zero counts, raise A and B
@@ -866,7 +876,7 @@ int mp_layer_route(mp_layer* L, const void* x, int T, void* stream) {
   }
   return launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, D.E, D.shared_gate,
                        D.top_k, D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts,
-                       L->batch_counts, L->ticket, L->blk_prefix, st, nullptr, L->wg32, L->partial);
+                       L->batch_counts, L->ticket, L->blk_prefix, st, nullptr, router_w32(L), L->partial);
 }
 
 int mp_layer_permute(mp_layer* L, const void* x, int T, const int32_t* counts_all, void* staging, void* stream) {

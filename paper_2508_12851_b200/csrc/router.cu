@@ -123,9 +123,8 @@ MP_DEV void select_topk_store(float v0, float v1, int E, int k, int score_mode, 
   bool taken0 = lane >= E, taken1 = lane + 32 >= E;
   float my_v = -INFINITY, mx = 0.f;  // lane j < k keeps the j-th selected logit and expert
   int my_i = 0;
-#pragma unroll
-  for (int j = 0; j < rt::kMaxK; ++j) {
-    if (j >= k) break;
+#pragma unroll 1
+  for (int j = 0; j < k; ++j) {  // (rolled: the unrolled rounds blew the kernel past the i-cache)
     float bv = -INFINITY;
     int bi = 0x7fffffff;
     if (!taken0) { bv = v0; bi = lane; }
@@ -308,6 +307,94 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1)
   }
 }
 
+// Stage 1, octet form (the layer's default).  Unit = (expert pass p, lane group g, token
+// octet o): one warp keeps 8 tokens x 8 experts = 32 FFMA2 accumulator pairs per lane, so
+// every Wg value a lane loads feeds 8 tokens -- half the L1 traffic per FMA of the quad form,
+// whose 16 float4 Wg loads per 128 FFMA2 kept the L1 the bottleneck.  Wg comes as bf16 rows
+// [E_pad][d] (one uint4 = 8 k of one expert per lane and step); the pair (e, e + 1) at one k
+// is two ALU ops.  Same chains, same butterfly, same partial layout as the quad form.
+constexpr int kOctTok = 8;
+// kWarps = 12: 12 x 32 threads x <= 168 registers fill the register file (some spills);
+// kWarps = 8: up to 255 registers, no spills, fewer warps to hide latency
+template <int kWarps>
+__global__ void __launch_bounds__(kWarps * 32, 1)
+    router_chain8_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wp, int T, int d,
+                         int E_pad, int n_lg, float* __restrict__ partial) {
+  griddep_launch_dependents();
+  griddep_wait();
+  const int lane = lane_id();
+  const int n_oct = (T + kOctTok - 1) / kOctTok;
+  const int n_pass = E_pad / kExpPerPass;
+  const int S = d / 256 / n_lg;
+  const int n_units = n_oct * n_pass * n_lg;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp_id();
+  const int n_warps = gridDim.x * (blockDim.x >> 5);
+  for (int u = gw; u < n_units; u += n_warps) {
+    const int o = u % n_oct, pg = u / n_oct;
+    const int g = pg % n_lg, pass = pg / n_lg;
+    const int t0 = o * kOctTok;
+    const __nv_bfloat16* xr = x + 256 * g + 8 * lane;
+    uint32_t rows[kOctTok];  // element offsets of the octet's rows (rows past T: row 0, discarded)
+#pragma unroll
+    for (int i = 0; i < kOctTok; ++i) rows[i] = uint32_t(t0 + i < T ? t0 + i : 0) * uint32_t(d);
+    const __nv_bfloat16* wr = wp + size_t(kExpPerPass) * pass * d + 256 * g + 8 * lane;
+    unsigned long long acc[kOctTok][kExpPerPass / 2];
+#pragma unroll
+    for (int i = 0; i < kOctTok; ++i)
+#pragma unroll
+      for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
+#pragma unroll 1
+    for (int s = 0; s < S; ++s) {
+      const size_t ko = size_t(256) * n_lg * s;
+      uint4 xv[kOctTok], wv[kExpPerPass];
+#pragma unroll
+      for (int j = 0; j < kExpPerPass; ++j) wv[j] = __ldg(reinterpret_cast<const uint4*>(wr + size_t(j) * d + ko));
+#pragma unroll
+      for (int i = 0; i < kOctTok; ++i) xv[i] = ld_nc_v4(xr + rows[i] + ko);
+#pragma unroll
+      for (int qk = 0; qk < 8; ++qk) {  // strictly ascending k inside the lane's slice
+        unsigned long long w2[kExpPerPass / 2];
+#pragma unroll
+        for (int j = 0; j < kExpPerPass / 2; ++j) {
+          const uint32_t u0 = (&wv[2 * j].x)[qk >> 1], u1 = (&wv[2 * j + 1].x)[qk >> 1];
+          w2[j] = (qk & 1) ? pack2(bf16_hi(u0), bf16_hi(u1)) : pack2(bf16_lo(u0), bf16_lo(u1));
+        }
+#pragma unroll
+        for (int i = 0; i < kOctTok; ++i) {
+          const uint32_t uu = (&xv[i].x)[qk >> 1];
+          const float xs = (qk & 1) ? bf16_hi(uu) : bf16_lo(uu);
+#pragma unroll
+          for (int j = 0; j < kExpPerPass / 2; ++j) ffma2(acc[i][j], xs, w2[j]);
+        }
+      }
+    }
+    // two butterfly reduce-scatters (tokens 0-3 and 4-7), as in the quad form
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < kExpPerPass / 2; ++j) {
+          v[i * 8 + 2 * j] = __uint_as_float(uint32_t(acc[4 * h + i][j]));
+          v[i * 8 + 2 * j + 1] = __uint_as_float(uint32_t(acc[4 * h + i][j] >> 32));
+        }
+#pragma unroll
+      for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+          const float send = upper ? v[i] : v[i + n / 2];
+          const float keep = upper ? v[i + n / 2] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+      }
+      const int tt = t0 + 4 * h + (lane >> 3);
+      if (tt < T) partial[(size_t(g) * T + tt) * E_pad + kExpPerPass * pass + (lane & 7)] = v[0];
+    }
+  }
+}
+
 // Stage 2 (selection).  CTA = one router block of 32 tokens (the histogram / permute
 // block), 8 warps, one warp per token (4 each): lane l reads the partials of experts l
 // and l + 32 straight from L2 (all of a warp's loads issued before any is used),
@@ -348,25 +435,27 @@ __global__ void __launch_bounds__(256)
 
   // ---- logits, top-k + weights: one warp per token
   const size_t gs = size_t(T) * E_pad;
-  constexpr int kPerWarp = rt::kTokens / 8;
-  float v0[kPerWarp], v1[kPerWarp], gl[kPerWarp];
-#pragma unroll
-  for (int i = 0; i < kPerWarp; ++i) {
-    const int t = min(t0 + warp + 8 * i, T - 1);
-    const float* pp = partial + size_t(t) * E_pad;
-    v0[i] = lane < E ? combine_groups(pp + lane, gs, n_lg) : -INFINITY;
-    v1[i] = lane + 32 < E ? combine_groups(pp + lane + 32, gs, n_lg) : -INFINITY;
-    gl[i] = has_gate ? combine_groups(pp + E, gs, n_lg) : 0.f;
-  }
-#pragma unroll
-  for (int i = 0; i < kPerWarp; ++i) {
-    const int t = t0 + warp + 8 * i;
+  auto load = [&](int t, float& a0, float& a1, float& ag) {
+    const float* pp = partial + size_t(min(t, T - 1)) * E_pad;
+    a0 = lane < E ? combine_groups(pp + lane, gs, n_lg) : -INFINITY;
+    a1 = lane + 32 < E ? combine_groups(pp + lane + 32, gs, n_lg) : -INFINITY;
+    ag = has_gate ? combine_groups(pp + E, gs, n_lg) : 0.f;
+  };
+  float c0, c1, cg;
+  load(t0 + warp, c0, c1, cg);
+#pragma unroll 1
+  for (int tt = warp; tt < rt::kTokens; tt += 8) {
+    const int t = t0 + tt;
     if (t >= T) break;
-    const float a = lane < E ? __fadd_rn(v0[i], bz0) : -INFINITY;
-    const float c = lane + 32 < E ? __fadd_rn(v1[i], bz1) : -INFINITY;
-    select_topk_store(bias != nullptr ? a : v0[i], bias != nullptr ? c : v1[i], E, k, score_mode, renorm,
-                      idx + size_t(t) * k, wout + size_t(t) * k, cnt_s);
-    if (lane == 0 && has_gate && shared_gate != nullptr) shared_gate[t] = 1.0f / (1.0f + expf(-gl[i]));
+    float n0, n1, ng;  // the next token's partials are in flight during this token's selection
+    load(t + 8, n0, n1, ng);
+    const float a = (lane < E && bias != nullptr) ? __fadd_rn(c0, bz0) : c0;
+    const float c = (lane + 32 < E && bias != nullptr) ? __fadd_rn(c1, bz1) : c1;
+    select_topk_store(a, c, E, k, score_mode, renorm, idx + size_t(t) * k, wout + size_t(t) * k, cnt_s);
+    if (lane == 0 && has_gate && shared_gate != nullptr) shared_gate[t] = 1.0f / (1.0f + expf(-cg));
+    c0 = n0;
+    c1 = n1;
+    cg = ng;
   }
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) {
@@ -530,13 +619,32 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   const int n_units = ((T + kTokPerWarp - 1) / kTokPerWarp) * (E_pad / kExpPerPass) * n_lg;
   int grid1 = std::min(kNumSMs, (n_units + kChainWarps - 1) / kChainWarps);
   if (const char* ge = getenv("MP_ROUTER_GRID")) grid1 = std::max(1, atoi(ge));
+  // the octet form over the bf16 rows is the default; an fp32 operand runs the quad form
+  // (MP_ROUTER_CHAIN=4 also runs the quad form over the bf16 rows)
+  const char* chain_env = getenv("MP_ROUTER_CHAIN");
+  const int chain = use32 ? 4 : (chain_env ? atoi(chain_env) : 8);
   cudaError_t e;
-  if (use32)
+  if (chain == 8) {
+    static const int oct_warps = [] {
+      const char* env = getenv("MP_ROUTER_OCT_WARPS");
+      return env != nullptr && atoi(env) == 12 ? 12 : 8;
+    }();
+    const int n_units8 = ((T + kOctTok - 1) / kOctTok) * (E_pad / kExpPerPass) * n_lg;
+    int grid8 = std::min(kNumSMs, (n_units8 + oct_warps - 1) / oct_warps);
+    if (const char* ge = getenv("MP_ROUTER_GRID")) grid8 = std::max(1, atoi(ge));
+    if (oct_warps == 12)
+      e = launch_pdl(router_chain8_kernel<12>, dim3(grid8), dim3(12 * 32), 0, stream, x, wg_packed, T, d, E_pad,
+                     n_lg, partial);
+    else
+      e = launch_pdl(router_chain8_kernel<8>, dim3(grid8), dim3(8 * 32), 0, stream, x, wg_packed, T, d, E_pad,
+                     n_lg, partial);
+  } else if (use32) {
     e = launch_pdl(router_chain_kernel<true>, dim3(grid1), dim3(kChainWarps * 32), 0, stream, x, wg_packed,
                    reinterpret_cast<const float4*>(w32), T, d, E_pad, n_lg, partial);
-  else
+  } else {
     e = launch_pdl(router_chain_kernel<false>, dim3(grid1), dim3(kChainWarps * 32), 0, stream, x, wg_packed,
                    static_cast<const float4*>(nullptr), T, d, E_pad, n_lg, partial);
+  }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return set_cuda_error(e, "router_chain_kernel launch");
 

@@ -272,10 +272,11 @@ class B200MoELayer:
         counts = self.gathered_counts(group).astype(float)
         return mp.ActivationStats.from_counts(counts[:, None, :], (self.shape.E,))
 
-    def trace_records(self, T: int, layer: int = 0, t: float = 0.0) -> list[dict]:
-        """The last forward's routing of this origin as reference trace records (cli.py:91-135)."""
+    def trace_records(self, T: int, layer: int = 0, t: float = 0.0, server: int | None = None) -> list[dict]:
+        """The last forward's routing of this origin as reference trace records (cli.py:91-135);
+        server defaults to this GPU's rank."""
         from .trace import trace_records
-        return trace_records(self.idx[:T].cpu().numpy(), self.rank, layer, t)
+        return trace_records(self.idx[:T].cpu().numpy(), self.rank if server is None else server, layer, t)
 
     def reset_counts(self) -> None:
         self.hist.zero_()
@@ -398,11 +399,14 @@ class HostPipeline:
         self.ev_out = [torch.cuda.Event() for _ in range(depth)]
         self.n = 0
 
-    def submit(self, x_host: torch.Tensor, out_host: torch.Tensor) -> None:
-        """Enqueue one batch: x_host [T, d] pinned bf16 -> layer -> out_host [T, d] pinned bf16."""
+    def submit(self, x_host: torch.Tensor, out_host: torch.Tensor, start_event=None) -> None:
+        """Enqueue one batch: x_host [T, d] pinned bf16 -> layer -> out_host [T, d] pinned bf16.
+        start_event: recorded on the copy-in stream right before this batch's copy starts."""
         b = self.n % self.depth
         if self.n >= self.depth:
             self.s_in.wait_event(self.ev_comp[b])      # xd[b] free once batch n-depth left the layer
+        if start_event is not None:
+            start_event.record(self.s_in)
         with torch.cuda.stream(self.s_in):
             self.xd[b].copy_(x_host, non_blocking=True)
             self.ev_in[b].record(self.s_in)

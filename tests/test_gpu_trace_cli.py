@@ -47,7 +47,7 @@ def test_gpu_trace_through_moeplace_place(tmp_path):
         layer.forward(torch.from_numpy(orc.synthetic_tokens(s, T, shape.d, seed)).cuda().bfloat16())
         torch.cuda.synchronize()
         counts[s] = layer.activation_counts()
-        write_trace(str(trace), layer.trace_records(T, layer=0, t=float(s)), append=s > 0)
+        write_trace(str(trace), layer.trace_records(T, layer=0, t=float(s), server=s), append=s > 0)
 
     m_e = shape.expert_bytes
     cluster = {"servers": [{"gpus": [{"memory": 4 * m_e, "load_bandwidth": 770e9}]} for _ in range(S)],
