@@ -496,6 +496,8 @@ def main_b200(args):
     # epilogue, so its rate is bounded by the GEMM, reported as bytes / GEMM2 time
     nvl_peak = 770.0
     k4 = None
+    peer_bw = measure_peer_copy(layer, G, rank) / 1e9 if G > 1 else None
+    peer_lat = measure_peer_latency(layer, rank, G) if G > 1 else None
     if G > 1:
         row_b = shape.d * 2
         disp = [r[0] * row_b / (r[2] * 1e-3) / 1e9 if r[2] > 0 else 0.0 for r in k4_rank]
@@ -505,6 +507,7 @@ def main_b200(args):
               "dispatch_GBps_per_gpu": disp, "return_GBps_per_gpu": retr,
               "dispatch_frac_of_peer_copy": max(disp) / nvl_peak, "peak_GBps": nvl_peak,
               "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+              "peer_copy_GBps_this_box": peer_bw, "small_copy_latency_s_this_box": peer_lat,
               "note": "dispatch = outgoing rows / permute kernel time (the kernel also writes the local rows); "
                       "return = rows sent back / GEMM2 time (the stores ride the GEMM epilogue)"}
     rows_list = [r for r, _ in per_rank]
@@ -1053,27 +1056,17 @@ def main_transport(args):
     layer.close()
 
 
-def measure_peer_latency(rank, world, reps: int = 200) -> float:
-    """Seconds per small (4 KB) copy to the next GPU over NVLink -- the link latency term of
-    comm_time (cost.py:139-149), measured with CUDA events on this rank's stream."""
+def measure_peer_latency(layer, rank, world, reps: int = 200) -> float:
+    """Seconds per small (4 KB) NVLink copy from the next GPU's window (mp_layer_peer_probe) --
+    the link latency term of comm_time (cost.py:139-149); max over ranks."""
     import torch
     import torch.distributed as dist
-    peer = (rank + 1) % world
-    src = torch.zeros(4096, dtype=torch.uint8, device=torch.cuda.current_device())
-    dst = torch.empty(4096, dtype=torch.uint8, device=torch.device("cuda", peer))
-    for _ in range(10):
-        dst.copy_(src, non_blocking=True)
-    torch.cuda.synchronize()
-    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(reps):
-        dst.copy_(src, non_blocking=True)
-    z.record()
-    torch.cuda.synchronize()
-    lat = torch.tensor([a.elapsed_time(z) * 1e-3 / reps], dtype=torch.float64, device=src.device)
-    dist.all_reduce(lat, op=dist.ReduceOp.MAX)
-    del dst
-    return float(lat.item())
+    dist.barrier()
+    lat = layer.peer_probe((rank + 1) % world, 4096, reps)
+    t = torch.tensor([lat], dtype=torch.float64, device=layer.device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    return float(t.item())
 
 
 def main_calibrate(args):
@@ -1141,7 +1134,7 @@ def main_calibrate(args):
     bw, lat = 770e9, 3e-6
     if G > 1:
         bw = measure_peer_copy(layer, G, rank)
-        lat = measure_peer_latency(rank, G)
+        lat = measure_peer_latency(layer, rank, G)
         uni = uniform_sets(shape, G)
         if all(len(uni[g]) <= layer.cap_slots for g in range(G)):
             layer.set_placement_sets(uni, b.expert_src)
@@ -1182,47 +1175,18 @@ def main_calibrate(args):
 
 
 def measure_peer_copy(layer, world, rank):
-    """NVLink pull bandwidth: copy one expert slot from the next GPU into a free staging slot."""
+    """NVLink pull bandwidth from the next GPU's window (mp_layer_peer_probe, up to 64 MiB per
+    copy); min over ranks."""
     import torch
     import torch.distributed as dist
-    peer = (rank + 1) % world
-    slot_maps = [None] * world
-    dist.all_gather_object(slot_maps, layer.slot_of.tolist())
-    src_slot = next(s for s in slot_maps[peer] if s >= 0)
-    dst_slot = layer._free[-1]
-    from paper_2508_12851_b200 import _lib
-    import ctypes
-    ops = (_lib.CopyOp * 1)(_lib.CopyOp(peer, int(src_slot), int(dst_slot)))
-    st = torch.cuda.current_stream()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(2):
-        _lib.check(layer.lib.mp_layer_migrate(layer._h, ops, 1, ctypes.c_void_p(st.cuda_stream), None))
-    a.record(st)
-    reps = 5
-    for _ in range(reps):
-        _lib.check(layer.lib.mp_layer_migrate(layer._h, ops, 1, ctypes.c_void_p(st.cuda_stream), None))
-    b.record(st)
-    torch.cuda.synchronize()
-    sec = a.elapsed_time(b) * 1e-3 / reps
-    bw = torch.tensor([layer.shape.expert_bytes / sec], dtype=torch.float64, device=layer.device)
+    dist.barrier()
+    cap = int(layer._ptrs.recv_cap) * layer.shape.d * 2
+    nbytes = min(cap, 64 << 20)
+    sec = layer.peer_probe((rank + 1) % world, nbytes, 5)
+    bw = torch.tensor([nbytes / sec], dtype=torch.float64, device=layer.device)
     dist.all_reduce(bw, op=dist.ReduceOp.MIN)
     dist.barrier()
     return float(bw.item())
-
-
-def self_launch(args) -> int:
-    """`python bench.py --gpus N` without a torchrun environment: re-exec this script under
-    torch.distributed.run with one process per GPU (127.0.0.1 rendezvous); rank 0's single JSON
-    line comes through on stdout."""
-    import socket
-    sock = socket.socket()
-    sock.bind(("127.0.0.1", 0))
-    port = sock.getsockname()[1]
-    sock.close()
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
-    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
-    return subprocess.run(cmd, env=env).returncode
 
 
 if __name__ == "__main__":

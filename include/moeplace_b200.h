@@ -248,6 +248,14 @@ typedef struct mp_copy_op {
 } mp_copy_op;
 int mp_layer_migrate(mp_layer* layer, const mp_copy_op* ops, int n_ops, void* stream, void* done_event);
 
+/* Link probe for the measured-cost inputs of the reference's TimeModel (comm_time,
+ * cost.py:139-149) and migration_cost's load bandwidth (cost.py:171-191): `reps`
+ * back-to-back copies of `bytes` from peer's receive region into ours over the
+ * NVLink mapping, timed with CUDA events on `stream` (synchronises).  Small sizes
+ * give the per-transfer latency, large sizes the bandwidth.  Overwrites the
+ * receive region (call between forwards). */
+int mp_layer_peer_probe(mp_layer* layer, int peer, int64_t bytes, int reps, void* stream, float* ms_per_copy);
+
 #ifdef __cplusplus
 }
 #endif

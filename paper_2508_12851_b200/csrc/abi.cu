@@ -970,6 +970,38 @@ int mp_layer_check(mp_layer* L, void* stream) {
   return MP_OK;
 }
 
+int mp_layer_peer_probe(mp_layer* L, int peer, int64_t bytes, int reps, void* stream, float* ms_per_copy) {
+  if (!L || !ms_per_copy) return set_error(MP_E_ARG, "mp_layer_peer_probe: null pointer");
+  if (peer < 0 || peer >= L->G || peer == L->rank) return set_error(MP_E_ARG, "mp_layer_peer_probe: peer %d", peer);
+  if (!L->peer_window[peer]) return set_error(MP_E_PEER, "mp_layer_peer_probe: peer %d not opened", peer);
+  const int64_t cap = int64_t(L->off_ret - L->off_recv);  // the receive region of both windows
+  if (bytes <= 0 || bytes > cap || reps < 1) return set_error(MP_E_ARG, "mp_layer_peer_probe: %lld bytes x %d",
+                                                              (long long)bytes, reps);
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaEvent_t a, b;
+  MP_CUDA(cudaEventCreate(&a));
+  MP_CUDA(cudaEventCreate(&b));
+  // the peer's receive region -> ours, over the NVLink mapping opened by mp_layer_open_peers
+  const uint8_t* src = L->peer_window[peer] + L->off_recv;
+  uint8_t* dst = L->window + L->off_recv;
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaEventRecord(a, st);
+  for (int i = 0; i < reps && e == cudaSuccess; ++i)
+    e = cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaEventRecord(b, st);
+  if (e == cudaSuccess) e = cudaEventSynchronize(b);
+  float ms = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (e != cudaSuccess) return set_cuda_error(e, "mp_layer_peer_probe");
+  *ms_per_copy = ms / float(reps);
+  return MP_OK;
+}
+
 int mp_layer_migrate(mp_layer* L, const mp_copy_op* ops, int n_ops, void* stream, void* done_event) {
   if (!L || (n_ops > 0 && !ops)) return set_error(MP_E_ARG, "mp_layer_migrate: null pointer");
   DeviceGuard dg(L->desc.device);

@@ -244,6 +244,14 @@ class B200MoELayer:
         """Execution plan the C ABI chose for this layer (mp_layer_config)."""
         return {k: int(self.lib.mp_layer_config(self._h, v)) for k, v in _lib.CFG_KEYS.items()}
 
+    def peer_probe(self, peer: int, nbytes: int, reps: int = 20) -> float:
+        """Seconds per `nbytes` copy from `peer` over NVLink (mp_layer_peer_probe; overwrites the
+        receive buffer -- call between forwards)."""
+        ms = ctypes.c_float()
+        _lib.check(self.lib.mp_layer_peer_probe(self._h, peer, int(nbytes), reps, self._stream(), byref(ms)),
+                   "mp_layer_peer_probe")
+        return ms.value * 1e-3
+
     def check(self) -> None:
         _lib.check(self.lib.mp_layer_check(self._h, self._stream()), "mp_layer_check")
 
