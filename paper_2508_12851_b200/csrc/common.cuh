@@ -263,6 +263,14 @@ MP_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;
 constexpr uint64_t kPeerTimeoutNs = 30ull * 1000ull * 1000ull * 1000ull;
 
 // 16-byte streaming load / store.
+// 16-byte asynchronous global -> shared copy (L2 only), grouped per thread.
+MP_DEV void cp_async_16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+MP_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+MP_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 MP_DEV uint4 ld_nc_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"

@@ -309,48 +309,80 @@ __global__ void __launch_bounds__(kChainWarps * 32, 1)
 
 // Stage 1, octet form (the layer's default).  Unit = (expert pass p, lane group g, token
 // octet o): one warp keeps 8 tokens x 8 experts = 32 FFMA2 accumulator pairs per lane, so
-// every Wg value a lane loads feeds 8 tokens -- half the L1 traffic per FMA of the quad form,
-// whose 16 float4 Wg loads per 128 FFMA2 kept the L1 the bottleneck.  Wg comes as bf16 rows
-// [E_pad][d] (one uint4 = 8 k of one expert per lane and step); the pair (e, e + 1) at one k
-// is two ALU ops.  Same chains, same butterfly, same partial layout as the quad form.
+// every Wg value a lane loads feeds 8 tokens (half the L1 traffic per FMA of the quad form).
+// Wg comes as bf16 rows [E_pad][d] (one uint4 = 8 k of one expert per lane and step); the
+// pair (e, e + 1) at one k is two ALU ops.  With one warp's 32 x 8 accumulators the register
+// file holds only 8 warps per SM, too few to hide load latency, so every lane streams its own
+// operands (8 x rows + 8 Wg rows, 16 B each per step) through a kStages-deep shared-memory
+// ring with cp.async, running ahead across unit boundaries -- a lane only ever reads back the
+// bytes it copied itself, so no warp or CTA synchronisation is involved.  Same chains, same
+// butterfly, same partial layout as the quad form.
 constexpr int kOctTok = 8;
-// kWarps = 12: 12 x 32 threads x <= 168 registers fill the register file (some spills);
-// kWarps = 8: up to 255 registers, no spills, fewer warps to hide latency
-template <int kWarps>
-__global__ void __launch_bounds__(kWarps * 32, 1)
+constexpr int kOctWarps = 8;
+constexpr int kOctStages = 3;
+constexpr int kOctChunks = kOctTok + kExpPerPass;  // 16-B chunks per lane and step
+constexpr size_t kOctSmem = size_t(kOctWarps) * kOctStages * kOctChunks * 32 * 16;  // 192 KB
+
+__global__ void __launch_bounds__(kOctWarps * 32, 1)
     router_chain8_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wp, int T, int d,
                          int E_pad, int n_lg, float* __restrict__ partial) {
+  extern __shared__ __align__(16) uint8_t ring_raw[];
   griddep_launch_dependents();
   griddep_wait();
-  const int lane = lane_id();
+  const int lane = lane_id(), warp = warp_id();
+  // this lane's ring: [stage][chunk] 16-B slots, lane-interleaved (conflict-free LDS.128)
+  uint4* ring = reinterpret_cast<uint4*>(ring_raw) + size_t(warp) * kOctStages * kOctChunks * 32 + lane;
   const int n_oct = (T + kOctTok - 1) / kOctTok;
   const int n_pass = E_pad / kExpPerPass;
   const int S = d / 256 / n_lg;
   const int n_units = n_oct * n_pass * n_lg;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + warp_id();
-  const int n_warps = gridDim.x * (blockDim.x >> 5);
-  for (int u = gw; u < n_units; u += n_warps) {
+  const int gw = blockIdx.x * kOctWarps + warp;
+  const int n_warps = gridDim.x * kOctWarps;
+  // (unit, step) pairs of this warp in order: unit u_i = gw + i * n_warps, steps 0..S-1
+  const int my_units = gw < n_units ? (n_units - 1 - gw) / n_warps + 1 : 0;
+  const int total = my_units * S;
+  auto fetch = [&](int f) {  // issue the copies of this warp's f-th (unit, step) into stage f % kStages
+    const int u = gw + (f / S) * n_warps, s = f % S;
     const int o = u % n_oct, pg = u / n_oct;
     const int g = pg % n_lg, pass = pg / n_lg;
-    const int t0 = o * kOctTok;
-    const __nv_bfloat16* xr = x + 256 * g + 8 * lane;
-    uint32_t rows[kOctTok];  // element offsets of the octet's rows (rows past T: row 0, discarded)
+    const size_t ko = size_t(256) * (n_lg * s + g) + 8 * lane;
+    uint4* slot = ring + size_t(f % kOctStages) * kOctChunks * 32;
 #pragma unroll
-    for (int i = 0; i < kOctTok; ++i) rows[i] = uint32_t(t0 + i < T ? t0 + i : 0) * uint32_t(d);
-    const __nv_bfloat16* wr = wp + size_t(kExpPerPass) * pass * d + 256 * g + 8 * lane;
-    unsigned long long acc[kOctTok][kExpPerPass / 2];
+    for (int i = 0; i < kOctTok; ++i) {
+      const int t = o * kOctTok + i;
+      cp_async_16(slot + i * 32, x + size_t(t < T ? t : 0) * d + ko);  // rows past T: discarded
+    }
 #pragma unroll
-    for (int i = 0; i < kOctTok; ++i)
+    for (int j = 0; j < kExpPerPass; ++j)
+      cp_async_16(slot + (kOctTok + j) * 32, wp + (size_t(kExpPerPass) * pass + j) * d + ko);
+  };
 #pragma unroll
-      for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
+  for (int f = 0; f < kOctStages - 1; ++f) {
+    if (f < total) fetch(f);
+    cp_async_commit();
+  }
+  unsigned long long acc[kOctTok][kExpPerPass / 2];
 #pragma unroll 1
-    for (int s = 0; s < S; ++s) {
-      const size_t ko = size_t(256) * n_lg * s;
-      uint4 xv[kOctTok], wv[kExpPerPass];
+  for (int c = 0; c < total; ++c) {
+    if (c + kOctStages - 1 < total) fetch(c + kOctStages - 1);
+    cp_async_commit();
+    cp_async_wait<kOctStages - 1>();  // this lane's copies of step c have landed
+    const int s = c % S;
+    if (s == 0) {
 #pragma unroll
-      for (int j = 0; j < kExpPerPass; ++j) wv[j] = __ldg(reinterpret_cast<const uint4*>(wr + size_t(j) * d + ko));
+      for (int i = 0; i < kOctTok; ++i)
 #pragma unroll
-      for (int i = 0; i < kOctTok; ++i) xv[i] = ld_nc_v4(xr + rows[i] + ko);
+        for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
+    }
+    const uint4* slot = ring + size_t(c % kOctStages) * kOctChunks * 32;
+    uint4 wv[kExpPerPass];
+#pragma unroll
+    for (int j = 0; j < kExpPerPass; ++j) wv[j] = slot[(kOctTok + j) * 32];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // two halves of the octet's x rows
+      uint4 xv[kOctTok / 2];
+#pragma unroll
+      for (int i = 0; i < kOctTok / 2; ++i) xv[i] = slot[(4 * h + i) * 32];
 #pragma unroll
       for (int qk = 0; qk < 8; ++qk) {  // strictly ascending k inside the lane's slice
         unsigned long long w2[kExpPerPass / 2];
@@ -360,43 +392,49 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
           w2[j] = (qk & 1) ? pack2(bf16_hi(u0), bf16_hi(u1)) : pack2(bf16_lo(u0), bf16_lo(u1));
         }
 #pragma unroll
-        for (int i = 0; i < kOctTok; ++i) {
+        for (int i = 0; i < kOctTok / 2; ++i) {
           const uint32_t uu = (&xv[i].x)[qk >> 1];
           const float xs = (qk & 1) ? bf16_hi(uu) : bf16_lo(uu);
 #pragma unroll
-          for (int j = 0; j < kExpPerPass / 2; ++j) ffma2(acc[i][j], xs, w2[j]);
+          for (int j = 0; j < kExpPerPass / 2; ++j) ffma2(acc[4 * h + i][j], xs, w2[j]);
         }
       }
     }
-    // two butterfly reduce-scatters (tokens 0-3 and 4-7), as in the quad form
+    if (s == S - 1) {
+      const int u = gw + (c / S) * n_warps;
+      const int o = u % n_oct, pg = u / n_oct;
+      const int g = pg % n_lg, pass = pg / n_lg;
+      // two butterfly reduce-scatters (tokens 0-3 and 4-7), as in the quad form
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float v[32];
+      for (int h = 0; h < 2; ++h) {
+        float v[32];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < kExpPerPass / 2; ++j) {
-          v[i * 8 + 2 * j] = __uint_as_float(uint32_t(acc[4 * h + i][j]));
-          v[i * 8 + 2 * j + 1] = __uint_as_float(uint32_t(acc[4 * h + i][j] >> 32));
+          for (int j = 0; j < kExpPerPass / 2; ++j) {
+            v[i * 8 + 2 * j] = __uint_as_float(uint32_t(acc[4 * h + i][j]));
+            v[i * 8 + 2 * j + 1] = __uint_as_float(uint32_t(acc[4 * h + i][j] >> 32));
+          }
+#pragma unroll
+        for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
+          const bool upper = (lane & off) != 0;
+#pragma unroll
+          for (int i = 0; i < n / 2; ++i) {
+            const float send = upper ? v[i] : v[i + n / 2];
+            const float keep = upper ? v[i + n / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+          }
         }
-#pragma unroll
-      for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
-        const bool upper = (lane & off) != 0;
-#pragma unroll
-        for (int i = 0; i < n / 2; ++i) {
-          const float send = upper ? v[i] : v[i + n / 2];
-          const float keep = upper ? v[i + n / 2] : v[i];
-          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-        }
+        const int tt = o * kOctTok + 4 * h + (lane >> 3);
+        if (tt < T) partial[(size_t(g) * T + tt) * E_pad + kExpPerPass * pass + (lane & 7)] = v[0];
       }
-      const int tt = t0 + 4 * h + (lane >> 3);
-      if (tt < T) partial[(size_t(g) * T + tt) * E_pad + kExpPerPass * pass + (lane & 7)] = v[0];
     }
   }
+  cp_async_wait<0>();
 }
 
 // Stage 2 (selection).  CTA = one router block of 32 tokens (the histogram / permute
-// block), 8 warps, one warp per token (4 each): lane l reads the partials of experts l
+// block), 32 warps, one warp per token: lane l reads the partials of experts l
 // and l + 32 straight from L2 (all of a warp's loads issued before any is used),
 // combines them by the contract's tree (q[g] += q[g + o], o = n_lg/2..1) + bias, then
 // top-k, gate weights and the block-aggregated histogram; the last CTA produces the
@@ -413,7 +451,8 @@ MP_DEV float combine_groups(const float* pp, size_t gs, int n_lg) {
   return v;
 }
 
-__global__ void __launch_bounds__(256)
+constexpr int kSelectThreads = rt::kTokens * 32;
+__global__ void __launch_bounds__(kSelectThreads)
     router_select_kernel(const float* __restrict__ partial, int n_lg, int E_pad, const float* __restrict__ bias,
                          int T, int E, int has_gate, int k, int score_mode, int renorm, int32_t* __restrict__ idx,
                          float* __restrict__ wout, float* __restrict__ shared_gate, uint32_t* __restrict__ hist,
@@ -441,21 +480,16 @@ __global__ void __launch_bounds__(256)
     a1 = lane + 32 < E ? combine_groups(pp + lane + 32, gs, n_lg) : -INFINITY;
     ag = has_gate ? combine_groups(pp + E, gs, n_lg) : 0.f;
   };
-  float c0, c1, cg;
-  load(t0 + warp, c0, c1, cg);
-#pragma unroll 1
-  for (int tt = warp; tt < rt::kTokens; tt += 8) {
-    const int t = t0 + tt;
-    if (t >= T) break;
-    float n0, n1, ng;  // the next token's partials are in flight during this token's selection
-    load(t + 8, n0, n1, ng);
+  // one warp per token of the block (32 warps): the selection is a chain of dependent shuffles,
+  // so its latency is hidden by warps, not by work per warp
+  const int t = t0 + warp;
+  if (warp < rt::kTokens && t < T) {
+    float c0, c1, cg;
+    load(t, c0, c1, cg);
     const float a = (lane < E && bias != nullptr) ? __fadd_rn(c0, bz0) : c0;
     const float c = (lane + 32 < E && bias != nullptr) ? __fadd_rn(c1, bz1) : c1;
     select_topk_store(a, c, E, k, score_mode, renorm, idx + size_t(t) * k, wout + size_t(t) * k, cnt_s);
     if (lane == 0 && has_gate && shared_gate != nullptr) shared_gate[t] = 1.0f / (1.0f + expf(-cg));
-    c0 = n0;
-    c1 = n1;
-    cg = ng;
   }
   __syncthreads();
   for (int e = tid; e < E; e += blockDim.x) {
@@ -625,19 +659,13 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
   const int chain = use32 ? 4 : (chain_env ? atoi(chain_env) : 8);
   cudaError_t e;
   if (chain == 8) {
-    static const int oct_warps = [] {
-      const char* env = getenv("MP_ROUTER_OCT_WARPS");
-      return env != nullptr && atoi(env) == 12 ? 12 : 8;
-    }();
     const int n_units8 = ((T + kOctTok - 1) / kOctTok) * (E_pad / kExpPerPass) * n_lg;
-    int grid8 = std::min(kNumSMs, (n_units8 + oct_warps - 1) / oct_warps);
+    int grid8 = std::min(kNumSMs, (n_units8 + kOctWarps - 1) / kOctWarps);
     if (const char* ge = getenv("MP_ROUTER_GRID")) grid8 = std::max(1, atoi(ge));
-    if (oct_warps == 12)
-      e = launch_pdl(router_chain8_kernel<12>, dim3(grid8), dim3(12 * 32), 0, stream, x, wg_packed, T, d, E_pad,
-                     n_lg, partial);
-    else
-      e = launch_pdl(router_chain8_kernel<8>, dim3(grid8), dim3(8 * 32), 0, stream, x, wg_packed, T, d, E_pad,
-                     n_lg, partial);
+    MP_TRY_R(ensure_max_dyn_smem(reinterpret_cast<const void*>(router_chain8_kernel), kOctSmem,
+                                 "cudaFuncSetAttribute(router_chain8)"));
+    e = launch_pdl(router_chain8_kernel, dim3(grid8), dim3(kOctWarps * 32), kOctSmem, stream, x, wg_packed, T, d,
+                   E_pad, n_lg, partial);
   } else if (use32) {
     e = launch_pdl(router_chain_kernel<true>, dim3(grid1), dim3(kChainWarps * 32), 0, stream, x, wg_packed,
                    reinterpret_cast<const float4*>(w32), T, d, E_pad, n_lg, partial);
@@ -661,7 +689,8 @@ int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const 
     const char* env = getenv("MP_ROUTER_PDL");
     return env == nullptr || atoi(env) != 0;
   }();
-  e = launch_pdl_if(sel_pdl || pdl_enabled(), router_select_kernel, dim3(grid2), dim3(256), bc_bytes, stream,
+  e = launch_pdl_if(sel_pdl || pdl_enabled(), router_select_kernel, dim3(grid2), dim3(kSelectThreads), bc_bytes,
+                    stream,
                     static_cast<const float*>(partial), n_lg, E_pad, bias, T, E, has_gate ? 1 : 0, k, score_mode,
                     renorm, idx, w, shared_gate, hist, blk_counts, batch_counts, ticket, blk_prefix,
                     sync ? *sync : PeerSync(), stage_counts ? 1 : 0);
