@@ -110,35 +110,38 @@ MP_DEV unsigned long long pack2(float lo, float hi) {
   return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
 }
 
-// Larger logit wins; equal logits -> lower expert id.
-MP_DEV bool better(float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); }
-
 // Warp-collective top-k + gate weights of one token from its logits (lane l holds
-// experts l and l + 32): k rounds of a warp arg-max (larger logit, ties -> lower
-// id), then softmax over the k (mode 0) or over all E (mode 1, optional
-// renormalisation).  Lane j < k writes idx_row[j] / w_row[j] and bumps cnt_s.
+// experts l and l + 32): k rounds of a warp arg-max -- larger logit, ties -> lower id,
+// as two redux.sync reductions over order-preserving keys -- then softmax over the k
+// (mode 0) or over all E (mode 1, optional renormalisation).  Lane j < k writes
+// idx_row[j] / w_row[j] and bumps cnt_s.
+// Order-preserving 32-bit key of an fp32 logit (-0 canonicalised to +0, so equal logits get
+// equal keys): larger logit <=> larger unsigned key.
+MP_DEV uint32_t logit_key(float v) {
+  const uint32_t u = __float_as_uint(v + 0.0f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
 MP_DEV void select_topk_store(float v0, float v1, int E, int k, int score_mode, int renorm, int32_t* idx_row,
                               float* w_row, int* cnt_s) {
   const int lane = lane_id();
-  bool taken0 = lane >= E, taken1 = lane + 32 >= E;
+  // candidates of this lane: expert lane (v0) and lane + 32 (v1); taken/absent -> key 0
+  uint32_t k0 = lane < E ? logit_key(v0) : 0u, k1 = lane + 32 < E ? logit_key(v1) : 0u;
   float my_v = -INFINITY, mx = 0.f;  // lane j < k keeps the j-th selected logit and expert
   int my_i = 0;
 #pragma unroll 1
-  for (int j = 0; j < k; ++j) {  // (rolled: the unrolled rounds blew the kernel past the i-cache)
-    float bv = -INFINITY;
-    int bi = 0x7fffffff;
-    if (!taken0) { bv = v0; bi = lane; }
-    if (!taken1 && (bi == 0x7fffffff || better(v1, lane + 32, bv, bi))) { bv = v1; bi = lane + 32; }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (oi != 0x7fffffff && (bi == 0x7fffffff || better(ov, oi, bv, bi))) { bv = ov; bi = oi; }
-    }
-    if (j == 0) mx = bv;  // every lane holds the arg-max after the xor butterfly
-    if (lane == j) { my_v = bv; my_i = bi; }
-    if (bi == lane) taken0 = true;
-    if (bi == lane + 32) taken1 = true;
+  for (int j = 0; j < k; ++j) {
+    // round j: the largest key over the warp (redux), then the lowest expert id holding it
+    const bool use1 = k1 > k0;  // ties inside the lane: the lower id (lane) wins
+    const uint32_t bk = use1 ? k1 : k0;
+    const uint32_t mk = __reduce_max_sync(0xffffffffu, bk);
+    const uint32_t cand = (bk == mk && mk != 0u) ? uint32_t(use1 ? lane + 32 : lane) : 0xffffffffu;
+    const uint32_t bi = __reduce_min_sync(0xffffffffu, cand);
+    const float bv = __shfl_sync(0xffffffffu, bi >= 32 ? v1 : v0, bi & 31);
+    if (j == 0) mx = bv;
+    if (lane == j) { my_v = bv; my_i = int(bi); }
+    if (bi == uint32_t(lane)) k0 = 0u;
+    if (bi == uint32_t(lane + 32)) k1 = 0u;
   }
   // weights: lane j < k owns w_j
   const float ej = lane < k ? expf(my_v - mx) : 0.f;
@@ -341,40 +344,60 @@ __global__ void __launch_bounds__(kOctWarps * 32, 1)
   // (unit, step) pairs of this warp in order: unit u_i = gw + i * n_warps, steps 0..S-1
   const int my_units = gw < n_units ? (n_units - 1 - gw) / n_warps + 1 : 0;
   const int total = my_units * S;
-  auto fetch = [&](int f) {  // issue the copies of this warp's f-th (unit, step) into stage f % kStages
-    const int u = gw + (f / S) * n_warps, s = f % S;
-    const int o = u % n_oct, pg = u / n_oct;
+  // producer cursor: the (unit, step) whose copies are issued next, with its row / Wg bases
+  // recomputed only when it crosses into the next unit
+  int f_s = 0, f_u = gw;
+  const __nv_bfloat16* fx = nullptr;   // x row of the octet's first token at this step and lane
+  const __nv_bfloat16* fw = nullptr;   // Wg row of the pass's first expert at this step and lane
+  uint32_t frow[kOctTok];              // element offsets of the octet's rows from the first one
+  auto unit_bases = [&]() {
+    const int o = f_u % n_oct, pg = f_u / n_oct;
     const int g = pg % n_lg, pass = pg / n_lg;
-    const size_t ko = size_t(256) * (n_lg * s + g) + 8 * lane;
-    uint4* slot = ring + size_t(f % kOctStages) * kOctChunks * 32;
+    const int t0 = o * kOctTok;
+    fx = x + size_t(t0) * d + 256 * g + 8 * lane;
+    fw = wp + size_t(kExpPerPass) * pass * d + 256 * g + 8 * lane;
 #pragma unroll
-    for (int i = 0; i < kOctTok; ++i) {
-      const int t = o * kOctTok + i;
-      cp_async_16(slot + i * 32, x + size_t(t < T ? t : 0) * d + ko);  // rows past T: discarded
+    for (int i = 0; i < kOctTok; ++i) frow[i] = uint32_t(t0 + i < T ? i : -t0) * uint32_t(d);  // past T: row 0
+  };
+  if (total > 0) unit_bases();
+  const size_t step_elems = size_t(256) * n_lg;
+  int f_slot = 0;
+  auto fetch = [&]() {  // issue the copies of the producer's (unit, step) into its ring stage
+    uint4* slot = ring + size_t(f_slot) * kOctChunks * 32;
+    const __nv_bfloat16* xs = fx + step_elems * f_s;
+    const __nv_bfloat16* ws = fw + step_elems * f_s;
+#pragma unroll
+    for (int i = 0; i < kOctTok; ++i) cp_async_16(slot + i * 32, xs + int32_t(frow[i]));
+#pragma unroll
+    for (int j = 0; j < kExpPerPass; ++j) cp_async_16(slot + (kOctTok + j) * 32, ws + size_t(j) * d);
+    if (++f_slot == kOctStages) f_slot = 0;
+    if (++f_s == S) {
+      f_s = 0;
+      f_u += n_warps;
+      if (f_u < n_units) unit_bases();
     }
-#pragma unroll
-    for (int j = 0; j < kExpPerPass; ++j)
-      cp_async_16(slot + (kOctTok + j) * 32, wp + (size_t(kExpPerPass) * pass + j) * d + ko);
   };
 #pragma unroll
   for (int f = 0; f < kOctStages - 1; ++f) {
-    if (f < total) fetch(f);
+    if (f < total) fetch();
     cp_async_commit();
   }
   unsigned long long acc[kOctTok][kExpPerPass / 2];
+  int c_s = 0, c_u = gw, c_slot = 0;  // consumer cursor
 #pragma unroll 1
   for (int c = 0; c < total; ++c) {
-    if (c + kOctStages - 1 < total) fetch(c + kOctStages - 1);
+    if (c + kOctStages - 1 < total) fetch();
     cp_async_commit();
     cp_async_wait<kOctStages - 1>();  // this lane's copies of step c have landed
-    const int s = c % S;
+    const int s = c_s;
     if (s == 0) {
 #pragma unroll
       for (int i = 0; i < kOctTok; ++i)
 #pragma unroll
         for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
     }
-    const uint4* slot = ring + size_t(c % kOctStages) * kOctChunks * 32;
+    const uint4* slot = ring + size_t(c_slot) * kOctChunks * 32;
+    if (++c_slot == kOctStages) c_slot = 0;
     uint4 wv[kExpPerPass];
 #pragma unroll
     for (int j = 0; j < kExpPerPass; ++j) wv[j] = slot[(kOctTok + j) * 32];
@@ -400,8 +423,10 @@ __global__ void __launch_bounds__(kOctWarps * 32, 1)
         }
       }
     }
-    if (s == S - 1) {
-      const int u = gw + (c / S) * n_warps;
+    if (++c_s == S) {
+      c_s = 0;
+      const int u = c_u;
+      c_u += n_warps;
       const int o = u % n_oct, pg = u / n_oct;
       const int g = pg % n_lg, pass = pg / n_lg;
       // two butterfly reduce-scatters (tokens 0-3 and 4-7), as in the quad form
