@@ -798,7 +798,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
                          D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
                          L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr, router_w32(L), L->partial));
-    ++launches;
+    launches += 2;  // chain + select
   } else if (G > 1) {
     // no router / permute on this origin: publish zero counts, raise A and B
     MP_TRY(launch_peer_sync(ps0, L->batch_counts, E, 2, st));

@@ -527,12 +527,16 @@ __global__ void __launch_bounds__(kSelectThreads)
   // per-expert counts (integer sums: order-independent), so they are ready when
   // the kernel completes -- no memset, no second pass.
   __shared__ int is_last;
-  __threadfence();
+  // one gpu-scope fence per CTA, from thread 0 after the barrier (cumulative over the CTA's
+  // count stores), as in a cooperative grid barrier -- not one per thread
   __syncthreads();
-  if (tid == 0) is_last = atomicAdd(ticket, 1u) == uint32_t(n_blk - 1);
+  if (tid == 0) {
+    __threadfence();
+    is_last = atomicAdd(ticket, 1u) == uint32_t(n_blk - 1);
+    if (is_last) __threadfence();
+  }
   __syncthreads();
   if (!is_last) return;
-  __threadfence();
   const int nb = n_blk;
   // stage the [nb][E] block-count matrix in shared memory with coalesced loads
   // (when it fits: up to 200 KB), then per-expert scans run from there
