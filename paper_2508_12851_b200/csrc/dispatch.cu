@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(256)
   __shared__ int C[8][64], R[8][64];
   __shared__ int base_s[64];
   __shared__ int wcnt[8][64];  // per-warp, per-expert pair counts -> exclusive prefix over warps
+  __shared__ int Mpre[8][64];  // rows of lower experts on GPU D (exclusive prefix over experts)
   const int b = blockIdx.x;
   const int t0 = b * kTok;
   const int nt = min(kTok, T - t0);
@@ -70,12 +71,37 @@ __global__ void __launch_bounds__(256)
   if (tid < np) s_e[tid] = idx[size_t(t0) * k + tid];
   for (int i = tid; i < 8 * 64; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
+  // receive layout of every GPU D: rows of expert e2 on D = sum over sources routing e2 to D;
+  // warp D scans them over the experts (exclusive), so each expert's base is O(G) work
+  {
+    const int w = tid >> 5, l = tid & 31;
+    if (w < G) {
+      int m[2] = {0, 0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e2 = l + 32 * h;
+        if (e2 < E)
+          for (int s = 0; s < G; ++s)
+            if (R[s][e2] == w) m[h] += C[s][e2];
+      }
+      int p0 = m[0], p1 = m[1];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t0 = __shfl_up_sync(0xffffffffu, p0, o), t1 = __shfl_up_sync(0xffffffffu, p1, o);
+        if (l >= o) {
+          p0 += t0;
+          p1 += t1;
+        }
+      }
+      const int tot0 = __shfl_sync(0xffffffffu, p0, 31);
+      Mpre[w][l] = p0 - m[0];
+      Mpre[w][l + 32] = tot0 + p1 - m[1];
+    }
+  }
+  __syncthreads();
   if (tid < E) {
     const int e = tid, D = R[rank][e];
-    int base = blk_prefix[size_t(b) * E + e];
-    for (int e2 = 0; e2 < e; ++e2)
-      for (int s = 0; s < G; ++s)
-        if (R[s][e2] == D) base += C[s][e2];
+    int base = blk_prefix[size_t(b) * E + e] + Mpre[D][e];
     for (int s = 0; s < rank; ++s)
       if (R[s][e] == D) base += C[s][e];
     base_s[e] = base;

@@ -61,35 +61,59 @@ struct TileCoord {
   int g, m_blk, n_blk;
 };
 
+// Inclusive warp scan (Kogge-Stone over the 32 lanes).
+MP_DEV int warp_incl_scan(int v) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
 // Prologue shared by both kernels: build the group table in shared memory
 // (explicit, derived from the exchanged counts, or a single dense group) and
-// the per-group tile prefix.  Called by every thread.
+// the per-group tile prefix.  Called by every thread; warp 0 does the
+// compaction and the scans with warp collectives (no serial thread-0 loops
+// over the experts on the critical path of every launch).
 template <class Tail>
 MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = lane_id();
   if (gs.mode == 1) {
-    if (tid < gs.E) {
+    if (tid < 32) {
+      // experts lane and lane + 32 (E <= 64): rows this GPU computes for them
       const int32_t* counts = gs.counts + (gs.parity ? size_t(*gs.parity) * gs.G * gs.E : 0);
-      int m = 0;
-      for (int s = 0; s < gs.G; ++s)
-        if (gs.route[s * gs.E + tid] == gs.rank) m += counts[s * gs.E + tid];
-      st.g_tmp[tid] = m;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int ng = 0, row = 0;
-      for (int e = 0; e < gs.E; ++e) {
-        const int m = st.g_tmp[e];
-        if (m > 0 && m >= gs.m_lo && m < gs.m_hi) {
-          st.g_arow[ng] = row;
-          st.g_m[ng] = m;
-          st.g_slot[ng] = gs.slot_of[e];
-          st.g_orow[ng] = row;
-          ++ng;
+      int m[2] = {0, 0}, slot[2] = {-1, -1};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = lane + 32 * h;
+        if (e < gs.E) {
+          for (int s = 0; s < gs.G; ++s)
+            if (gs.route[s * gs.E + e] == gs.rank) m[h] += counts[s * gs.E + e];
+          slot[h] = gs.slot_of[e];
         }
-        row += m;
       }
-      st.n_groups = ng;
+      // rows of lower experts (receive layout: expert-major) and the compacted group index
+      const int p0 = warp_incl_scan(m[0]);
+      const int tot0 = __shfl_sync(0xffffffffu, p0, 31);
+      const int p1 = warp_incl_scan(m[1]);
+      const int row[2] = {p0 - m[0], tot0 + p1 - m[1]};
+      const bool sel0 = m[0] > 0 && m[0] >= gs.m_lo && m[0] < gs.m_hi;
+      const bool sel1 = m[1] > 0 && m[1] >= gs.m_lo && m[1] < gs.m_hi;
+      const unsigned b0 = __ballot_sync(0xffffffffu, sel0), b1 = __ballot_sync(0xffffffffu, sel1);
+      const unsigned lt = (1u << lane) - 1u;
+      const int idx[2] = {__popc(b0 & lt), __popc(b0) + __popc(b1 & lt)};
+      const bool sel[2] = {sel0, sel1};
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (sel[h]) {
+          st.g_arow[idx[h]] = row[h];
+          st.g_m[idx[h]] = m[h];
+          st.g_slot[idx[h]] = slot[h];
+          st.g_orow[idx[h]] = row[h];
+        }
+      if (lane == 0) st.n_groups = __popc(b0) + __popc(b1);
     }
   } else if (gs.mode == 2) {
     if (tid == 0) {
@@ -110,21 +134,21 @@ MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
     }
   }
   __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    st.tile_prefix[0] = 0;
-    for (int g = 0; g < st.n_groups; ++g) {
-      const int m_blocks = (st.g_m[g] + bm - 1) / bm;
-      acc += m_blocks * n_blocks;
-      st.tile_prefix[g + 1] = acc;
+  if (tid < 32) {  // tile prefix over the groups, 32 at a time
+    const int ng = st.n_groups;
+    int carry = 0;
+    if (lane == 0) st.tile_prefix[0] = 0;
+    for (int g0 = 0; g0 < ng; g0 += 32) {
+      const int g = g0 + lane;
+      const int tiles = g < ng ? ((st.g_m[g] + bm - 1) / bm) * n_blocks : 0;
+      const int incl = warp_incl_scan(tiles);
+      if (g < ng) st.tile_prefix[g + 1] = carry + incl;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    st.total_tiles = acc;
+    if (lane == 0) st.total_tiles = carry;
   }
 }
 
-// tile -> (group, n-block, m-block): one group at a time, m fastest, so the
-// CTAs running concurrently share the group's weight tile in L2.  (An
-// n-block-major order that interleaves the groups was measured slower.)
 template <class Tail>
 MP_DEV TileCoord decode_any(const Tail& s, int tile, int n_blocks, int bm) {
   TileCoord c;
