@@ -1189,6 +1189,21 @@ def measure_peer_copy(layer, world, rank):
     return float(bw.item())
 
 
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` without a torchrun environment: re-exec this script under
+    torch.distributed.run with one process per GPU (127.0.0.1 rendezvous); rank 0's single JSON
+    line comes through on stdout."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
+
+
 if __name__ == "__main__":
     a = parse()
     if a.gpus > 1 and "WORLD_SIZE" not in os.environ and a.impl != "reference":
