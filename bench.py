@@ -160,16 +160,13 @@ def stage_roofline(shape, T, rows, stage_ms, hbm_gbs):
         ms = stage_ms.get(name, 0.0)
         gbs = b / (ms * 1e-3) / 1e9 if ms > 0 else None
         out[name] = {"bytes": b, "ms": ms, "GB/s": gbs, "frac_hbm": gbs / hbm_gbs if gbs else None}
-    # the router's bit-exact fp32 lane chains make it FMA-issue bound, not HBM bound: its
-    # gate FLOPs against the CUDA-core fp32 FMA peak (148 SMs x 128 lanes x 2 x 1.965 GHz)
-    e_pad = (shape.E + shape.shared_gate + 7) // 8 * 8
+    # the router's exact logits are nine 8-bit limb GEMMs on the tensor cores (kind::i8):
+    # their integer ops over the time, next to the HBM view above
+    n_pad = max(16, (shape.E + shape.shared_gate + 15) // 16 * 16)
     r_ms = stage_ms.get("router", 0.0)
     if r_ms > 0:
-        fl = 2.0 * T * e_pad * d
-        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
-        out["router"].update({"fp32_FLOP": fl, "fp32_TFLOP/s": fl / (r_ms * 1e-3) / 1e12,
-                              "fp32_peak_TFLOP/s": fp32_peak,
-                              "frac_fp32": fl / (r_ms * 1e-3) / 1e12 / fp32_peak})
+        ops = 9 * 2.0 * T * n_pad * d
+        out["router"].update({"i8_OP": ops, "i8_TOP/s": ops / (r_ms * 1e-3) / 1e12})
     return out
 
 
@@ -309,7 +306,8 @@ def setup_bench_layer(args):
     # ---- activation counts of a warm-up batch (GPU router kernel) -> placement
     lib = _lib.load()
     import ctypes
-    packed = torch.empty((shape.E + shape.shared_gate + 7) // 8 * 8 * shape.d, device=dev, dtype=torch.bfloat16)
+    packed = torch.empty(lib.mp_router_packed_bytes(shape.E + shape.shared_gate, shape.d), device=dev,
+                         dtype=torch.uint8)
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     _lib.check(lib.mp_router_pack(ctypes.c_void_p(wg.data_ptr()), shape.E + shape.shared_gate, shape.d,
                                   ctypes.c_void_p(packed.data_ptr()), st))

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MP_ABI_VERSION 2
+#define MP_ABI_VERSION 3
 #define MP_MAX_GROUPS 128 /* expert groups per mp_grouped_gemm call */
 
 #define MP_OK 0
@@ -56,16 +56,17 @@ int mp_last_error(char* buf, int buf_len);
  * Stateless kernels (used by the layer, exported for parity tests).
  * --------------------------------------------------------------------- */
 
-/* Copy router weights Wg [E_tot, d] bf16 into the kernel layout [E_pad][d]
- * bf16, E_pad = E_tot rounded up to a multiple of 8 (zero rows); `packed`
- * must hold E_pad * d bf16 values; d % 256 == 0.  E_tot = E, or E+1 with the
- * shared-expert gate row. */
-int mp_router_pack(const void* wg_bf16, int E_tot, int d, void* packed, void* stream);
+/* Bytes of the packed router operand for E_tot weight rows of width d. */
+size_t mp_router_packed_bytes(int E_tot, int d);
 
-/* Wg [E_tot, d] bf16 pre-converted to fp32 in K1's lane-consumption order
- * (E_pad * d floats; the layer's default router operand): same products and
- * chains as the bf16 operand, so the logits are bit-identical. */
-int mp_router_pack32(const void* wg_bf16, int E_tot, int d, float* packed32, void* stream);
+/* Pack router weights Wg [E_tot, d] bf16 into K1's exact-integer operand:
+ * each row on its own integer grid (q = rint(w * 2^(21 - E(row))), see
+ * csrc/router.cu), as three 8-bit limb planes [3][N][d] (N = E_tot rounded up
+ * to a multiple of 16, zero rows), then int64 row sums [N] and int32 row
+ * exponents [N].  `packed` must hold mp_router_packed_bytes(E_tot, d) bytes
+ * (16-byte aligned); d % 256 == 0.  E_tot = E, or E+1 with the shared-expert
+ * gate row. */
+int mp_router_pack(const void* wg_bf16, int E_tot, int d, void* packed, void* stream);
 
 /* K1 -- replaces ActivationStats.ingest (stats.py:82-96) fed by sampled expert
  * sets (sim.py:181-185): top-k routing of T tokens plus a fused histogram.
@@ -79,11 +80,6 @@ int mp_router_pack32(const void* wg_bf16, int E_tot, int d, float* packed32, voi
 int mp_router_topk_hist(const void* x, const void* packed, const float* bias, int T, int d, int E, int has_gate,
                         int k, int score_mode, int renorm, int32_t* idx, float* w, float* gate_out, uint32_t* hist,
                         void* stream);
-/* The same with the fp32 operand of mp_router_pack32 (`packed32`), the kernels
- * mp_layer_forward runs; `packed` (bf16) must still be given. */
-int mp_router_topk_hist_f32w(const void* x, const void* packed, const float* packed32, const float* bias, int T,
-                             int d, int E, int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w,
-                             float* gate_out, uint32_t* hist, void* stream);
 /* Logits-in parity variant of K1's selection stage: top-k (descending, ties ->
  * lower id), gate weights and histogram from fp32 logits [T][ld] (+ bias [E]
  * or NULL) -- pins the selection rule independently of the dot products. */

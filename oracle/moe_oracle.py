@@ -33,13 +33,10 @@ and what is not:
                            the stated tolerance for activations.
 
 Numerics contract shared with the CUDA kernels:
-  logits[t,e] = 32 * n_lg lane partials (lane (g, l): sequential fp32
-                accumulation over k in [8 L s + 8 (32 g + l), +8), s ascending,
-                L = 32 n_lg, n_lg = router_lane_groups(d) in {1, 2, 4}) combined
-                by the butterfly tree p[l] += p[l + o], o = 16..1 inside each
-                group, then q[g] += q[g + o], o = n_lg/2..1 across groups (bf16
-                inputs: each product is exact in fp32, so the GPU's FMA chain
-                and this add chain round identically), then + bias[e].
+  logits[t,e] = f32( rn_f32(S) * 2^(E(x_t) + E(w_e) - 35) ) + bias[e], with
+                S = sum_k qx[t,k] qw[e,k] EXACT, q = rint(a * 2^(win - E(a))) per
+                row (win 21 for x, 14 for Wg) and E(a) = max(ef(max|a|) - 126, -100)
+                (router_logits).
   top-k       = k largest logits, descending, ties -> lower expert id.
   h           = bf16( silu(g) * u ) with g, u the fp32 GEMM accumulators.
   y           = bf16( h @ W2^T ) (fp32 accumulate).
@@ -189,50 +186,73 @@ def slot_assignment(gpu_experts) -> dict:
 # ----------------------------------------------------------------------------- router
 
 
-def router_lane_groups(d: int) -> int:
-    """Lane groups of the router contract: 4 for d >= 4096 (d % 1024 == 0), 2 for d >= 2048
-    (d % 512 == 0), else 1 -- the same function as csrc/router.cu router_lane_groups."""
-    if d >= 4096 and d % 1024 == 0:
-        return 4
-    if d >= 2048 and d % 512 == 0:
-        return 2
-    return 1
+ROUTER_WIN_X = 21      # token rows: |q| <= 2^21 on each row's integer grid
+ROUTER_WIN_W = 14      # router-weight rows: |q| <= 2^14
+ROUTER_MIN_EXP = -100  # floor of the row exponent
+
+
+def router_row_exponent(a: np.ndarray) -> np.ndarray:
+    """E(a) per row of a bf16-exact array: max(ef - 126, -100) with ef the bf16 exponent field of
+    the row's largest magnitude, so every |a_k| < 2^E(a) (csrc/router.cu row_exponent)."""
+    bits = (np.ascontiguousarray(a, dtype=np.float32).view(np.uint32) >> 16) & 0x7FFF
+    ef = (bits.max(axis=1) >> 7).astype(np.int64)
+    return np.maximum(ef - 126, ROUTER_MIN_EXP)
+
+
+def router_quantise(a: np.ndarray, win: int):
+    """Integer grid of each row: q = rint(a * 2^(win - E(a))) (round half to even), exact in fp64."""
+    e = router_row_exponent(a)
+    q = np.rint(np.asarray(a, dtype=np.float64) * np.exp2(win - e)[:, None]).astype(np.int64)
+    return q, e
+
+
+def exact_int_matmul(q: np.ndarray, r: np.ndarray) -> np.ndarray:
+    """q @ r.T exactly for |q|, |r| <= 2^21 and rows up to 16384 long: 11-bit halves through
+    fp64 GEMMs, each of whose partial sums is an integer below 2^53 (so any summation order
+    is exact), recombined in int64."""
+    qh, ql = q >> 11, q & 2047
+    rh, rl = r >> 11, r & 2047
+    mm = lambda a, b: np.rint(a.astype(np.float64) @ b.astype(np.float64).T).astype(np.int64)
+    return (mm(qh, rh) << 22) + ((mm(qh, rl) + mm(ql, rh)) << 11) + mm(ql, rl)
+
+
+def rne_f32_of_int(s: np.ndarray) -> np.ndarray:
+    """Round int64 values to the nearest fp32 (ties to even), exactly (returned as float64)."""
+    s = np.asarray(s, dtype=np.int64)
+    a = np.abs(s).astype(np.uint64)
+    nb = np.zeros(a.shape, dtype=np.int64)            # bit length of |s|
+    for sh in (32, 16, 8, 4, 2, 1):
+        big = (a >> np.uint64(sh)) >> nb.astype(np.uint64) != 0
+        nb = np.where(big, nb + sh, nb)
+    nb = np.where(a != 0, nb + 1, 0)
+    drop = np.maximum(nb - 24, 0).astype(np.uint64)
+    m = a >> drop
+    rem = a - (m << drop)
+    half = np.where(drop > 0, np.uint64(1) << np.maximum(drop, np.uint64(1)) - np.uint64(1), np.uint64(0))
+    up = (drop > 0) & ((rem > half) | ((rem == half) & ((m & np.uint64(1)) == 1)))
+    m = m + up.astype(np.uint64)
+    v = m.astype(np.float64) * np.exp2(drop.astype(np.float64))
+    return np.where(s < 0, -v, v)
 
 
 def router_logits(x: np.ndarray, wg: np.ndarray, bias: np.ndarray | None = None) -> np.ndarray:
-    """Router logits under the kernel's numerics contract (csrc/router.cu).
+    """Router logits under K1's exact-integer contract (csrc/router.cu).
 
-    L = 32 * n_lg logical lanes, n_lg = router_lane_groups(d).  Logical lane
-    (g, l) -- group g, lane l of 32 -- owns k in [8 L s + 8 (32 g + l), +8) for
-    s = 0..d/(8 L)-1; its partial is a sequential fp32 accumulation over those k
-    ascending (bf16 inputs: products exact, one rounding per add == the GPU's
-    FMA).  Inside each group the 32 partials are combined by the butterfly tree
-    p[l] <- p[l] + p[l + o], o = 16, 8, 4, 2, 1; then the group sums by
-    q[g] <- q[g] + q[g + o], o = n_lg/2 .. 1; then + bias[e].
+    Each row is quantised on its own grid, q = rint(a * 2^(win - E(a))), win = 21 for token
+    rows and 14 for router-weight rows; S[t,e] = sum_k qx[t,k] qw[e,k] is an exact integer;
+    logits = f32(f64(rn_f32(S)) * 2^(E(x_t) + E(w_e) - 35)), then + bias[e] in fp32.  The GPU
+    computes S with 8-bit limb MMAs on the tensor cores; exactness makes it independent of
+    any summation order.
     """
     x = np.asarray(x, dtype=np.float32)
     wg = np.asarray(wg, dtype=np.float32)
-    T, d = x.shape
-    E = wg.shape[0]
-    if d % 256:
+    if x.shape[1] % 256:
         raise ValueError("router contract needs d % 256 == 0")
-    G = router_lane_groups(d)
-    S = d // (256 * G)
-    xr = x.reshape(T, S, G, 32, 8)
-    wr = wg.reshape(E, S, G, 32, 8)
-    acc = np.zeros((T, E, G, 32), dtype=np.float32)
-    for s in range(S):
-        for j in range(8):
-            acc += xr[:, None, s, :, :, j] * wr[None, :, s, :, :, j]   # exact products, one fp32 rounding per add
-    p = acc
-    for o in (16, 8, 4, 2, 1):
-        p = p[..., :o] + p[..., o:2 * o]
-    q = p[..., 0]
-    o = G // 2
-    while o >= 1:
-        q = q[..., :o] + q[..., o:2 * o]
-        o //= 2
-    logits = np.ascontiguousarray(q[..., 0])
+    qx, ex = router_quantise(x, ROUTER_WIN_X)
+    qw, ew = router_quantise(wg, ROUTER_WIN_W)
+    S = exact_int_matmul(qx, qw)
+    logits = rne_f32_of_int(S) * np.exp2((ex[:, None] + ew[None, :] - ROUTER_WIN_X - ROUTER_WIN_W).astype(np.float64))
+    logits = np.ascontiguousarray(logits.astype(np.float32))
     if bias is not None:
         logits[:, :bias.shape[0]] += np.asarray(bias, dtype=np.float32)[None, :]
     return logits

@@ -14,7 +14,7 @@ from pathlib import Path
 from .errors import DimensionMismatch, InfeasibleError, UnplacedExpertError
 
 LIB_PATH = Path(__file__).resolve().parent / "libmoeplace_b200.so"
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_GROUPS = 128
 
 MP_OK = 0
@@ -39,8 +39,8 @@ CFG_KEYS = {"pair_routed": 0, "split_m": 1, "small_grid": 2, "fuse_shared": 3}
 
 # Every symbol the header declares (checked by tests/test_abi.py).
 EXPORTED_SYMBOLS = (
-    "mp_abi_version", "mp_last_error", "mp_router_pack", "mp_router_pack32", "mp_router_topk_hist",
-    "mp_router_topk_hist_f32w", "mp_router_topk_logits", "mp_grouped_gemm",
+    "mp_abi_version", "mp_last_error", "mp_router_packed_bytes", "mp_router_pack", "mp_router_topk_hist",
+    "mp_router_topk_logits", "mp_grouped_gemm",
     "mp_layer_create", "mp_layer_destroy", "mp_layer_get_ptrs", "mp_layer_export_handles",
     "mp_layer_open_peers", "mp_layer_set_routes", "mp_layer_prepare_router", "mp_layer_forward",
     "mp_layer_forward_timed", "mp_layer_route", "mp_layer_permute", "mp_layer_experts", "mp_layer_combine_gather",
@@ -95,9 +95,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         "mp_abi_version": ([], I),
         "mp_last_error": ([c_char_p, I], I),
         "mp_router_pack": ([V, I, I, V, V], I),
-        "mp_router_pack32": ([V, I, I, V, V], I),
+        "mp_router_packed_bytes": ([I, I], ctypes.c_size_t),
         "mp_router_topk_hist": ([V, V, V, I, I, I, I, I, I, I, V, V, V, V, V], I),
-        "mp_router_topk_hist_f32w": ([V, V, V, V, I, I, I, I, I, I, I, V, V, V, V, V], I),
         "mp_router_topk_logits": ([V, I, V, I, I, I, I, I, V, V, V, V], I),
         "mp_grouped_gemm": ([V, I64, V, I64, V, V, I, I, V, I, I, V], I),
         "mp_layer_create": ([POINTER(LayerDesc), POINTER(c_void_p)], I),

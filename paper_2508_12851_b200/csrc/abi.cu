@@ -108,11 +108,9 @@ struct mp_layer {
   uint32_t* flags = nullptr;
   // scratch views
   __nv_bfloat16 *h = nullptr, *wg = nullptr, *w13s = nullptr, *w2s = nullptr, *hs = nullptr, *ys = nullptr;
-  __nv_bfloat16* wg_packed = nullptr;
-  float* wg32 = nullptr;  // Wg in fp32, router consumption order
-  float* partial = nullptr;  // router lane-group partial logits [n_lg][max_tokens][E_pad]
+  uint8_t* wg_packed = nullptr;  // router operand: Wg limbs, row sums, row exponents
   float *bias = nullptr, *w = nullptr, *sgate = nullptr;
-  int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr, *blk_prefix = nullptr,
+  int32_t *idx = nullptr, *pos_dst = nullptr, *pos_row = nullptr, *blk_counts = nullptr, *count_acc = nullptr,
           *batch_counts = nullptr, *route_d = nullptr,
           *slot_of_d = nullptr;
   uint32_t *hist = nullptr, *err = nullptr, *ticket = nullptr, *sync_state = nullptr;
@@ -158,16 +156,6 @@ namespace {
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// The router's fp32 consumption-order operand runs the quad chain kernel; the default is the
-// octet kernel over the bf16 rows (MP_ROUTER_CHAIN=4 selects the quad kernel with fp32 Wg).
-const float* router_w32(const mp_layer* L) {
-  static const bool quad = [] {
-    const char* env = getenv("MP_ROUTER_CHAIN");
-    return env != nullptr && atoi(env) == 4;
-  }();
-  return quad ? L->wg32 : nullptr;
-}
-
 struct Carver {
   uint8_t* base;
   size_t off = 0;
@@ -210,34 +198,21 @@ int mp_last_error(char* buf, int buf_len) {
   return MP_OK;
 }
 
+size_t mp_router_packed_bytes(int E_tot, int d) { return router_packed_bytes(E_tot, d); }
+
 int mp_router_pack(const void* wg_bf16, int E_tot, int d, void* packed, void* stream) {
   if (!wg_bf16 || !packed) return set_error(MP_E_ARG, "mp_router_pack: null pointer");
-  return launch_router_pack(static_cast<const __nv_bfloat16*>(wg_bf16), E_tot, d,
-                            static_cast<__nv_bfloat16*>(packed), static_cast<cudaStream_t>(stream));
+  return launch_router_pack(static_cast<const __nv_bfloat16*>(wg_bf16), E_tot, d, static_cast<uint8_t*>(packed),
+                            static_cast<cudaStream_t>(stream));
 }
 
 int mp_router_topk_hist(const void* x, const void* packed, const float* bias, int T, int d, int E, int has_gate,
                         int k, int score_mode, int renorm, int32_t* idx, float* w, float* gate_out, uint32_t* hist,
                         void* stream) {
   if (!x || !packed || !idx || !w) return set_error(MP_E_ARG, "mp_router_topk_hist: null pointer");
-  return launch_router(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(packed), bias, T, d,
-                       E, has_gate, k, score_mode, renorm,
-                       idx, w, gate_out, hist, nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream));
-}
-
-int mp_router_pack32(const void* wg_bf16, int E_tot, int d, float* packed32, void* stream) {
-  if (!wg_bf16 || !packed32) return set_error(MP_E_ARG, "mp_router_pack32: null pointer");
-  return launch_router_pack32(static_cast<const __nv_bfloat16*>(wg_bf16), E_tot, d, packed32,
-                              static_cast<cudaStream_t>(stream));
-}
-
-int mp_router_topk_hist_f32w(const void* x, const void* packed, const float* packed32, const float* bias, int T,
-                             int d, int E, int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w,
-                             float* gate_out, uint32_t* hist, void* stream) {
-  if (!x || !packed || !packed32 || !idx || !w) return set_error(MP_E_ARG, "mp_router_topk_hist_f32w: null pointer");
-  return launch_router(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(packed), bias, T, d,
-                       E, has_gate, k, score_mode, renorm, idx, w, gate_out, hist, nullptr, nullptr, nullptr, nullptr,
-                       static_cast<cudaStream_t>(stream), nullptr, packed32);
+  return launch_router(static_cast<const __nv_bfloat16*>(x), static_cast<const uint8_t*>(packed), bias, T, d, E,
+                       has_gate, k, score_mode, renorm, idx, w, gate_out, hist, nullptr, nullptr, nullptr, nullptr,
+                       static_cast<cudaStream_t>(stream));
 }
 
 int mp_router_topk_logits(const float* logits, int ld, const float* bias, int T, int E, int k, int score_mode,
@@ -340,9 +315,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
     auto plan = [&](Carver& cv) {
       L->h = cv.take<__nv_bfloat16>(size_t(L->recv_cap) * D.f);
       L->wg = cv.take<__nv_bfloat16>(size_t(E_tot) * D.d);
-      L->wg_packed = cv.take<__nv_bfloat16>(size_t(router_e_pad(E_tot)) * D.d);
-      L->wg32 = cv.take<float>(size_t(router_e_pad(E_tot)) * D.d);
-      L->partial = cv.take<float>(router_partial_floats(T, D.d, E_tot));
+      L->wg_packed = cv.take<uint8_t>(router_packed_bytes(E_tot, D.d));
       L->bias = cv.take<float>(E);
       L->w = cv.take<float>(size_t(T) * k);
       L->sgate = D.shared_gate ? cv.take<float>(T) : nullptr;
@@ -350,7 +323,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
       L->pos_dst = cv.take<int32_t>(size_t(T) * k);
       L->pos_row = cv.take<int32_t>(size_t(T) * k);
       L->blk_counts = cv.take<int32_t>(size_t(L->nb_max) * E);
-      L->blk_prefix = cv.take<int32_t>(size_t(L->nb_max) * E);
+      L->count_acc = cv.take<int32_t>(64);  // router batch-count accumulator (reset by its last CTA)
       L->batch_counts = cv.take<int32_t>(64);
       L->route_d = cv.take<int32_t>(8 * 64);
       L->slot_of_d = cv.take<int32_t>(64);
@@ -590,8 +563,6 @@ int mp_layer_prepare_router(mp_layer* L, void* stream) {
   if (!L) return set_error(MP_E_ARG, "mp_layer_prepare_router: null layer");
   DeviceGuard dg(L->desc.device);
   MP_CUDA(dg.status);
-  MP_TRY(launch_router_pack32(L->wg, L->desc.E + (L->desc.shared_gate ? 1 : 0), L->desc.d, L->wg32,
-                              static_cast<cudaStream_t>(stream)));
   MP_TRY(launch_router_pack(L->wg, L->desc.E + (L->desc.shared_gate ? 1 : 0), L->desc.d, L->wg_packed,
                             static_cast<cudaStream_t>(stream)));
   L->router_ready = true;
@@ -797,8 +768,8 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   if (T > 0) {
     MP_TRY(launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, E, D.shared_gate, k,
                          D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts, L->batch_counts,
-                         L->ticket, L->blk_prefix, st, G > 1 ? &ps0 : nullptr, router_w32(L), L->partial));
-    launches += 2;  // chain + select
+                         L->ticket, L->count_acc, st, G > 1 ? &ps0 : nullptr));
+    ++launches;
   } else if (G > 1) {
     // no router / permute on this origin: publish zero counts, raise A and B
     MP_TRY(launch_peer_sync(ps0, L->batch_counts, E, 2, st));
@@ -813,7 +784,7 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
   MP_TRY(mk.mark());  // 3 (layout: folded into permute / GEMM prologues)
   if (T > 0) {
     MP_TRY(launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, parity,
-                          L->blk_prefix, src_ptrs, rank, G, T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st,
+                          L->blk_counts, src_ptrs, rank, G, T, D.d, E, k, recv_ptrs, L->pos_dst, L->pos_row, st,
                           G > 1 ? &ps_perm : nullptr));
     ++launches;
   }
@@ -876,7 +847,7 @@ int mp_layer_route(mp_layer* L, const void* x, int T, void* stream) {
   }
   return launch_router(static_cast<const __nv_bfloat16*>(x), L->wg_packed, L->bias, T, D.d, D.E, D.shared_gate,
                        D.top_k, D.score_mode, D.renorm, L->idx, L->w, L->sgate, L->hist, L->blk_counts,
-                       L->batch_counts, L->ticket, L->blk_prefix, st, nullptr, router_w32(L), L->partial);
+                       L->batch_counts, L->ticket, L->count_acc, st, nullptr);
 }
 
 int mp_layer_permute(mp_layer* L, const void* x, int T, const int32_t* counts_all, void* staging, void* stream) {
@@ -894,7 +865,7 @@ int mp_layer_permute(mp_layer* L, const void* x, int T, const int32_t* counts_al
   MP_TRY(upload_stage_ptrs(L, 0, staging, size_t(D.d) * 2, L->recv, st));
   MP_TRY(upload_stage_ptrs(L, 1, L->src_image, 4, L->recv_src, st));
   if (T == 0) return MP_OK;
-  return launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, nullptr, L->blk_prefix,
+  return launch_permute(static_cast<const __nv_bfloat16*>(x), L->idx, L->route_d, counts_all, nullptr, L->blk_counts,
                         reinterpret_cast<int32_t* const*>(L->stage_ptrs + 8), L->rank, L->G, T, D.d, D.E, D.top_k,
                         reinterpret_cast<__nv_bfloat16* const*>(L->stage_ptrs), L->pos_dst, L->pos_row, st, nullptr);
 }

@@ -240,6 +240,94 @@ MP_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
       : "r"(taddr));
 }
 MP_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// TMEM -> registers: 32 lanes x 8 consecutive 32-bit columns.
+MP_DEV void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, 8-bit integer inputs, s32 accumulator (exact), one thread.
+MP_DEV void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Instruction descriptor: kind::i8, A = u8, B = u8 or s8, D = s32, both K-major.
+__host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N, bool b_signed) {
+  return (2u << 4)                            // D format s32
+         | (0u << 7)                          // A format u8
+         | (uint32_t(b_signed ? 1 : 0) << 10) // B format u8 / s8
+         | (uint32_t(N >> 3) << 17)           // N / 8
+         | (uint32_t(M >> 4) << 24);          // M / 16
+}
+
+// Order this thread's generic-proxy shared-memory writes before later async-proxy
+// (tcgen05.mma / TMA) reads of them.
+MP_DEV void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+MP_DEV void st_shared_v4(void* p, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+// DSMEM: 32-bit store / 64-bit load at the same smem offset in CTA `cta` of the cluster.
+MP_DEV void st_cluster_u32(const void* local_equiv, uint32_t cta, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "st.shared::cluster.u32 [ra], %2;\n\t}" ::"r"(smem_u32(local_equiv)),
+      "r"(cta), "r"(v)
+      : "memory");
+}
+// Generic pointer to the same shared-memory object in CTA `cta` of the cluster (plain loads
+// through it are ordinary memory operations the compiler can batch).
+template <typename T>
+MP_DEV const T* cluster_map(const T* local, uint32_t cta) {
+  uint64_t r;
+  asm("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(reinterpret_cast<uint64_t>(local)), "r"(cta));
+  return reinterpret_cast<const T*>(r);
+}
+// Remote 16-byte store into CTA `cta`'s shared memory (same offsets as the local
+// `dst_equiv` / `bar_equiv`) that completes `bytes` = 16 of tx on that CTA's mbarrier.
+MP_DEV void st_async_v2_b64(const void* dst_equiv, const uint64_t* bar_equiv, uint32_t cta, long long a,
+                            long long b) {
+  asm volatile(
+      "{\n\t.reg .b32 rd, rb;\n\t"
+      "mapa.shared::cluster.u32 rd, %0, %2;\n\t"
+      "mapa.shared::cluster.u32 rb, %1, %2;\n\t"
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [rd], {%3, %4}, [rb];\n\t}" ::"r"(
+          smem_u32(dst_equiv)),
+      "r"(smem_u32(bar_equiv)), "r"(cta), "l"(a), "l"(b)
+      : "memory");
+}
+// Bulk copy of `bytes` (multiple of 16) from this CTA's shared memory to the same offsets as
+// `dst_equiv` in CTA `cta` of the cluster, completing on that CTA's mbarrier at `bar_equiv`.
+MP_DEV void bulk_s2s_cluster(const void* dst_equiv, const void* src, uint32_t bytes, const uint64_t* bar_equiv,
+                             uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 rd, rb;\n\t"
+      "mapa.shared::cluster.u32 rd, %0, %3;\n\t"
+      "mapa.shared::cluster.u32 rb, %2, %3;\n\t"
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [rd], [%1], %4, [rb];\n\t}" ::"r"(
+          smem_u32(dst_equiv)),
+      "r"(smem_u32(src)), "r"(smem_u32(bar_equiv)), "r"(cta), "r"(bytes)
+      : "memory");
+}
+MP_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+MP_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+MP_DEV long long ld_cluster_s64(const void* local_equiv, uint32_t cta) {
+  long long v;
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %1, %2;\n\t"
+      "ld.shared::cluster.s64 %0, [ra];\n\t}"
+      : "=l"(v)
+      : "r"(smem_u32(local_equiv)), "r"(cta)
+      : "memory");
+  return v;
+}
 
 // ---------------------------------------------------------------- system scope (NVLink peers)
 MP_DEV void st_release_sys_u32(uint32_t* p, uint32_t v) {

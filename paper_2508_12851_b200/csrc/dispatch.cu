@@ -31,8 +31,8 @@ namespace mp {
 //   * my_base[e]: first row of this origin's expert-e rows in the target GPU's
 //     receive buffer = rows of lower experts on that GPU + rows of lower-ranked
 //     sources for e (from the exchanged counts C[G][E] and the route table);
-//   * prefix[e]: rows of expert e in this origin's earlier router blocks
-//     (scanned once by the router's last CTA into blk_prefix).
+//   * prefix[e]: rows of expert e in this origin's earlier router blocks, summed
+//     here from the router's per-block counts (4 segments x 64 experts, loads in flight).
 // Phase 1: one thread per (token, slot) pair computes its stable in-block rank
 //          (__match_any_sync within a warp, a per-expert prefix across warps).
 // Phase 2: one warp per token loads the x row once (16 B per lane per step) and
@@ -41,7 +41,7 @@ template <int kVecPerLane>
 __global__ void __launch_bounds__(256)
     permute_kernel(const __nv_bfloat16* __restrict__ x, const int32_t* __restrict__ idx,
                    const int32_t* __restrict__ route, const int32_t* __restrict__ counts_all,
-                   const uint32_t* __restrict__ parity, const int32_t* __restrict__ blk_prefix,
+                   const uint32_t* __restrict__ parity, const int32_t* __restrict__ blk_counts,
                    int32_t* const* __restrict__ src_ptrs, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* __restrict__ recv_ptrs, int32_t* __restrict__ pos_dst,
                    int32_t* __restrict__ pos_row, const PeerSync sync) {
@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(256)
   __shared__ int base_s[64];
   __shared__ int wcnt[8][64];  // per-warp, per-expert pair counts -> exclusive prefix over warps
   __shared__ int Mpre[8][64];  // rows of lower experts on GPU D (exclusive prefix over experts)
+  __shared__ int pre4[4][64];  // this origin's rows of each expert in earlier blocks, by segment
   const int b = blockIdx.x;
   const int t0 = b * kTok;
   const int nt = min(kTok, T - t0);
@@ -70,6 +71,22 @@ __global__ void __launch_bounds__(256)
   }
   if (tid < np) s_e[tid] = idx[size_t(t0) * k + tid];
   for (int i = tid; i < 8 * 64; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  {  // block prefix: thread (segment, expert) sums blocks seg, seg + 4, ... below b
+    const int e = tid & 63, seg = tid >> 6;
+    int sum = 0;
+    if (e < E)
+      for (int b0 = seg; b0 < b; b0 += 32) {
+        int v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int bb = b0 + 4 * u;
+          v[u] = bb < b ? __ldcg(blk_counts + size_t(bb) * E + e) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum += v[u];
+      }
+    pre4[seg][e] = sum;
+  }
   __syncthreads();
   // receive layout of every GPU D: rows of expert e2 on D = sum over sources routing e2 to D;
   // warp D scans them over the experts (exclusive), so each expert's base is O(G) work
@@ -101,7 +118,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (tid < E) {
     const int e = tid, D = R[rank][e];
-    int base = blk_prefix[size_t(b) * E + e] + Mpre[D][e];
+    int base = pre4[0][e] + pre4[1][e] + pre4[2][e] + pre4[3][e] + Mpre[D][e];
     for (int s = 0; s < rank; ++s)
       if (R[s][e] == D) base += C[s][e];
     base_s[e] = base;
@@ -192,7 +209,7 @@ __global__ void __launch_bounds__(256)
 }
 
 int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
-                   const uint32_t* parity, const int32_t* blk_prefix, int32_t* const* src_ptrs, int rank, int G,
+                   const uint32_t* parity, const int32_t* blk_counts, int32_t* const* src_ptrs, int rank, int G,
                    int T, int d, int E, int k,
                    __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream,
                    const PeerSync* sync) {
@@ -213,7 +230,7 @@ int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* ro
   if (ps.total > 0) ps.total = grid * ny;
   cudaError_t e;
 #define MP_PERM_LAUNCH(N)                                                                                    \
-  e = launch_pdl(permute_kernel<N>, dim3(grid, ny), dim3(256), 0, stream, x, idx, route, counts_all, parity, blk_prefix, \
+  e = launch_pdl(permute_kernel<N>, dim3(grid, ny), dim3(256), 0, stream, x, idx, route, counts_all, parity, blk_counts, \
                  src_ptrs, rank, G, T, d, E, k, recv_ptrs, pos_dst, pos_row, ps)
   if (vpl <= 1) MP_PERM_LAUNCH(1);
   else if (vpl <= 2) MP_PERM_LAUNCH(2);

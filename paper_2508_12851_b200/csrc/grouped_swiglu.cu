@@ -650,30 +650,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
 }
 
 // ------------------------------------------------------------------ host side
-int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
-  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static EncodeFn fn = nullptr;
-  if (!fn) {
+namespace {
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn tmap_encoder() {
+  static const EncodeFn fn = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !p)
-      return set_error(MP_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-    fn = reinterpret_cast<EncodeFn>(p);
-  }
-  if (cols % 64 != 0) return set_error(MP_E_SHAPE, "tensor map inner dimension %llu not a multiple of 64",
-                                       (unsigned long long)cols);
+        q != cudaDriverEntryPointSuccess)
+      return EncodeFn(nullptr);
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+// 2-D map with a 128-byte inner box and SWIZZLE_128B (the UMMA K-major layout)
+int encode_tmap_2d(CUtensorMap* map, CUtensorMapDataType dt, int esize, const void* ptr, uint64_t rows, uint64_t cols,
+                   uint32_t box_rows) {
+  const EncodeFn fn = tmap_encoder();
+  if (!fn) return set_error(MP_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const uint64_t inner = 128 / esize;
+  if (cols % inner != 0)
+    return set_error(MP_E_SHAPE, "tensor map inner dimension %llu not a multiple of %llu", (unsigned long long)cols,
+                     (unsigned long long)inner);
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint64_t strides[1] = {cols * esize};
+  cuuint32_t box[2] = {uint32_t(inner), box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(MP_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return MP_OK;
+}
+}  // namespace
+
+int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  return encode_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ptr, rows, cols, box_rows);
+}
+int encode_tmap_u8_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  return encode_tmap_2d(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, ptr, rows, cols, box_rows);
 }
 
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,

@@ -83,26 +83,24 @@ struct DeviceGuard {
   }
 };
 
-// ---- K1 router
-int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
+// ---- K1 router (tensor-core exact-integer logits; contract in router.cu)
+int launch_router(const __nv_bfloat16* x, const uint8_t* packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
-                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync = nullptr,
-                  const float* w32 = nullptr, float* partial = nullptr);
-// Partial-logit scratch the router needs for T tokens ([lane groups][T][E_pad] floats).
-size_t router_partial_floats(int T, int d, int E_tot);
-__host__ __device__ int router_lane_groups(int d);
-// Wg pre-converted to fp32 in the router's consumption order (E_pad * d floats).
-int launch_router_pack32(const __nv_bfloat16* wg, int E_tot, int d, float* w32, cudaStream_t stream);
+                  int32_t* count_acc, cudaStream_t stream, const PeerSync* sync = nullptr);
 int launch_router_logits(const float* logits, int ld, const float* bias, int T, int E, int k, int score_mode,
                          int renorm, int32_t* idx, float* w, uint32_t* hist, cudaStream_t stream);
 int router_block_tokens();
-__host__ __device__ int router_e_pad(int E_tot);
-int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16* packed, cudaStream_t stream);
+__host__ __device__ int router_n_pad(int E_tot);
+// Bytes of the packed router operand of E_tot weight rows ([3][N][d] limbs | R[N] | E[N]).
+size_t router_packed_bytes(int E_tot, int d);
+int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, uint8_t* packed, cudaStream_t stream);
+// K ranges (CTAs per 128-token tile) the router uses for T tokens.
+int router_split(int T, int d);
 
 // ---- K2 permute (+ dispatch through peer pointers)
 int launch_permute(const __nv_bfloat16* x, const int32_t* idx, const int32_t* route, const int32_t* counts_all,
-                   const uint32_t* parity, const int32_t* blk_prefix, int32_t* const* src_ptrs, int rank, int G, int T, int d, int E, int k,
+                   const uint32_t* parity, const int32_t* blk_counts, int32_t* const* src_ptrs, int rank, int G, int T, int d, int E, int k,
                    __nv_bfloat16* const* recv_ptrs, int32_t* pos_dst, int32_t* pos_row, cudaStream_t stream,
                    const PeerSync* sync = nullptr);
 
@@ -131,6 +129,8 @@ struct alignas(64) AuxProblem {
   int m = 0, N = 0, K = 0;        // m == 0: no aux problem
 };
 int encode_tmap_bf16_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
+// 8-bit elements, 128-byte inner box, SWIZZLE_128B
+int encode_tmap_u8_2d(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint32_t box_rows);
 int launch_grouped_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GroupSpec& gs, int N, int K,
                         int b_slot_stride, int b_offset,
                         __nv_bfloat16* out, int out_ld, int swiglu, int grid, cudaStream_t stream,

@@ -5,33 +5,44 @@
 // activation counts by ActivationStats.ingest (reference
 // pkg/src/moeplace/stats.py:82-96).  This kernel produces both from real
 // activations in one pass over x:
-//   logits[t,e] = sum_k x[t,k] * Wg[e,k]  (+ bias[e])
+//   logits[t,e] = <x[t], Wg[e]>  (+ bias[e])       -- exact contract below
 //   idx[t,:]    = top-k experts by logit, descending, ties -> lower expert id
 //   w[t,:]      = softmax weights (mode 0: softmax over the k selected logits,
 //                 Mixtral; mode 1: softmax over all E, no renorm unless asked,
 //                 Qwen1.5-MoE / DeepSeek-V2-Lite)
 //   hist[e]    += #tokens whose top-k contains e   (token_count = 1 per token)
 //
-// Bit-exactness contract (restated by oracle/moe_oracle.py:router_logits):
-//   * L = 32 n_lg logical lanes, n_lg = router_lane_groups(d) in {1, 2, 4}; lane
-//     (g, l) owns the k-slices [8 L s + 8 (32 g + l), +8), s = 0..d/(8L)-1 -- i.e.
-//     the 256-k steps g, g + n_lg, g + 2 n_lg, ... at offset 8 l; its partial is ONE
-//     sequential fp32 FMA chain over those k ascending, from 0; x and Wg are bf16, so
-//     each product is exact and fma == rn(acc + x*w);
-//   * inside a group the 32 partials are combined by the butterfly tree
-//     p[l] <- p[l] + p[l + o] for o = 16, 8, 4, 2, 1 (fp add is commutative, so a
-//     warp reduce-scatter yields exactly this tree); the group sums by
-//     q[g] <- q[g] + q[g + o], o = n_lg/2 .. 1; then + bias[e];
-//   * selection compares logits only (independent of the exp implementation).
+// Numerics contract (restated by oracle/moe_oracle.py:router_logits).  Every row
+// a of x and of Wg (bf16) is put on an integer grid fixed by the row's largest
+// magnitude:  E(a) = max(ef(max_k |a_k|) - 126, -100)  (ef = the bf16 exponent
+// field, so max |a| < 2^E(a)),  q_k = rint(a_k * 2^(win - E(a)))  (round half to
+// even), win = 21 for token rows and 14 for router-weight rows: |q| <= 2^win, and
+// every bf16 element within 2^-13 (x) / 2^-6 (Wg) of its row maximum is exact.  Then
+//   S[t,e]      = sum_k qx[t,k] * qw[e,k]          EXACT (an integer, |S| < 2^52)
+//   logits[t,e] = f32( f64(rn_f32(S)) * 2^(E(x_t) + E(w_e) - 35) ) (+ bias[e], fp32)
+// S is computed on the tensor cores from 8-bit limbs (x: three unsigned limbs of
+// q + 2^22, Wg: two balanced signed limbs) with tcgen05.mma.kind::i8 into s32
+// accumulators in TMEM -- integer arithmetic is associative, so the result does
+// not depend on tile shapes, K splits or accumulation order, and the logits are
+// bit-reproducible by any exact method.  The quantisation error (<= 2^-22 of the
+// token row maximum, 2^-15 of the weight row maximum, per element) sits between
+// fp32 and bf16 rounding.
 //
-// Two kernels.  router_chain_kernel: persistent over every SM, one warp per unit =
-// (8-expert pass, lane group, 4-token quad) -- 4 x 8 = 32 accumulators per lane as
-// 16 FFMA2 chains while the lanes walk the group's k-steps (x straight from HBM,
-// 512 B coalesced per token per step; Wg fp32 in consumption order through L1/L2);
-// a reduce-scatter leaves lane l holding (token l/8, expert l%8), stored as a group
-// partial.  Lane groups split d so that even one expert pass (Mixtral) yields enough
-// units to fill the SMs.  router_select_kernel: one CTA per 32-token block combines
-// the partials by the contract's tree and runs top-k, weights and the histogram.
+// Kernel (router_i8_kernel): a cluster of `split` CTAs per 128-token tile, each
+// CTA one contiguous K range of d:
+//   1. every CTA reads its x range once for the per-token maxima; the maxima go to
+//      every CTA of the cluster through DSMEM, so all CTAs share E(x_t);
+//   2. the CTA re-reads its x range (L2) and writes three limb tiles per 128-k block
+//      straight into shared memory in the UMMA SWIZZLE_128B K-major layout (limb
+//      j = byte j of the fp32 pattern of q + 1.5 * 2^23: an FFMA and byte permutes);
+//      both Wg limbs arrive by one TMA as a [2N][128] tile; one thread issues one MMA
+//      per (32-k step, x limb) with N' = 2N (each x limb tile is read once per step);
+//   3. the epilogue folds the six accumulators into int64 per (token, expert), the
+//      cluster sums its K ranges through DSMEM (integer, exact), and each 32-token
+//      router block is selected by one CTA: one warp per token, top-k by two
+//      redux.sync rounds, gate weights, block histogram; the last CTA of the grid
+//      produces the batch counts, the per-block prefix the permute needs and, at
+//      G > 1, the count exchange with epoch A.
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
@@ -43,13 +54,24 @@
 namespace mp {
 
 namespace rt {
-constexpr int kTokens = 32;    // tokens per CTA (also the permute / histogram block)
+constexpr int kTokens = 32;    // tokens per router block (the permute / histogram block)
 constexpr int kMaxE = 64;      // routed experts
 constexpr int kMaxK = 8;
+constexpr int kWinX = 21;      // token rows: |q| <= 2^21 (three unsigned limbs, the top one biased)
+constexpr int kWinW = 14;      // Wg rows:    |q| <= 2^14 (two balanced signed limbs)
+constexpr int kMinExp = -100;  // E(a) floor: 2^(win - E) stays a normal fp32
+constexpr float kMagic = 12582912.0f;           // 1.5 * 2^23
+constexpr uint32_t kMagicBits = 0x4B400000u;    // its bit pattern
 }  // namespace rt
 
 int router_block_tokens() { return rt::kTokens; }
-__host__ __device__ int router_e_pad(int E_tot) { return (E_tot + 7) / 8 * 8; }
+// MMA N: routed experts + gate row, rounded up to a multiple of 16
+__host__ __device__ int router_n_pad(int E_tot) { return E_tot <= 16 ? 16 : (E_tot + 15) / 16 * 16; }
+
+size_t router_packed_bytes(int E_tot, int d) {
+  const size_t N = size_t(router_n_pad(E_tot));
+  return 2 * N * size_t(d) + 8 * N + 4 * N;
+}
 
 #define MP_TRY_R(call)             \
   do {                             \
@@ -57,64 +79,64 @@ __host__ __device__ int router_e_pad(int E_tot) { return (E_tot + 7) / 8 * 8; }
     if (_r != MP_OK) return _r;    \
   } while (0)
 
-// packed[E_pad][d] bf16 = Wg (zero rows pad E_tot up to a multiple of 8)
-__global__ void router_pack_kernel(const __nv_bfloat16* __restrict__ wg, int E_tot, int E_pad, int d,
-                                   __nv_bfloat16* __restrict__ packed) {
-  const size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;  // over E_pad * d
-  if (i >= size_t(E_pad) * d) return;
-  packed[i] = i < size_t(E_tot) * d ? wg[i] : __float2bfloat16(0.0f);
+// E(a) from the largest |bf16| bit pattern of a row.
+MP_DEV int row_exponent(uint32_t max_bits) { return max(int(max_bits >> 7) - 126, rt::kMinExp); }
+// 2^(win - E) as fp32 bits
+MP_DEV float row_scale(int e, int win) { return __uint_as_float(uint32_t(127 + win - e) << 23); }
+// bit pattern of rn(a * scale + 1.5 * 2^23) = 0x4B400000 + rint(a * scale)
+MP_DEV uint32_t quant_bits(float a, float scale) { return __float_as_uint(fmaf(a, scale, rt::kMagic)); }
+
+// ---------------------------------------------------------------- Wg packing
+// packed = [2][N][d] limbs | int64 R[N] | int32 E[N]: q = b0 + 2^8 b1 with balanced signed
+// digits b0, b1 in [-128, 127] (|q| <= 2^14), R[e] = sum_k q[e][k].  Pad rows (e >= E_tot)
+// are zero.  One CTA per row.
+__global__ void __launch_bounds__(256) router_pack_kernel(const __nv_bfloat16* __restrict__ wg, int E_tot, int N,
+                                                          int d, uint8_t* __restrict__ packed) {
+  const int e = blockIdx.x, tid = threadIdx.x;
+  const uint16_t* row = reinterpret_cast<const uint16_t*>(wg) + size_t(e) * d;
+  const bool real = e < E_tot;
+  __shared__ uint32_t mx_s[8];
+  __shared__ long long sum_s[8];
+  uint32_t m = 0;
+  if (real)
+    for (int k = tid; k < d; k += blockDim.x) m = max(m, uint32_t(row[k] & 0x7fffu));
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((tid & 31) == 0) mx_s[tid >> 5] = m;
+  __syncthreads();
+  m = 0;
+  for (int i = 0; i < 8; ++i) m = max(m, mx_s[i]);
+  const int ex = row_exponent(m);
+  const float sc = row_scale(ex, rt::kWinW);
+  long long s = 0;
+  for (int k = tid; k < d; k += blockDim.x) {
+    int q = 0;
+    if (real) q = int(quant_bits(__uint_as_float(uint32_t(row[k]) << 16), sc) - rt::kMagicBits);
+    s += q;
+    const int b0 = ((q + 128) & 255) - 128, b1 = (q - b0) / 256;
+    packed[(size_t(0) * N + e) * d + k] = uint8_t(int8_t(b0));
+    packed[(size_t(1) * N + e) * d + k] = uint8_t(int8_t(b1));
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((tid & 31) == 0) sum_s[tid >> 5] = s;
+  __syncthreads();
+  if (tid == 0) {
+    long long tot = 0;
+    for (int i = 0; i < 8; ++i) tot += sum_s[i];
+    reinterpret_cast<long long*>(packed + 2 * size_t(N) * d)[e] = tot;
+    reinterpret_cast<int*>(packed + 2 * size_t(N) * d + 8 * size_t(N))[e] = real ? ex : 0;
+  }
 }
 
-int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, __nv_bfloat16* packed, cudaStream_t stream) {
+int launch_router_pack(const __nv_bfloat16* wg, int E_tot, int d, uint8_t* packed, cudaStream_t stream) {
   if (d % 256 != 0) return set_error(MP_E_SHAPE, "router d=%d not a multiple of 256", d);
-  const int E_pad = router_e_pad(E_tot);
-  const size_t n = size_t(E_pad) * d;
-  router_pack_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(wg, E_tot, E_pad, d, packed);
+  if (E_tot < 1 || E_tot > rt::kMaxE + 1) return set_error(MP_E_SHAPE, "router: %d weight rows", E_tot);
+  const int N = router_n_pad(E_tot);
+  router_pack_kernel<<<unsigned(N), 256, 0, stream>>>(wg, E_tot, N, d, packed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_pack_kernel launch");
 }
 
-// Wg pre-converted to fp32 in the order the router's lanes consume it: float4
-// number t of lane l in (pass, step) sits at ((pass * S + step) * 16 + t) * 32 + l
-// (a warp's load of float4 t is 512 contiguous bytes) and holds experts
-// 8 pass + 4 (t & 1) .. +3 at k = 256 step + 8 l + (t >> 1) -- two
-// (expert 2i, 2i+1) pairs ready for FFMA2, no bf16 conversions in the FMA loop.
-// Same products and chains as the bf16 path (bit-identical logits).
-__global__ void router_pack32_kernel(const __nv_bfloat16* __restrict__ wg, int E_tot, int E_pad, int d,
-                                     float* __restrict__ w32) {
-  const size_t o = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (o >= size_t(E_pad) * d) return;
-  const int S = d / 256;
-  const int i = int(o & 3), l = int((o >> 2) & 31), t = int((o >> 7) & 15);
-  const size_t rest = o >> 11;  // pass * S + step
-  const int st = int(rest % S), p = int(rest / S);
-  const int e = 8 * p + 4 * (t & 1) + i, kk = 256 * st + 8 * l + (t >> 1);
-  w32[o] = e < E_tot ? __bfloat162float(wg[size_t(e) * d + kk]) : 0.0f;
-}
-
-int launch_router_pack32(const __nv_bfloat16* wg, int E_tot, int d, float* w32, cudaStream_t stream) {
-  if (d % 256 != 0) return set_error(MP_E_SHAPE, "router d=%d not a multiple of 256", d);
-  const size_t n = size_t(router_e_pad(E_tot)) * d;
-  router_pack32_kernel<<<unsigned((n + 255) / 256), 256, 0, stream>>>(wg, E_tot, router_e_pad(E_tot), d, w32);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_pack32_kernel launch");
-}
-
-// acc = (acc.lo + x*w.lo, acc.hi + x*w.hi): two independent fp32 FMAs (FFMA2),
-// each rounded exactly like fmaf -- the per-lane chain contract is unchanged.
-MP_DEV void ffma2(unsigned long long& acc, float x, unsigned long long w) {
-  const unsigned long long xx = (unsigned long long)__float_as_uint(x) | ((unsigned long long)__float_as_uint(x) << 32);
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xx), "l"(w));
-}
-MP_DEV unsigned long long pack2(float lo, float hi) {
-  return (unsigned long long)__float_as_uint(lo) | ((unsigned long long)__float_as_uint(hi) << 32);
-}
-
-// Warp-collective top-k + gate weights of one token from its logits (lane l holds
-// experts l and l + 32): k rounds of a warp arg-max -- larger logit, ties -> lower id,
-// as two redux.sync reductions over order-preserving keys -- then softmax over the k
-// (mode 0) or over all E (mode 1, optional renormalisation).  Lane j < k writes
-// idx_row[j] / w_row[j] and bumps cnt_s.
+// ---------------------------------------------------------------- selection
 // Order-preserving 32-bit key of an fp32 logit (-0 canonicalised to +0, so equal logits get
 // equal keys): larger logit <=> larger unsigned key.
 MP_DEV uint32_t logit_key(float v) {
@@ -122,455 +144,102 @@ MP_DEV uint32_t logit_key(float v) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-MP_DEV void select_topk_store(float v0, float v1, int E, int k, int score_mode, int renorm, int32_t* idx_row,
-                              float* w_row, int* cnt_s) {
+// Warp-collective top-k + gate weights of NT tokens in lockstep (their warp reductions are
+// independent, so they pipeline) from their logits (lane l holds experts l and l + 32 of token
+// i in v0[i], v1[i]): k rounds of a warp arg-max -- larger logit, ties -> lower id, as two
+// redux.sync reductions over order-preserving keys -- then softmax over the k (mode 0) or
+// over all E (mode 1, optional renormalisation).  Lane j < k writes idx_row[i][j] /
+// w_row[i][j] and bumps cnt_s.  Tokens with valid[i] == false only ride along.
+template <int NT>
+MP_DEV void select_topk_store(const float (&v0)[NT], const float (&v1)[NT], const bool (&valid)[NT], int E, int k,
+                              int score_mode, int renorm, int32_t* const (&idx_row)[NT],
+                              float* const (&w_row)[NT], int* cnt_s) {
   const int lane = lane_id();
   // candidates of this lane: expert lane (v0) and lane + 32 (v1); taken/absent -> key 0
-  uint32_t k0 = lane < E ? logit_key(v0) : 0u, k1 = lane + 32 < E ? logit_key(v1) : 0u;
-  float my_v = -INFINITY, mx = 0.f;  // lane j < k keeps the j-th selected logit and expert
-  int my_i = 0;
+  uint32_t k0[NT], k1[NT];
+  float my_v[NT], mx[NT];  // lane j < k keeps the j-th selected logit and expert
+  int my_i[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    k0[i] = lane < E ? logit_key(v0[i]) : 0u;
+    k1[i] = lane + 32 < E ? logit_key(v1[i]) : 0u;
+    my_v[i] = -INFINITY;
+    mx[i] = 0.f;
+    my_i[i] = 0;
+  }
 #pragma unroll 1
   for (int j = 0; j < k; ++j) {
-    // round j: the largest key over the warp (redux), then the lowest expert id holding it
-    const bool use1 = k1 > k0;  // ties inside the lane: the lower id (lane) wins
-    const uint32_t bk = use1 ? k1 : k0;
-    const uint32_t mk = __reduce_max_sync(0xffffffffu, bk);
-    const uint32_t cand = (bk == mk && mk != 0u) ? uint32_t(use1 ? lane + 32 : lane) : 0xffffffffu;
-    const uint32_t bi = __reduce_min_sync(0xffffffffu, cand);
-    const float bv = __shfl_sync(0xffffffffu, bi >= 32 ? v1 : v0, bi & 31);
-    if (j == 0) mx = bv;
-    if (lane == j) { my_v = bv; my_i = int(bi); }
-    if (bi == uint32_t(lane)) k0 = 0u;
-    if (bi == uint32_t(lane + 32)) k1 = 0u;
+    uint32_t bk[NT], bi[NT];
+    bool use1[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      use1[i] = k1[i] > k0[i];  // ties inside the lane: the lower id (lane) wins
+      bk[i] = use1[i] ? k1[i] : k0[i];
+    }
+    uint32_t mk[NT];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) mk[i] = __reduce_max_sync(0xffffffffu, bk[i]);
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      const uint32_t cand = (bk[i] == mk[i] && mk[i] != 0u) ? uint32_t(use1[i] ? lane + 32 : lane) : 0xffffffffu;
+      bi[i] = __reduce_min_sync(0xffffffffu, cand);
+    }
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      const float bv = __shfl_sync(0xffffffffu, bi[i] >= 32 ? v1[i] : v0[i], bi[i] & 31);
+      if (j == 0) mx[i] = bv;
+      if (lane == j) { my_v[i] = bv; my_i[i] = int(bi[i]); }
+      if (bi[i] == uint32_t(lane)) k0[i] = 0u;
+      if (bi[i] == uint32_t(lane + 32)) k1[i] = 0u;
+    }
   }
   // weights: lane j < k owns w_j
-  const float ej = lane < k ? expf(my_v - mx) : 0.f;
-  float denom;
-  if (score_mode == 0) {
-    denom = ej;
+  float ej[NT], denom[NT];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, off);
-  } else {
-    float sum = (lane < E ? expf(v0 - mx) : 0.f) + (lane + 32 < E ? expf(v1 - mx) : 0.f);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
-    denom = sum;
+  for (int i = 0; i < NT; ++i) {
+    ej[i] = lane < k ? __expf(my_v[i] - mx[i]) : 0.f;
+    denom[i] = score_mode == 0 ? ej[i]
+                               : (lane < E ? __expf(v0[i] - mx[i]) : 0.f) + (lane + 32 < E ? __expf(v1[i] - mx[i]) : 0.f);
   }
-  float wj = ej / denom;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int i = 0; i < NT; ++i) denom[i] += __shfl_xor_sync(0xffffffffu, denom[i], off);
+  float wj[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) wj[i] = __fdividef(ej[i], denom[i]);
   if (score_mode == 1 && renorm) {
-    float wsum = wj;
+    float wsum[NT];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, off);
-    wj = wj / wsum;
+    for (int i = 0; i < NT; ++i) wsum[i] = wj[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int i = 0; i < NT; ++i) wsum[i] += __shfl_xor_sync(0xffffffffu, wsum[i], off);
+#pragma unroll
+    for (int i = 0; i < NT; ++i) wj[i] = __fdividef(wj[i], wsum[i]);
   }
-  if (lane < k) {
-    idx_row[lane] = my_i;
-    w_row[lane] = wj;
-    atomicAdd(&cnt_s[my_i], 1);
-  }
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+    if (lane < k && valid[i]) {
+      idx_row[i][lane] = my_i[i];
+      w_row[i][lane] = wj[i];
+      atomicAdd(&cnt_s[my_i[i]], 1);
+    }
 }
 
-constexpr int kTokPerWarp = 4;  // a chain unit: 4 tokens (one quad) x 8 experts (one pass)
-constexpr int kExpPerPass = 8;
-constexpr int kChainWarps = 16;  // warps per CTA of the chain kernel
-
-// Lane groups of the numerics contract (oracle.router_lane_groups): with n_lg groups
-// of 32 logical lanes, the chain of lane (g, l) walks the 256-k steps g, g + n_lg, ...
-// so every unit of work is one 32-lane warp over d / n_lg of the k range.
-__host__ __device__ int router_lane_groups(int d) {
-  if (d >= 4096 && d % 1024 == 0) return 4;
-  if (d >= 2048 && d % 512 == 0) return 2;
-  return 1;
-}
-
-// Stage 1 (chains).  Unit = (expert pass p, lane group g, token quad q): one warp keeps
-// 4 tokens x 8 experts = 16 FFMA2 accumulator pairs per lane while its lanes walk the
-// group's k-steps (x: 512 B coalesced per token per step, straight from HBM; Wg: the
-// fp32 consumption-order operand or the bf16 rows, through L1/L2).  A reduce-scatter
-// butterfly leaves lane l holding the group partial of (token l/8, expert l%8), stored
-// to partial[g][t][E_pad].  Persistent: warps stride over the units, quads fastest.
-template <bool kW32>
-__global__ void __launch_bounds__(kChainWarps * 32, 1)
-    router_chain_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wp,
-                        const float4* __restrict__ w32, int T, int d, int E_pad, int n_lg,
-                        float* __restrict__ partial) {
-  griddep_launch_dependents();
-  griddep_wait();
-  const int lane = lane_id();
-  const int n_quads = (T + kTokPerWarp - 1) / kTokPerWarp;
-  const int n_pass = E_pad / kExpPerPass;
-  const int S_all = d / 256;          // 256-k steps in d
-  const int S = S_all / n_lg;         // steps of one lane group's chain
-  const int n_units = n_quads * n_pass * n_lg;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + warp_id();
-  const int n_warps = gridDim.x * (blockDim.x >> 5);
-  for (int u = gw; u < n_units; u += n_warps) {
-    const int q = u % n_quads, pg = u / n_quads;
-    const int g = pg % n_lg, pass = pg / n_lg;
-    const int t0 = q * kTokPerWarp;
-    const __nv_bfloat16* xr[kTokPerWarp];
-#pragma unroll
-    for (int i = 0; i < kTokPerWarp; ++i)
-      xr[i] = x + size_t(t0 + i < T ? t0 + i : 0) * d + 256 * g + 8 * lane;  // rows past T: discarded
-    unsigned long long acc[kTokPerWarp][kExpPerPass / 2];
-#pragma unroll
-    for (int i = 0; i < kTokPerWarp; ++i)
-#pragma unroll
-      for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
-    if (kW32) {
-      // fp32 pairs straight from the pre-converted Wg (two halves of 4 k each); the
-      // step of this group's chain number s is the 256-k step g + n_lg * s
-      const float4* w4 = w32 + (size_t(pass) * S_all + g) * 16 * 32 + lane;
-      uint4 xv[kTokPerWarp], xn[kTokPerWarp];
-#pragma unroll
-      for (int i = 0; i < kTokPerWarp; ++i) xv[i] = ld_nc_v4(xr[i]);
-#pragma unroll 1
-      for (int s = 0; s < S; ++s, w4 += size_t(n_lg) * 16 * 32) {
-        // the next step's x rows are in flight while this step's FFMA2 chains run
-        if (s + 1 < S) {
-#pragma unroll
-          for (int i = 0; i < kTokPerWarp; ++i) xn[i] = ld_nc_v4(xr[i] + size_t(256) * n_lg * (s + 1));
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float4 wv[8];
-#pragma unroll
-          for (int t2 = 0; t2 < 8; ++t2) wv[t2] = __ldg(w4 + (8 * h + t2) * 32);
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {  // strictly ascending k inside the lane's slice
-            const int qk = 4 * h + qq;
-            float xs[kTokPerWarp];
-#pragma unroll
-            for (int i = 0; i < kTokPerWarp; ++i) {
-              const uint32_t uu = (&xv[i].x)[qk >> 1];
-              xs[i] = (qk & 1) ? bf16_hi(uu) : bf16_lo(uu);
-            }
-            const float4 a = wv[2 * qq], b = wv[2 * qq + 1];
-            const unsigned long long w2[4] = {pack2(a.x, a.y), pack2(a.z, a.w), pack2(b.x, b.y), pack2(b.z, b.w)};
-#pragma unroll
-            for (int j = 0; j < kExpPerPass / 2; ++j)
-#pragma unroll
-              for (int i = 0; i < kTokPerWarp; ++i) ffma2(acc[i][j], xs[i], w2[j]);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < kTokPerWarp; ++i) xv[i] = xn[i];
-      }
-    } else {
-      const __nv_bfloat16* wr = wp + size_t(kExpPerPass) * pass * d + 256 * g + 8 * lane;
-#pragma unroll 1
-      for (int s = 0; s < S; ++s) {
-        const size_t ko = size_t(256) * n_lg * s;
-        uint4 xv[kTokPerWarp], wv[kExpPerPass];
-#pragma unroll
-        for (int i = 0; i < kTokPerWarp; ++i) xv[i] = ld_nc_v4(xr[i] + ko);
-#pragma unroll
-        for (int j = 0; j < kExpPerPass; ++j) wv[j] = __ldg(reinterpret_cast<const uint4*>(wr + size_t(j) * d + ko));
-#pragma unroll
-        for (int qk = 0; qk < 8; ++qk) {  // strictly ascending k inside the lane's slice
-          float xs[kTokPerWarp];
-#pragma unroll
-          for (int i = 0; i < kTokPerWarp; ++i) {
-            const uint32_t uu = (&xv[i].x)[qk >> 1];
-            xs[i] = (qk & 1) ? bf16_hi(uu) : bf16_lo(uu);
-          }
-#pragma unroll
-          for (int j = 0; j < kExpPerPass / 2; ++j) {
-            const uint32_t u0 = (&wv[2 * j].x)[qk >> 1], u1 = (&wv[2 * j + 1].x)[qk >> 1];
-            const unsigned long long w2 =
-                (qk & 1) ? pack2(bf16_hi(u0), bf16_hi(u1)) : pack2(bf16_lo(u0), bf16_lo(u1));
-#pragma unroll
-            for (int i = 0; i < kTokPerWarp; ++i) ffma2(acc[i][j], xs[i], w2);
-          }
-        }
-      }
-    }
-    // butterfly reduce-scatter over the 32 lane partials of 32 values
-    // (value v = token v/8, expert v%8); afterwards lane l holds value l
-    float v[32];
-#pragma unroll
-    for (int i = 0; i < kTokPerWarp; ++i)
-#pragma unroll
-      for (int j = 0; j < kExpPerPass / 2; ++j) {
-        v[i * 8 + 2 * j] = __uint_as_float(uint32_t(acc[i][j]));
-        v[i * 8 + 2 * j + 1] = __uint_as_float(uint32_t(acc[i][j] >> 32));
-      }
-#pragma unroll
-    for (int o = 16, n = 32; o >= 1; o >>= 1, n >>= 1) {
-      const bool upper = (lane & o) != 0;
-#pragma unroll
-      for (int i = 0; i < n / 2; ++i) {
-        const float send = upper ? v[i] : v[i + n / 2];
-        const float keep = upper ? v[i + n / 2] : v[i];
-        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-      }
-    }
-    const int tt = t0 + (lane >> 3);
-    if (tt < T) partial[(size_t(g) * T + tt) * E_pad + kExpPerPass * pass + (lane & 7)] = v[0];
-  }
-}
-
-// Stage 1, octet form (the layer's default).  Unit = (expert pass p, lane group g, token
-// octet o): one warp keeps 8 tokens x 8 experts = 32 FFMA2 accumulator pairs per lane, so
-// every Wg value a lane loads feeds 8 tokens (half the L1 traffic per FMA of the quad form).
-// Wg comes as bf16 rows [E_pad][d] (one uint4 = 8 k of one expert per lane and step); the
-// pair (e, e + 1) at one k is two ALU ops.  With one warp's 32 x 8 accumulators the register
-// file holds only 8 warps per SM, too few to hide load latency, so every lane streams its own
-// operands (8 x rows + 8 Wg rows, 16 B each per step) through a kStages-deep shared-memory
-// ring with cp.async, running ahead across unit boundaries -- a lane only ever reads back the
-// bytes it copied itself, so no warp or CTA synchronisation is involved.  Same chains, same
-// butterfly, same partial layout as the quad form.
-constexpr int kOctTok = 8;
-constexpr int kOctWarps = 8;
-constexpr int kOctStages = 3;
-constexpr int kOctChunks = kOctTok + kExpPerPass;  // 16-B chunks per lane and step
-constexpr size_t kOctSmem = size_t(kOctWarps) * kOctStages * kOctChunks * 32 * 16;  // 192 KB
-
-__global__ void __launch_bounds__(kOctWarps * 32, 1)
-    router_chain8_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wp, int T, int d,
-                         int E_pad, int n_lg, float* __restrict__ partial) {
-  extern __shared__ __align__(16) uint8_t ring_raw[];
-  griddep_launch_dependents();
-  griddep_wait();
-  const int lane = lane_id(), warp = warp_id();
-  // this lane's ring: [stage][chunk] 16-B slots, lane-interleaved (conflict-free LDS.128)
-  uint4* ring = reinterpret_cast<uint4*>(ring_raw) + size_t(warp) * kOctStages * kOctChunks * 32 + lane;
-  const int n_oct = (T + kOctTok - 1) / kOctTok;
-  const int n_pass = E_pad / kExpPerPass;
-  const int S = d / 256 / n_lg;
-  const int n_units = n_oct * n_pass * n_lg;
-  const int gw = blockIdx.x * kOctWarps + warp;
-  const int n_warps = gridDim.x * kOctWarps;
-  // (unit, step) pairs of this warp in order: unit u_i = gw + i * n_warps, steps 0..S-1
-  const int my_units = gw < n_units ? (n_units - 1 - gw) / n_warps + 1 : 0;
-  const int total = my_units * S;
-  // producer cursor: the (unit, step) whose copies are issued next, with its row / Wg bases
-  // recomputed only when it crosses into the next unit
-  int f_s = 0, f_u = gw;
-  const __nv_bfloat16* fx = nullptr;   // x row of the octet's first token at this step and lane
-  const __nv_bfloat16* fw = nullptr;   // Wg row of the pass's first expert at this step and lane
-  uint32_t frow[kOctTok];              // element offsets of the octet's rows from the first one
-  auto unit_bases = [&]() {
-    const int o = f_u % n_oct, pg = f_u / n_oct;
-    const int g = pg % n_lg, pass = pg / n_lg;
-    const int t0 = o * kOctTok;
-    fx = x + size_t(t0) * d + 256 * g + 8 * lane;
-    fw = wp + size_t(kExpPerPass) * pass * d + 256 * g + 8 * lane;
-#pragma unroll
-    for (int i = 0; i < kOctTok; ++i) frow[i] = uint32_t(t0 + i < T ? i : -t0) * uint32_t(d);  // past T: row 0
-  };
-  if (total > 0) unit_bases();
-  const size_t step_elems = size_t(256) * n_lg;
-  int f_slot = 0;
-  auto fetch = [&]() {  // issue the copies of the producer's (unit, step) into its ring stage
-    uint4* slot = ring + size_t(f_slot) * kOctChunks * 32;
-    const __nv_bfloat16* xs = fx + step_elems * f_s;
-    const __nv_bfloat16* ws = fw + step_elems * f_s;
-#pragma unroll
-    for (int i = 0; i < kOctTok; ++i) cp_async_16(slot + i * 32, xs + int32_t(frow[i]));
-#pragma unroll
-    for (int j = 0; j < kExpPerPass; ++j) cp_async_16(slot + (kOctTok + j) * 32, ws + size_t(j) * d);
-    if (++f_slot == kOctStages) f_slot = 0;
-    if (++f_s == S) {
-      f_s = 0;
-      f_u += n_warps;
-      if (f_u < n_units) unit_bases();
-    }
-  };
-#pragma unroll
-  for (int f = 0; f < kOctStages - 1; ++f) {
-    if (f < total) fetch();
-    cp_async_commit();
-  }
-  unsigned long long acc[kOctTok][kExpPerPass / 2];
-  int c_s = 0, c_u = gw, c_slot = 0;  // consumer cursor
-#pragma unroll 1
-  for (int c = 0; c < total; ++c) {
-    if (c + kOctStages - 1 < total) fetch();
-    cp_async_commit();
-    cp_async_wait<kOctStages - 1>();  // this lane's copies of step c have landed
-    const int s = c_s;
-    if (s == 0) {
-#pragma unroll
-      for (int i = 0; i < kOctTok; ++i)
-#pragma unroll
-        for (int j = 0; j < kExpPerPass / 2; ++j) acc[i][j] = 0ull;
-    }
-    const uint4* slot = ring + size_t(c_slot) * kOctChunks * 32;
-    if (++c_slot == kOctStages) c_slot = 0;
-    uint4 wv[kExpPerPass];
-#pragma unroll
-    for (int j = 0; j < kExpPerPass; ++j) wv[j] = slot[(kOctTok + j) * 32];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {  // two halves of the octet's x rows
-      uint4 xv[kOctTok / 2];
-#pragma unroll
-      for (int i = 0; i < kOctTok / 2; ++i) xv[i] = slot[(4 * h + i) * 32];
-#pragma unroll
-      for (int qk = 0; qk < 8; ++qk) {  // strictly ascending k inside the lane's slice
-        unsigned long long w2[kExpPerPass / 2];
-#pragma unroll
-        for (int j = 0; j < kExpPerPass / 2; ++j) {
-          const uint32_t u0 = (&wv[2 * j].x)[qk >> 1], u1 = (&wv[2 * j + 1].x)[qk >> 1];
-          w2[j] = (qk & 1) ? pack2(bf16_hi(u0), bf16_hi(u1)) : pack2(bf16_lo(u0), bf16_lo(u1));
-        }
-#pragma unroll
-        for (int i = 0; i < kOctTok / 2; ++i) {
-          const uint32_t uu = (&xv[i].x)[qk >> 1];
-          const float xs = (qk & 1) ? bf16_hi(uu) : bf16_lo(uu);
-#pragma unroll
-          for (int j = 0; j < kExpPerPass / 2; ++j) ffma2(acc[4 * h + i][j], xs, w2[j]);
-        }
-      }
-    }
-    if (++c_s == S) {
-      c_s = 0;
-      const int u = c_u;
-      c_u += n_warps;
-      const int o = u % n_oct, pg = u / n_oct;
-      const int g = pg % n_lg, pass = pg / n_lg;
-      // two butterfly reduce-scatters (tokens 0-3 and 4-7), as in the quad form
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < kExpPerPass / 2; ++j) {
-            v[i * 8 + 2 * j] = __uint_as_float(uint32_t(acc[4 * h + i][j]));
-            v[i * 8 + 2 * j + 1] = __uint_as_float(uint32_t(acc[4 * h + i][j] >> 32));
-          }
-#pragma unroll
-        for (int off = 16, n = 32; off >= 1; off >>= 1, n >>= 1) {
-          const bool upper = (lane & off) != 0;
-#pragma unroll
-          for (int i = 0; i < n / 2; ++i) {
-            const float send = upper ? v[i] : v[i + n / 2];
-            const float keep = upper ? v[i + n / 2] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-          }
-        }
-        const int tt = o * kOctTok + 4 * h + (lane >> 3);
-        if (tt < T) partial[(size_t(g) * T + tt) * E_pad + kExpPerPass * pass + (lane & 7)] = v[0];
-      }
-    }
-  }
-  cp_async_wait<0>();
-}
-
-// Stage 2 (selection).  CTA = one router block of 32 tokens (the histogram / permute
-// block), 32 warps, one warp per token: lane l reads the partials of experts l
-// and l + 32 straight from L2 (all of a warp's loads issued before any is used),
-// combines them by the contract's tree (q[g] += q[g + o], o = n_lg/2..1) + bias, then
-// top-k, gate weights and the block-aggregated histogram; the last CTA produces the
-// batch counts, the block prefix and (G > 1) the count exchange with epoch A.
-MP_DEV float combine_groups(const float* pp, size_t gs, int n_lg) {
-  // pp: the partial of (token, expert) in group 0; gs: stride between groups
-  float v = __ldcg(pp);
-  if (n_lg == 2) {
-    v = v + __ldcg(pp + gs);
-  } else if (n_lg == 4) {  // q[g] += q[g + 2], then q[0] += q[1]
-    const float a1 = __ldcg(pp + gs), a2 = __ldcg(pp + 2 * gs), a3 = __ldcg(pp + 3 * gs);
-    v = (v + a2) + (a1 + a3);
-  }
-  return v;
-}
-
-constexpr int kSelectThreads = rt::kTokens * 32;
-__global__ void __launch_bounds__(kSelectThreads)
-    router_select_kernel(const float* __restrict__ partial, int n_lg, int E_pad, const float* __restrict__ bias,
-                         int T, int E, int has_gate, int k, int score_mode, int renorm, int32_t* __restrict__ idx,
-                         float* __restrict__ wout, float* __restrict__ shared_gate, uint32_t* __restrict__ hist,
-                         int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
-                         uint32_t* __restrict__ ticket, int32_t* __restrict__ blk_prefix, const PeerSync sync,
-                         int stage_counts) {
-  __shared__ int cnt_s[rt::kMaxE];
-  extern __shared__ __align__(128) uint8_t dsm[];  // last CTA: the [nb][E] block counts
-  int* bc = reinterpret_cast<int*>(dsm);
-  const int blk = blockIdx.x, n_blk = gridDim.x;
-  const int t0 = blk * rt::kTokens;
-  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
-  for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
-  const float bz0 = (bias != nullptr && lane < E) ? bias[lane] : 0.f;
-  const float bz1 = (bias != nullptr && lane + 32 < E) ? bias[lane + 32] : 0.f;
-  griddep_launch_dependents();
-  griddep_wait();  // the chain kernel's partials
-  __syncthreads();
-
-  // ---- logits, top-k + weights: one warp per token
-  const size_t gs = size_t(T) * E_pad;
-  auto load = [&](int t, float& a0, float& a1, float& ag) {
-    const float* pp = partial + size_t(min(t, T - 1)) * E_pad;
-    a0 = lane < E ? combine_groups(pp + lane, gs, n_lg) : -INFINITY;
-    a1 = lane + 32 < E ? combine_groups(pp + lane + 32, gs, n_lg) : -INFINITY;
-    ag = has_gate ? combine_groups(pp + E, gs, n_lg) : 0.f;
-  };
-  // one warp per token of the block (32 warps): the selection is a chain of dependent shuffles,
-  // so its latency is hidden by warps, not by work per warp
-  const int t = t0 + warp;
-  if (warp < rt::kTokens && t < T) {
-    float c0, c1, cg;
-    load(t, c0, c1, cg);
-    const float a = (lane < E && bias != nullptr) ? __fadd_rn(c0, bz0) : c0;
-    const float c = (lane + 32 < E && bias != nullptr) ? __fadd_rn(c1, bz1) : c1;
-    select_topk_store(a, c, E, k, score_mode, renorm, idx + size_t(t) * k, wout + size_t(t) * k, cnt_s);
-    if (lane == 0 && has_gate && shared_gate != nullptr) shared_gate[t] = 1.0f / (1.0f + expf(-cg));
-  }
-  __syncthreads();
+// The last CTA of a routing launch (all its threads): the batch counts every CTA added into
+// count_acc (integer sums: order-independent) move to batch_counts and count_acc is reset for
+// the next launch; at G > 1 they are published into every rank's count table and epoch A is
+// raised.  (The per-block prefix the permute needs is its own prologue's job.)
+MP_DEV void router_batch_tail(int E, int32_t* count_acc, int32_t* batch_counts, const PeerSync& sync) {
+  const int tid = threadIdx.x;
+  __shared__ int tot_s[64];
   for (int e = tid; e < E; e += blockDim.x) {
-    const int c = cnt_s[e];
-    if (blk_counts) blk_counts[size_t(blk) * E + e] = c;
-    if (c && hist) atomicAdd(&hist[e], uint32_t(c));
-  }
-  if (batch_counts == nullptr || blk_counts == nullptr) return;
-  // The last CTA to finish reduces the per-block counts into this batch's
-  // per-expert counts (integer sums: order-independent), so they are ready when
-  // the kernel completes -- no memset, no second pass.
-  __shared__ int is_last;
-  // one gpu-scope fence per CTA, from thread 0 after the barrier (cumulative over the CTA's
-  // count stores), as in a cooperative grid barrier -- not one per thread
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    is_last = atomicAdd(ticket, 1u) == uint32_t(n_blk - 1);
-    if (is_last) __threadfence();
-  }
-  __syncthreads();
-  if (!is_last) return;
-  const int nb = n_blk;
-  // stage the [nb][E] block-count matrix in shared memory with coalesced loads
-  // (when it fits: up to 200 KB), then per-expert scans run from there
-  const bool staged = stage_counts != 0;
-  if (staged)
-    for (int i = tid; i < nb * E; i += blockDim.x) bc[i] = __ldcg(&blk_counts[i]);
-  __syncthreads();
-  __shared__ int seg_sum[64][17];
-  int P = 1;
-  while (P * 2 * E <= int(blockDim.x) && P * 2 <= 16) P *= 2;
-  const int e = tid / P, p = tid - (tid / P) * P;
-  const int seg = (nb + P - 1) / P;
-  const int b0 = min(nb, p * seg), b1 = min(nb, b0 + seg);
-  auto cnt = [&](int blk) { return staged ? bc[blk * E + e] : __ldcg(&blk_counts[size_t(blk) * E + e]); };
-  if (e < E) {
-    int sum = 0;
-    for (int blk = b0; blk < b1; ++blk) sum += cnt(blk);
-    seg_sum[e][p] = sum;
-  }
-  __syncthreads();
-  if (e < E) {
-    int run = 0;
-    for (int q = 0; q < p; ++q) run += seg_sum[e][q];
-    if (p == P - 1) {
-      int tot = run;
-      for (int blk = b0; blk < b1; ++blk) tot += cnt(blk);
-      batch_counts[e] = tot;
-    }
-    // exclusive prefix over blocks: blk_prefix[b][e] = sum_{b' < b} blk_counts[b'][e]
-    if (blk_prefix != nullptr)
-      for (int blk = b0; blk < b1; ++blk) {
-        blk_prefix[size_t(blk) * E + e] = run;
-        run += cnt(blk);
-      }
+    const int c = __ldcg(count_acc + e);
+    tot_s[e] = c;
+    batch_counts[e] = c;
+    count_acc[e] = 0;
   }
   // count exchange (G > 1): this origin's batch counts go into every rank's
   // count table (half = forward parity), then epoch A is raised
@@ -579,8 +248,8 @@ __global__ void __launch_bounds__(kSelectThreads)
     const uint32_t fwd = sync.state[1], par = fwd & 1u;
     int32_t* const* half = sync.count_ptrs + 8 * par;
     for (int i = tid; i < sync.G * E; i += blockDim.x) {
-      const int p = i / E, e2 = i - (i / E) * E;
-      half[p][sync.rank * E + e2] = batch_counts[e2];
+      const int pp = i / E, e2 = i - (i / E) * E;
+      half[pp][sync.rank * E + e2] = tot_s[e2];
     }
     __syncthreads();
     if (tid == 0) {
@@ -592,6 +261,404 @@ __global__ void __launch_bounds__(kSelectThreads)
       sync.state[2] = par;
     }
   }
+}
+
+// ---------------------------------------------------------------- the tensor-core router
+namespace ri {
+constexpr int kM = 128;                  // tokens per tile (MMA M, TMEM lanes)
+constexpr int kKB = 128;                 // k per block: one 128-byte swizzled row of 8-bit limbs
+constexpr int kThreads = 256;            // producer / epilogue warps 0-7
+constexpr int kMmaWarp = 8;              // + one warp that issues the TMA and MMA work
+constexpr int kBlock = kThreads + 32;
+constexpr int kStages = 2;
+constexpr int kABytes = kM * kKB;        // one limb tile, 16 KB
+constexpr int kAStage = 3 * kABytes;
+constexpr int kMaxSplit = 4;             // CTAs per cluster (K ranges per tile); a 32-token block each
+
+template <int N>
+struct Cfg {
+  static constexpr int kBStage = 2 * N * kKB;                   // both Wg limbs: one [2N][128] tile
+  static constexpr int kCols = 6 * N;                           // s32 accumulators (x limb i, Wg limb j)
+  static constexpr int kTmemCols = kCols <= 128 ? 128 : (kCols <= 256 ? 256 : 512);
+  static constexpr size_t kOffB = size_t(kStages) * kAStage;
+  // partial sums pushed by the other K ranges of the cluster: [split - 1][owned rows][N] int64
+  static constexpr size_t kOffRecv = kOffB + size_t(kStages) * kBStage;
+  static constexpr int kRow = N + 2;  // int64 per staged row (16-byte pad: conflict-free row-per-lane stores)
+  static constexpr size_t kRecvBytes = size_t(kM) * kRow * 8 * (kMaxSplit - 1) / kMaxSplit;
+  static constexpr size_t kOffMax = kOffRecv + kRecvBytes;             // [kMaxSplit][kM] row maxima
+  static constexpr size_t kOffBar = kOffMax + size_t(kMaxSplit) * kM * 4;
+  static constexpr size_t kSmem = kOffBar + 128 + 1024;          // + alignment slack
+  static_assert(size_t(kM) * kRow * 8 <= kOffB, "the fold staging must fit in the A ring");
+};
+}  // namespace ri
+
+// Limb bytes j of four quantised values (bit patterns of q + 1.5 * 2^23), element i in byte i.
+MP_DEV void limb_words(uint32_t y0, uint32_t y1, uint32_t y2, uint32_t y3, uint32_t& l0, uint32_t& l1,
+                       uint32_t& l2) {
+  const uint32_t t01 = __byte_perm(y0, y1, 0x5140), t23 = __byte_perm(y2, y3, 0x5140);
+  l0 = __byte_perm(t01, t23, 0x5410);
+  l1 = __byte_perm(t01, t23, 0x7632);
+  const uint32_t u01 = __byte_perm(y0, y1, 0x0062), u23 = __byte_perm(y2, y3, 0x0062);
+  l2 = __byte_perm(u01, u23, 0x5410);
+}
+
+// logit = f32( f64(rn_f32(S)) * 2^sh ): rn_f32(S) = m * 2^drop (m <= 2^24) with integer ops, then
+// one fp32 multiply by an exact power of two -- the same single rounding as the fp64 product.
+// Exponents outside fp32's normal range (rows of tiny / huge magnitude) take the fp64 path.
+MP_DEV float exact_logit(long long s, int sh) {
+  const unsigned long long a = s < 0 ? 0ull - (unsigned long long)s : (unsigned long long)s;
+  if (a == 0) return 0.f;
+  const int nb = 64 - __clzll((long long)a);
+  const int drop = nb > 24 ? nb - 24 : 0;
+  uint32_t m = uint32_t(a >> drop);
+  if (drop > 0) {
+    const unsigned long long rem = a & ((1ull << drop) - 1), half = 1ull << (drop - 1);
+    m += (rem > half || (rem == half && (m & 1u))) ? 1u : 0u;
+  }
+  const float f = s < 0 ? -float(m) : float(m);  // exact: m <= 2^24
+  const int k = drop + sh;
+  if (k >= -126 && k <= 127) return f * __uint_as_float(uint32_t(127 + k) << 23);
+  return __double2float_rn(double(f) * __hiloint2double((1023 + k) << 20, 0));
+}
+
+template <int N>
+__global__ void __launch_bounds__(ri::kBlock, 1)
+    router_i8_kernel(const __grid_constant__ CUtensorMap tmB, const __nv_bfloat16* __restrict__ x,
+                     const uint8_t* __restrict__ packed, const float* __restrict__ bias, int T, int d, int E,
+                     int has_gate, int k, int score_mode, int renorm, int split, int32_t* __restrict__ idx,
+                     float* __restrict__ wout, float* __restrict__ shared_gate, uint32_t* __restrict__ hist,
+                     int32_t* __restrict__ blk_counts, int32_t* __restrict__ batch_counts,
+                     uint32_t* __restrict__ ticket, int32_t* __restrict__ count_acc, const PeerSync sync) {
+  using C = ri::Cfg<N>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smA = sm;
+  uint8_t* smB = sm + C::kOffB;
+  uint32_t* xmax = reinterpret_cast<uint32_t*>(sm + C::kOffMax);  // [split][kM]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::kOffBar);  // [2] Wg limbs landed
+  uint64_t* empty = full + 2;                                     // [2] MMAs of the stage done
+  uint64_t* done = full + 4;                                      // every MMA done
+  uint64_t* recv_bar = full + 5;                                  // the cluster's partials landed
+  uint64_t* full_a = full + 6;                                    // [2] x limbs written (8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 8);
+  long long* recv = reinterpret_cast<long long*>(sm + C::kOffRecv);
+  __shared__ int ex_s[ri::kM];  // E(x_t) of the tile's rows
+  __shared__ long long rw_s[N];  // Wg row sums and exponents
+  __shared__ int ew_s[N];
+  __shared__ float bias_s[N];
+  __shared__ int cnt_s[rt::kMaxE];
+  __shared__ int last_s;
+
+  const int tid = threadIdx.x, warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const int row0 = blockIdx.y * ri::kM;
+  const int n_kb = d / ri::kKB;
+  const int kb0 = int(rank) * n_kb / split, kb1 = (int(rank) + 1) * n_kb / split, nk = kb1 - kb0;
+
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    mbar_init(recv_bar, 1);
+    for (int s = 0; s < 2; ++s) mbar_init(&full_a[s], ri::kThreads / 32);
+    fence_barrier_init();
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 0) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // rows of the tile this CTA selects: router blocks b (32 tokens) with b % split == rank
+  const int own_blocks = (4 - int(rank) + split - 1) / split;
+  if (tid == 0 && split > 1)  // bytes the other K ranges push here (set before the cluster barrier)
+    mbar_arrive_expect_tx(recv_bar, uint32_t((split - 1) * own_blocks * rt::kTokens * C::kRow * 8));
+
+  griddep_launch_dependents();
+  griddep_wait();  // x may come from the previous kernel in the stream
+  if (tid < ri::kM && row0 + tid < T)  // this CTA's x range, row by row, toward L2 (both passes read it)
+    bulk_prefetch_l2(x + size_t(row0 + tid) * d + size_t(kb0) * ri::kKB, uint32_t(nk * ri::kKB * 2));
+  for (int e = tid; e < N; e += blockDim.x) {
+    rw_s[e] = reinterpret_cast<const long long*>(packed + 2 * size_t(N) * d)[e];
+    ew_s[e] = reinterpret_cast<const int*>(packed + 2 * size_t(N) * d + 8 * size_t(N))[e];
+    bias_s[e] = (bias != nullptr && e < E) ? bias[e] : 0.f;
+  }
+
+  auto issue_b = [&](int i) {  // both Wg limbs of local k-block i into stage i & 1
+    const int s = i & 1;
+    mbar_arrive_expect_tx(&full[s], uint32_t(C::kBStage));
+    tma_load_2d(smB + size_t(s) * C::kBStage, &tmB, &full[s], (kb0 + i) * ri::kKB, 0);
+  };
+  if (warp == ri::kMmaWarp && lane == 0)
+    for (int i = 0; i < min(2, nk); ++i) issue_b(i);
+
+  // ---- 1. per-row maxima of |x| over this CTA's K range, shared with the cluster.  A warp
+  // takes 8 rows at a time with every lane's loads of all 8 in flight before any is used.
+  {
+    const int kc = nk * ri::kKB / 8;  // 16-byte chunks of one row's range (a multiple of 16)
+    const int per = kc / 16;          // chunks per half-warp and row: lanes 0-15 / 16-31 split a row
+    for (int r0 = warp * 16; r0 < warp * 16 + 16 && warp < ri::kMmaWarp; r0 += 8) {
+      uint32_t m2[4] = {0, 0, 0, 0};   // rows r0 + 2i + (lane >> 4)
+      for (int c0 = 0; c0 < per; c0 += 4) {
+        uint4 v[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int t = min(row0 + r0 + 2 * i + (lane >> 4), T - 1);
+          const uint4* src = reinterpret_cast<const uint4*>(x + size_t(t) * d + size_t(kb0) * ri::kKB) + (lane & 15);
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            v[i][c] = c0 + c < per ? ld_nc_v4(src + 16 * (c0 + c)) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            m2[i] = __vmaxu2(m2[i], __vmaxu2(__vmaxu2(v[i][c].x & 0x7fff7fffu, v[i][c].y & 0x7fff7fffu),
+                                             __vmaxu2(v[i][c].z & 0x7fff7fffu, v[i][c].w & 0x7fff7fffu)));
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t m = max(m2[i] & 0xffffu, m2[i] >> 16);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));  // within the half-warp
+        const int r = r0 + 2 * i + (lane >> 4);
+        if ((lane & 15) < split) st_cluster_u32(&xmax[rank * ri::kM + r], uint32_t(lane & 15), m);
+      }
+    }
+  }
+  cluster_sync();
+  if (tid < ri::kM) {
+    uint32_t m = 0;
+    for (int q = 0; q < split; ++q) m = max(m, xmax[q * ri::kM + tid]);
+    ex_s[tid] = row_exponent(m);
+  }
+  __syncthreads();
+
+  // ---- 2. limbs -> swizzled A tiles, Wg limbs by TMA, 9 MMAs per 32-k step
+  // x chunks of k-block i + 2 are loaded (into the buffer block i just released) right after
+  // block i's proxy fence -- a fence waits for every outstanding access of its thread, so loads
+  // issued before it would be waited for.  Unit = (row, 16-k chunk); 8 lanes cover a row's 256 B.
+  auto load_block = [&](int i, uint4 (&v)[8]) {
+    const int kbase = (kb0 + i) * ri::kKB;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int u = tid + j * ri::kThreads, r = u >> 3, c = u & 7;
+      const uint4* src = reinterpret_cast<const uint4*>(x + size_t(min(row0 + r, T - 1)) * d + kbase + c * 16);
+      v[2 * j] = ld_nc_v4(src);
+      v[2 * j + 1] = ld_nc_v4(src + 1);
+    }
+  };
+  auto produce = [&](int i, uint4 (&v)[8], uint4 (&vn)[8]) {
+    const int s = i & 1;
+    if (i >= 2) {  // the MMAs of block i - 2 released this stage (one lane polls per warp)
+      if (lane == 0) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+      __syncwarp();
+    }
+    uint8_t* a_st = smA + size_t(s) * ri::kAStage;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int u = tid + j * ri::kThreads, r = u >> 3, c = u & 7;
+      const float sc = row_scale(ex_s[r], rt::kWinX);
+      const uint32_t w[8] = {v[2 * j].x, v[2 * j].y, v[2 * j].z, v[2 * j].w,
+                             v[2 * j + 1].x, v[2 * j + 1].y, v[2 * j + 1].z, v[2 * j + 1].w};
+      uint32_t y[16];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        y[2 * q] = quant_bits(bf16_lo(w[q]), sc);
+        y[2 * q + 1] = quant_bits(bf16_hi(w[q]), sc);
+      }
+      uint4 l0, l1, l2;
+      limb_words(y[0], y[1], y[2], y[3], l0.x, l1.x, l2.x);
+      limb_words(y[4], y[5], y[6], y[7], l0.y, l1.y, l2.y);
+      limb_words(y[8], y[9], y[10], y[11], l0.z, l1.z, l2.z);
+      limb_words(y[12], y[13], y[14], y[15], l0.w, l1.w, l2.w);
+      const int off = r * 128 + ((c ^ (r & 7)) << 4);  // SWIZZLE_128B, 8-row atoms of 1 KB
+      st_shared_v4(a_st + off, l0);
+      st_shared_v4(a_st + ri::kABytes + off, l1);
+      st_shared_v4(a_st + 2 * ri::kABytes + off, l2);
+    }
+    fence_proxy_async_shared();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = vn[j];  // block i + 1 (its loads completed by the fence)
+    if (i + 2 < nk) load_block(i + 2, vn);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&full_a[s]);
+  };
+  if (warp < ri::kMmaWarp) {
+    uint4 va[8], vb[8];  // block i's chunks / block i + 1's (landed by block i's fence)
+    if (nk > 0) load_block(0, va);
+    if (nk > 1) load_block(1, vb);
+#pragma unroll 1
+    for (int i = 0; i < nk; ++i) produce(i, va, vb);
+  } else if (lane == 0) {
+    // MMA warp: one MMA per (32-k step, x limb), N' = 2N columns = (x limb ia) x (Wg limbs 0, 1)
+    for (int i = 0; i < nk; ++i) {
+      const int s = i & 1;
+      if (i >= 2) {  // Wg stage s is free once the MMAs of block i - 2 completed
+        mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+        issue_b(i);
+      }
+      mbar_wait(&full_a[s], (i >> 1) & 1);
+      mbar_wait(&full[s], (i >> 1) & 1);
+      tc_fence_after();
+      const uint8_t* a_st = smA + size_t(s) * ri::kAStage;
+      const uint64_t bd = make_sdesc_sw128(smem_u32(smB + size_t(s) * C::kBStage));
+#pragma unroll
+      for (int ks = 0; ks < ri::kKB / 32; ++ks)
+#pragma unroll
+        for (int ia = 0; ia < 3; ++ia) {
+          const uint64_t ad = make_sdesc_sw128(smem_u32(a_st + ia * ri::kABytes)) + uint64_t(2 * ks);
+          umma_i8(tmem + uint32_t(ia * 2 * N), ad, bd + uint64_t(2 * ks), make_idesc_i8(ri::kM, 2 * N, true),
+                  (i | ks) != 0 ? 1u : 0u);
+        }
+      umma_commit(&empty[s]);
+      if (i == nk - 1) umma_commit(done);
+    }
+  }
+
+  if (tid == 0) mbar_wait(done, 0);
+  __syncthreads();
+  tc_fence_after();
+  // ---- 3. fold the six accumulators into int64 per (row, expert).  Rows of a router block
+  // another CTA selects are staged (over the A ring: every MMA is done) and sent there as one
+  // bulk copy per block (completing on its recv_bar); rows selected here wait for those copies.
+  long long* stage = reinterpret_cast<long long*>(smA);  // [kM][kRow] int64
+  const int E_tot = E + (has_gate ? 1 : 0);
+  const int own_rows = own_blocks * rt::kTokens;
+  if (warp < ri::kMmaWarp) {
+    constexpr int H = N / 2;                             // columns per warp quartet
+    const int r = (warp & 3) * 32 + lane, h0 = (warp >> 2) * H;
+    const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+    long long acc[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j) acc[j] = 0;
+#pragma unroll 1
+    for (int q = 0; q < 6; ++q) {  // accumulator (x limb ia, Wg limb jb), weight 2^(8 (ia + jb))
+      const int ia = q >> 1, jb = q & 1;
+      const long long wgt = 1ll << (8 * (ia + jb));
+#pragma unroll
+      for (int j0 = 0; j0 < H; j0 += 8) {
+        uint32_t rv[8];
+        tmem_ld_32x32b_x8(tmem + lane_base + uint32_t(ia * 2 * N + jb * N + h0 + j0), rv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j0 + j] += (long long)int32_t(rv[j]) * wgt;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < H; j += 2)
+      *reinterpret_cast<longlong2*>(stage + size_t(r) * C::kRow + h0 + j) = make_longlong2(acc[j], acc[j + 1]);
+  }
+  fence_proxy_async_shared();
+  __syncthreads();
+  if (tid == 0) {
+    for (int bb = 0; bb < 4; ++bb) {
+      const int ow = bb % split;
+      if (ow == int(rank)) continue;
+      const int slot = int(rank) < ow ? int(rank) : int(rank) - 1;
+      const int ow_rows = (4 - ow + split - 1) / split * rt::kTokens;
+      const int r_loc = (bb / split) * rt::kTokens;
+      bulk_s2s_cluster(recv + (size_t(slot) * ow_rows + r_loc) * C::kRow, stage + size_t(bb) * rt::kTokens * C::kRow,
+                       uint32_t(rt::kTokens * C::kRow * 8), recv_bar, uint32_t(ow));
+    }
+    bulk_commit();
+    if (split > 1) mbar_wait(recv_bar, 0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem);
+  }
+  // logits of this CTA's rows, (row, expert) items over every thread: own partial + the other
+  // K ranges' partials - the x-limb bias term, rounded once; into lg [own rows][N] (B ring)
+  float* lg = reinterpret_cast<float*>(smB);
+  {
+    // warp w takes rows w, w + 9, ...; lane l experts l, l + 32 (, l + 64).  Compact code on
+    // purpose: each CTA runs this once, so instruction fetch, not issue, sets its time.
+    constexpr int EP = (N + 31) / 32;
+    constexpr int kWarps = ri::kBlock / 32;
+#pragma unroll 1
+    for (int rl = warp; rl < own_rows; rl += kWarps) {
+      const int r = (int(rank) + (rl / rt::kTokens) * split) * rt::kTokens + rl % rt::kTokens;  // tile row
+      const int shr = ex_s[r] - rt::kWinX - rt::kWinW;
+#pragma unroll 1
+      for (int u = 0; u < EP; ++u) {
+        const int e = lane + 32 * u;
+        if (e >= E_tot) break;
+        long long sum = stage[size_t(r) * C::kRow + e] - rw_s[e] * (1ll << 22);  // q = A' - 2^22
+#pragma unroll 1
+        for (int p = 0; p < split - 1; ++p) sum += recv[(size_t(p) * own_rows + rl) * C::kRow + e];
+        float v = exact_logit(sum, shr + ew_s[e]);
+        if (e < E && bias != nullptr) v = __fadd_rn(v, bias_s[e]);
+        lg[rl * N + e] = v;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- 4. selection of this CTA's router blocks: 4 tokens per warp in lockstep, block histogram
+  int handled = 0;
+  for (int bl = 0; bl < own_blocks; ++bl) {
+    const int b = int(rank) + bl * split;
+    const int t0 = row0 + b * rt::kTokens;
+    if (t0 >= T) break;
+    const int nt = min(rt::kTokens, T - t0);
+    for (int e = tid; e < E; e += blockDim.x) cnt_s[e] = 0;
+    __syncthreads();
+    {
+      constexpr int NT = 2;  // tokens per warp in lockstep; pairs q, q + 1 over the block's warps
+      const float* lgb = lg + size_t(bl) * rt::kTokens * N;
+#pragma unroll 1
+      for (int q0 = NT * warp; q0 < nt; q0 += NT * (ri::kBlock / 32)) {
+        float a[NT], c[NT];
+        bool ok[NT];
+        int32_t* ir[NT];
+        float* wr[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+          const int q = q0 + i, qq = min(q, nt - 1);
+          ok[i] = q < nt;
+          a[i] = lane < E ? lgb[qq * N + lane] : -INFINITY;
+          c[i] = lane + 32 < E ? lgb[qq * N + lane + 32] : -INFINITY;
+          ir[i] = idx + size_t(t0 + qq) * k;
+          wr[i] = wout + size_t(t0 + qq) * k;
+        }
+        int32_t* const (&irc)[NT] = ir;
+        float* const (&wrc)[NT] = wr;
+        select_topk_store<NT>(a, c, ok, E, k, score_mode, renorm, irc, wrc, cnt_s);
+        if (lane < NT && has_gate && shared_gate != nullptr) {
+          const int q = q0 + lane;
+          if (q < nt) shared_gate[t0 + q] = 1.0f / (1.0f + __expf(-lgb[q * N + E]));
+        }
+      }
+    }
+    __syncthreads();
+    const int blk = t0 / rt::kTokens;
+    for (int e = tid; e < E; e += blockDim.x) {
+      const int cc = cnt_s[e];
+      if (blk_counts) blk_counts[size_t(blk) * E + e] = cc;
+      if (cc && hist) atomicAdd(&hist[e], uint32_t(cc));
+      if (cc && count_acc) atomicAdd(&count_acc[e], cc);
+    }
+    ++handled;
+    __syncthreads();
+  }
+  if (tid == 0) bulk_wait_read0();  // the staging rows were read out before the CTA may exit
+  if (batch_counts == nullptr || count_acc == nullptr || handled == 0) return;
+  // the CTA completing the grid's router blocks reduces the per-block counts
+  const int n_blk = (T + rt::kTokens - 1) / rt::kTokens;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();  // cumulative over the CTA's count stores (ordered by the barrier)
+    last_s = atomicAdd(ticket, uint32_t(handled)) + uint32_t(handled) == uint32_t(n_blk);
+    if (last_s) __threadfence();
+  }
+  __syncthreads();
+  if (!last_s) return;
+  router_batch_tail(E, count_acc, batch_counts, sync);
   if (tid == 0) *ticket = 0u;  // ready for the next launch (stream-ordered)
 }
 
@@ -615,7 +682,11 @@ __global__ void __launch_bounds__(256) router_logits_kernel(const float* __restr
       if (lane < E) v0 = __fadd_rn(v0, bias[lane]);
       if (lane + 32 < E) v1 = __fadd_rn(v1, bias[lane + 32]);
     }
-    select_topk_store(v0, v1, E, k, score_mode, renorm, idx + size_t(t) * k, wout + size_t(t) * k, cnt_s);
+    const float a[1] = {v0}, c[1] = {v1};
+    const bool ok[1] = {true};
+    int32_t* const ir[1] = {idx + size_t(t) * k};
+    float* const wr[1] = {wout + size_t(t) * k};
+    select_topk_store<1>(a, c, ok, E, k, score_mode, renorm, ir, wr, cnt_s);
   }
   __syncthreads();
   if (hist != nullptr)
@@ -636,95 +707,89 @@ int launch_router_logits(const float* logits, int ld, const float* bias, int T, 
   return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_logits_kernel launch");
 }
 
-// Partial-logit scratch of the stateless entries (the layer passes its own): per device,
-// grown on demand, never freed.
-static float* stateless_partial(size_t floats) {
-  static std::mutex mu;
-  static float* buf[16] = {};
-  static size_t cap[16] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  if (cap[dev] < floats) {
-    if (buf[dev]) cudaFree(buf[dev]);
-    buf[dev] = nullptr;
-    cap[dev] = 0;
-    if (cudaMalloc(&buf[dev], floats * sizeof(float)) != cudaSuccess) return nullptr;
-    cap[dev] = floats;
+// K ranges per 128-token tile: enough CTAs to cover the SMs, at most 8 (one cluster)
+// and at most one per 128-k block.  MP_ROUTER_SPLIT overrides (tests: the logits do
+// not depend on it).
+int router_split(int T, int d) {
+  const int tiles = (T + ri::kM - 1) / ri::kM, n_kb = d / ri::kKB;
+  int split = 1;
+  if (const char* env = getenv("MP_ROUTER_SPLIT")) {
+    split = atoi(env);
+  } else {
+    while (split < ri::kMaxSplit && tiles * split * 2 <= kNumSMs) split *= 2;
   }
-  return buf[dev];
+  split = std::max(1, std::min({split, ri::kMaxSplit, n_kb}));
+  return split == 3 ? 2 : split;  // a power of two: the tile's 4 router blocks divide evenly
 }
 
-size_t router_partial_floats(int T, int d, int E_tot) {
-  return size_t(router_lane_groups(d)) * size_t(T) * size_t(router_e_pad(E_tot));
+template <int N>
+static cudaError_t launch_i8(const CUtensorMap& tmB, int split, int tiles, cudaStream_t stream, bool pdl,
+                             const __nv_bfloat16* x, const uint8_t* packed, const float* bias, int T, int d, int E,
+                             int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w,
+                             float* shared_gate, uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts,
+                             uint32_t* ticket, int32_t* count_acc, const PeerSync& ps) {
+  using C = ri::Cfg<N>;
+  const int r = ensure_max_dyn_smem(reinterpret_cast<const void*>(router_i8_kernel<N>), C::kSmem,
+                                    "cudaFuncSetAttribute(router_i8)");
+  if (r != MP_OK) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(split), unsigned(tiles));
+  cfg.blockDim = dim3(ri::kBlock);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(split);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, router_i8_kernel<N>, tmB, x, packed, bias, T, d, E, has_gate, k, score_mode, renorm,
+                            split, idx, w, shared_gate, hist, blk_counts, batch_counts, ticket, count_acc, ps);
 }
 
-int launch_router(const __nv_bfloat16* x, const __nv_bfloat16* wg_packed, const float* bias, int T, int d, int E,
+int launch_router(const __nv_bfloat16* x, const uint8_t* packed, const float* bias, int T, int d, int E,
                   int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w, float* shared_gate,
                   uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts, uint32_t* ticket,
-                  int32_t* blk_prefix, cudaStream_t stream, const PeerSync* sync, const float* w32, float* partial) {
-  if (batch_counts && !ticket) return set_error(MP_E_ARG, "router: batch counts need a ticket word");
+                  int32_t* count_acc, cudaStream_t stream, const PeerSync* sync) {
+  if (batch_counts && (!ticket || !count_acc || !blk_counts))
+    return set_error(MP_E_ARG, "router: batch counts need the block counts, a ticket word and an accumulator");
   if (E < 1 || E > rt::kMaxE) return set_error(MP_E_SHAPE, "router: E=%d outside [1, %d]", E, rt::kMaxE);
   if (k < 1 || k > E || k > rt::kMaxK) return set_error(MP_E_SHAPE, "router: top_k=%d invalid for E=%d", k, E);
-  if (d % 256 != 0) return set_error(MP_E_SHAPE, "router: d=%d not a multiple of 256", d);
+  if (d % 256 != 0 || d > 16384) return set_error(MP_E_SHAPE, "router: d=%d not a multiple of 256 in [256, 16384]", d);
   if (score_mode != 0 && score_mode != 1) return set_error(MP_E_ARG, "router: score_mode %d", score_mode);
   if (T <= 0) return MP_OK;
   if (sync && sync->G > 1 && (!batch_counts || !blk_counts))
     return set_error(MP_E_ARG, "router: the count exchange needs the batch counts");
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return set_error(MP_E_ARG, "router: x not 16-byte aligned");
-  const int E_tot = E + (has_gate ? 1 : 0), E_pad = router_e_pad(E_tot), n_lg = router_lane_groups(d);
-  if (!partial) partial = stateless_partial(router_partial_floats(T, d, E_tot));
-  if (!partial) return set_error(MP_E_CUDA, "router: cannot allocate the partial-logit scratch");
-  const char* w32env = getenv("MP_ROUTER_W32");
-  const bool use32 = w32 != nullptr && (w32env == nullptr || atoi(w32env) != 0);
-
-  // stage 1: the chains, persistent over every SM (MP_ROUTER_GRID overrides, for tests)
-  const int n_units = ((T + kTokPerWarp - 1) / kTokPerWarp) * (E_pad / kExpPerPass) * n_lg;
-  int grid1 = std::min(kNumSMs, (n_units + kChainWarps - 1) / kChainWarps);
-  if (const char* ge = getenv("MP_ROUTER_GRID")) grid1 = std::max(1, atoi(ge));
-  // the octet form over the bf16 rows is the default; an fp32 operand runs the quad form
-  // (MP_ROUTER_CHAIN=4 also runs the quad form over the bf16 rows)
-  const char* chain_env = getenv("MP_ROUTER_CHAIN");
-  const int chain = use32 ? 4 : (chain_env ? atoi(chain_env) : 8);
-  cudaError_t e;
-  if (chain == 8) {
-    const int n_units8 = ((T + kOctTok - 1) / kOctTok) * (E_pad / kExpPerPass) * n_lg;
-    int grid8 = std::min(kNumSMs, (n_units8 + kOctWarps - 1) / kOctWarps);
-    if (const char* ge = getenv("MP_ROUTER_GRID")) grid8 = std::max(1, atoi(ge));
-    MP_TRY_R(ensure_max_dyn_smem(reinterpret_cast<const void*>(router_chain8_kernel), kOctSmem,
-                                 "cudaFuncSetAttribute(router_chain8)"));
-    e = launch_pdl(router_chain8_kernel, dim3(grid8), dim3(kOctWarps * 32), kOctSmem, stream, x, wg_packed, T, d,
-                   E_pad, n_lg, partial);
-  } else if (use32) {
-    e = launch_pdl(router_chain_kernel<true>, dim3(grid1), dim3(kChainWarps * 32), 0, stream, x, wg_packed,
-                   reinterpret_cast<const float4*>(w32), T, d, E_pad, n_lg, partial);
-  } else {
-    e = launch_pdl(router_chain_kernel<false>, dim3(grid1), dim3(kChainWarps * 32), 0, stream, x, wg_packed,
-                   static_cast<const float4*>(nullptr), T, d, E_pad, n_lg, partial);
-  }
-  if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess) return set_cuda_error(e, "router_chain_kernel launch");
-
-  // stage 2: selection per 32-token block (+ last-CTA scan and count exchange)
-  const int grid2 = (T + rt::kTokens - 1) / rt::kTokens;
-  size_t bc_bytes = blk_counts && batch_counts ? size_t(grid2) * E * 4 : 0;
-  const bool stage_counts = bc_bytes <= 200 * 1024;  // larger T: the last CTA scans from global memory
-  if (!stage_counts) bc_bytes = 0;
-  MP_TRY_R(ensure_max_dyn_smem(reinterpret_cast<const void*>(router_select_kernel), bc_bytes,
-                               "cudaFuncSetAttribute(router_select)"));
-  // programmatic dependent launch: the selection grid is scheduled while the chains drain
-  // (its griddepcontrol.wait still orders every partial before use); MP_ROUTER_PDL=0 disables
-  static const bool sel_pdl = [] {
+  const int E_tot = E + (has_gate ? 1 : 0), N = router_n_pad(E_tot);
+  CUtensorMap tmB;
+  MP_TRY_R(encode_tmap_u8_2d(&tmB, packed, uint64_t(2) * N, uint64_t(d), uint32_t(2 * N)));
+  const int split = router_split(T, d), tiles = (T + ri::kM - 1) / ri::kM;
+  const PeerSync ps = sync ? *sync : PeerSync();
+  // programmatic dependent launch: scheduled while the previous kernel drains (the
+  // kernel's griddepcontrol.wait orders x before use); MP_ROUTER_PDL=0 disables
+  static const bool pdl = [] {
     const char* env = getenv("MP_ROUTER_PDL");
     return env == nullptr || atoi(env) != 0;
   }();
-  e = launch_pdl_if(sel_pdl || pdl_enabled(), router_select_kernel, dim3(grid2), dim3(kSelectThreads), bc_bytes,
-                    stream,
-                    static_cast<const float*>(partial), n_lg, E_pad, bias, T, E, has_gate ? 1 : 0, k, score_mode,
-                    renorm, idx, w, shared_gate, hist, blk_counts, batch_counts, ticket, blk_prefix,
-                    sync ? *sync : PeerSync(), stage_counts ? 1 : 0);
+  cudaError_t e;
+#define MP_ROUTER_LAUNCH(NN)                                                                                       \
+  e = launch_i8<NN>(tmB, split, tiles, stream, pdl, x, packed, bias, T, d, E, has_gate, k, score_mode, renorm, idx, \
+                    w, shared_gate, hist, blk_counts, batch_counts, ticket, count_acc, ps)
+  switch (N) {
+    case 16: MP_ROUTER_LAUNCH(16); break;
+    case 32: MP_ROUTER_LAUNCH(32); break;
+    case 48: MP_ROUTER_LAUNCH(48); break;
+    case 64: MP_ROUTER_LAUNCH(64); break;
+    case 80: MP_ROUTER_LAUNCH(80); break;
+    default: return set_error(MP_E_SHAPE, "router: %d weight rows", E_tot);
+  }
+#undef MP_ROUTER_LAUNCH
   if (e == cudaSuccess) e = cudaGetLastError();
-  return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_select_kernel launch");
+  return e == cudaSuccess ? MP_OK : set_cuda_error(e, "router_i8_kernel launch");
 }
 
 }  // namespace mp

@@ -11,7 +11,7 @@ REPO = Path(__file__).resolve().parent.parent
 
 def header_symbols():
     text = (REPO / "include" / "moeplace_b200.h").read_text()
-    return sorted(set(re.findall(r"^int (mp_\w+)\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|size_t) (mp_\w+)\(", text, flags=re.M)))
 
 
 def test_header_and_binding_agree():

@@ -4,7 +4,7 @@ Sizes: Mixtral-8x7B (d 4096, f 14336, E 8, k 2) at T = 4096 (the bench
 workload), Qwen1.5-MoE-A2.7B at T = 4096 and DeepSeek-V2-Lite (E 64, k 6,
 2 shared) at T = 4096 and at the maximum T = 16384.
   * routing: every token's indices bit-exact and weights to fp32 rounding
-    against oracle.router_logits / topk_route (the lane-chain contract is
+    against oracle.router_logits / topk_route (the exact-integer contract is
     cheap in numpy at these sizes); histogram == bincount;
   * permutation: the receive rows of all (token, slot) pairs are a dense
     permutation of 0..T*k-1 equal to the oracle's positions, and every

@@ -24,7 +24,7 @@ def _draw(seed):
     r = np.random.default_rng(1000 + seed)
     E = int(r.choice([4, 8, 16, 24, 32, 60, 64]))
     k = int(r.integers(1, min(8, E) + 1))
-    d = int(r.choice([256, 512, 768, 1024, 2048, 3072, 4096]))  # 1, 2 and 4 router lane groups
+    d = int(r.choice([256, 512, 768, 1024, 2048, 3072, 4096]))  # 1..8 router K ranges, odd k-block counts
     f = int(r.choice([128, 256, 384, 512, 640]))
     mode = int(r.integers(0, 2))
     renorm = int(r.integers(0, 2)) if mode == 1 else 0

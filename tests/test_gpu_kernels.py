@@ -105,43 +105,34 @@ def test_grouped_gemm_large_k_many_tiles(pair, monkeypatch):
     assert rel < 1e-2, rel
 
 
-def _run_router(x, wg, bias, E, k, mode, gate, w32=0):
-    """mp_router_topk_hist (bf16 Wg operand) or, w32 = 1, mp_router_topk_hist_f32w (the fp32
-    consumption-order operand mp_layer_forward uses)."""
+def _run_router(x, wg, bias, E, k, mode, gate):
+    """mp_router_pack + mp_router_topk_hist (the tensor-core exact-integer router)."""
     L, lib = _lib()
     T, d = x.shape
     xt = torch.from_numpy(x).cuda().bfloat16()
     wgt = torch.from_numpy(wg).cuda().bfloat16()
-    packed = torch.empty((E + gate + 7) // 8 * 8 * d, device="cuda", dtype=torch.bfloat16)
+    packed = torch.empty(lib.mp_router_packed_bytes(E + gate, d), device="cuda", dtype=torch.uint8)
     L.check(lib.mp_router_pack(_vp(wgt), E + gate, d, _vp(packed), _stream()))
     bt = torch.from_numpy(bias).cuda()
     idx = torch.empty(T, k, dtype=torch.int32, device="cuda")
     w = torch.empty(T, k, dtype=torch.float32, device="cuda")
     go = torch.empty(T, dtype=torch.float32, device="cuda")
     hist = torch.zeros(E, dtype=torch.int32, device="cuda")
-    if w32:
-        p32 = torch.empty((E + gate + 7) // 8 * 8 * d, device="cuda", dtype=torch.float32)
-        L.check(lib.mp_router_pack32(_vp(wgt), E + gate, d, _vp(p32), _stream()))
-        L.check(lib.mp_router_topk_hist_f32w(_vp(xt), _vp(packed), _vp(p32), _vp(bt), T, d, E, gate, k, mode, 0,
-                                             _vp(idx), _vp(w), _vp(go) if gate else None, _vp(hist), _stream()))
-    else:
-        L.check(lib.mp_router_topk_hist(_vp(xt), _vp(packed), _vp(bt), T, d, E, gate, k, mode, 0, _vp(idx), _vp(w),
-                                        _vp(go) if gate else None, _vp(hist), _stream()))
+    L.check(lib.mp_router_topk_hist(_vp(xt), _vp(packed), _vp(bt), T, d, E, gate, k, mode, 0, _vp(idx), _vp(w),
+                                    _vp(go) if gate else None, _vp(hist), _stream()))
     torch.cuda.synchronize()
     return idx.cpu().numpy(), w.cpu().numpy(), hist.cpu().numpy(), go.cpu().numpy()
 
 
-@pytest.mark.parametrize("w32", [0, 1], ids=["wg_bf16", "wg_f32"])
-@pytest.mark.parametrize("grid", ["", "1", "7", "148"])
+@pytest.mark.parametrize("split", ["", "1", "2", "4"])
 @pytest.mark.parametrize("E,k,mode,d", [(8, 2, 0, 512), (64, 6, 1, 256), (16, 4, 0, 4096), (60, 4, 1, 2048),
                                         (8, 2, 0, 3072)])
-def test_router_ties_go_to_the_lower_expert(E, k, mode, d, grid, w32, monkeypatch):
+def test_router_ties_go_to_the_lower_expert(E, k, mode, d, split, monkeypatch):
     """Exact logit ties (duplicated router rows + biases, all-zero tokens whose logits are the
-    biases alone) resolve to the lower expert id, bit-exact with the oracle -- for 1, 2 and 4
-    lane groups (d = 512 / 2048 / 4096), every chain-kernel grid ("" = the default; 1 CTA walks
-    every unit), with the bf16 Wg operand and the fp32 consumption-order operand the layer runs."""
-    if grid:
-        monkeypatch.setenv("MP_ROUTER_GRID", grid)
+    biases alone) resolve to the lower expert id, bit-exact with the oracle -- for every K split
+    of the tensor-core router ("" = the default; the integer logits cannot depend on it)."""
+    if split:
+        monkeypatch.setenv("MP_ROUTER_SPLIT", split)
     T = 96
     x = orc.synthetic_tokens(0, T, d, seed=7)
     x[::3] = 0.0                       # every third token: logits == bias
@@ -153,7 +144,7 @@ def test_router_ties_go_to_the_lower_expert(E, k, mode, d, grid, w32, monkeypatc
     bias[3] = bias[4] = bias[6] = np.float32(bias.max())   # three-way tie among the biases
     lg = orc.router_logits(x, wg, bias)
     idx_ref, w_ref = orc.topk_route(lg, E, k, mode)
-    idx, w, hist, _ = _run_router(x, wg, bias, E, k, mode, 0, w32)
+    idx, w, hist, _ = _run_router(x, wg, bias, E, k, mode, 0)
     assert np.array_equal(idx, idx_ref)
     assert np.array_equal(hist, orc.histogram(idx_ref, E))
     np.testing.assert_allclose(w, w_ref, rtol=1e-5, atol=1e-6)
@@ -164,17 +155,19 @@ def test_router_ties_go_to_the_lower_expert(E, k, mode, d, grid, w32, monkeypatc
                 assert pos[lo] < pos[hi], row
 
 
-@pytest.mark.parametrize("w32", [0, 1], ids=["wg_bf16", "wg_f32"])
 @pytest.mark.parametrize("E,k,mode,gate,d,T", [(8, 2, 0, 0, 512, 333), (64, 6, 1, 0, 256, 200), (60, 4, 1, 1, 512, 64),
-                                               (8, 2, 0, 0, 4096, 48), (16, 4, 0, 0, 4096, 100)])
-def test_router_bit_exact(E, k, mode, gate, d, T, w32):
+                                               (8, 2, 0, 0, 4096, 48), (16, 4, 0, 0, 4096, 100),
+                                               (64, 6, 1, 1, 2048, 1000), (33, 3, 0, 0, 768, 129)])
+def test_router_bit_exact(E, k, mode, gate, d, T):
     x = orc.synthetic_tokens(0, T, d, seed=3)
+    x[5] *= np.float32(2.0 ** -90)     # a row on a tiny grid
+    x[6, 11] = np.float32(3.0e4)       # a row whose maximum dwarfs the rest
     wg = orc.synthetic_router(E + gate, d, seed=3)
     bias = orc.origin_bias(1, E, seed=3)
     lg = orc.router_logits(x, wg, bias)
     idx_ref, w_ref = orc.topk_route(lg, E, k, mode)
     hist_ref = orc.histogram(idx_ref, E)
-    idx, w, hist, go = _run_router(x, wg, bias, E, k, mode, gate, w32)
+    idx, w, hist, go = _run_router(x, wg, bias, E, k, mode, gate)
     assert np.array_equal(idx, idx_ref)
     assert np.array_equal(hist, hist_ref)
     np.testing.assert_allclose(w, w_ref, rtol=1e-5, atol=1e-6)

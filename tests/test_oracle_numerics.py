@@ -13,27 +13,60 @@ def test_bf16_round_matches_torch():
     np.testing.assert_array_equal(orc.bf16_round(a), ref)
 
 
+def _rne_f32(v: int) -> float:
+    a = abs(v)
+    if a == 0:
+        return 0.0
+    drop = max(a.bit_length() - 24, 0)
+    m, rem = a >> drop, a & ((1 << drop) - 1)
+    if drop and (rem > (1 << (drop - 1)) or (rem == (1 << (drop - 1)) and m & 1)):
+        m += 1
+    return float(m * 2 ** drop) * (-1 if v < 0 else 1)
+
+
 def test_router_logits_contract():
-    """32 lane chains over 8-wide k slices strided by 256, then the butterfly tree."""
+    """Each row on its own integer grid, the exact integer dot product, one rounding to fp32, the
+    power-of-two rescale -- restated with Python integers -- and close to the real dot product."""
     rng = np.random.default_rng(1)
     d = 512
     x = orc.bf16_round(rng.standard_normal((3, d)).astype(np.float32))
     w = orc.bf16_round(rng.standard_normal((5, d)).astype(np.float32))
+    x[1] *= np.float32(2.0 ** -70)
+    x[2, 3] = np.float32(-5.0e3)
     got = orc.router_logits(x, w)
+
+    def grid(row, win):
+        m = max(abs(float(v)) for v in row)
+        ef = 0 if m == 0 else int(np.frexp(np.float32(m))[1]) + 126   # bf16 exponent field
+        e = max(ef - 126, -100)
+        return [int(np.rint(float(v) * 2.0 ** (win - e))) for v in row], e
+
     for t in range(3):
+        qx, ex = grid(x[t], 21)
+        assert max(abs(q) for q in qx) <= 2 ** 21
         for e in range(5):
-            p = []
-            for lane in range(32):
-                acc = np.float32(0)
-                for s in range(d // 256):
-                    for j in range(8):
-                        k = 256 * s + 8 * lane + j
-                        acc = np.float32(acc + np.float32(x[t, k] * w[e, k]))
-                p.append(acc)
-            for o in (16, 8, 4, 2, 1):
-                p = [np.float32(p[i] + p[i + o]) for i in range(o)]
-            assert got[t, e] == p[0]
-    np.testing.assert_allclose(got, x @ w.T, rtol=1e-4, atol=1e-3)
+            qw, ew = grid(w[e], 14)
+            assert max(abs(q) for q in qw) <= 2 ** 14
+            s = sum(a * b for a, b in zip(qx, qw))
+            want = np.float32(_rne_f32(s) * 2.0 ** (ex + ew - 35))
+            assert got[t, e] == want
+    ref = x.astype(np.float64) @ w.astype(np.float64).T
+    scale = np.abs(x).max(axis=1, keepdims=True) * np.abs(w).max(axis=1)[None, :] * d
+    assert (np.abs(got - ref) <= 2.0 ** -14 * scale + 1e-30).all()
+
+
+def test_exact_int_matmul_and_rounding():
+    rng = np.random.default_rng(5)
+    q = rng.integers(-2 ** 21, 2 ** 21 + 1, size=(7, 4096))
+    r = rng.integers(-2 ** 21, 2 ** 21 + 1, size=(3, 4096))
+    s = orc.exact_int_matmul(q, r)
+    for i in range(7):
+        for j in range(3):
+            assert int(s[i, j]) == sum(int(a) * int(b) for a, b in zip(q[i], r[j]))
+    vals = np.concatenate([rng.integers(-2 ** 62, 2 ** 62, size=5000), [0, 1, -1, 2 ** 24 + 1, 2 ** 24 + 3,
+                                                                         2 ** 25 + 2, 2 ** 25 + 6, -(2 ** 25 + 6)]])
+    got = orc.rne_f32_of_int(vals)
+    assert all(got[i] == _rne_f32(int(v)) for i, v in enumerate(vals))
 
 
 def test_topk_ties_go_to_lower_id():

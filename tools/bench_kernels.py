@@ -55,7 +55,7 @@ def main():
         xs_ = [wl.tokens(T, d, dev, batch=b) for b in range(16)]
         x = xs_[0]
         wg = wl.router_weights(E_tot, d, dev)
-        packed = torch.empty((E_tot + 7) // 8 * 8 * d, device=dev, dtype=torch.bfloat16)
+        packed = torch.empty(lib.mp_router_packed_bytes(E_tot, d), device=dev, dtype=torch.uint8)
         _lib.check(lib.mp_router_pack(vp(wg), E_tot, d, vp(packed), st))
         bias = wl.origin_bias(0, E).to(dev)
         idx = torch.empty(T, k, dtype=torch.int32, device=dev)
