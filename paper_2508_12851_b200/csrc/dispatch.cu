@@ -32,7 +32,7 @@ namespace mp {
 //     receive buffer = rows of lower experts on that GPU + rows of lower-ranked
 //     sources for e (from the exchanged counts C[G][E] and the route table);
 //   * prefix[e]: rows of expert e in this origin's earlier router blocks, summed
-//     here from the router's per-block counts (4 segments x 64 experts, loads in flight).
+//     here from the router's per-block counts (coalesced over experts, loads in flight).
 // Phase 1: one thread per (token, slot) pair computes its stable in-block rank
 //          (__match_any_sync within a warp, a per-expert prefix across warps).
 // Phase 2: one warp per token loads the x row once (16 B per lane per step) and
@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(256)
   __shared__ int base_s[64];
   __shared__ int wcnt[8][64];  // per-warp, per-expert pair counts -> exclusive prefix over warps
   __shared__ int Mpre[8][64];  // rows of lower experts on GPU D (exclusive prefix over experts)
-  __shared__ int pre4[4][64];  // this origin's rows of each expert in earlier blocks, by segment
+  __shared__ int pre_s[64];  // this origin's rows of each expert in earlier router blocks
+  __shared__ int pre_seg[4][64];
   const int b = blockIdx.x;
   const int t0 = b * kTok;
   const int nt = min(kTok, T - t0);
@@ -71,21 +72,28 @@ __global__ void __launch_bounds__(256)
   }
   if (tid < np) s_e[tid] = idx[size_t(t0) * k + tid];
   for (int i = tid; i < 8 * 64; i += blockDim.x) (&wcnt[0][0])[i] = 0;
-  {  // block prefix: thread (segment, expert) sums blocks seg, seg + 4, ... below b
-    const int e = tid & 63, seg = tid >> 6;
+  {  // block prefix: thread (segment, expert) sums blocks seg, seg + S, ... below b -- lanes over
+    // consecutive experts (coalesced), 32 loads in flight per thread -- then a sum over segments
+    const int S = blockDim.x / 64, e = tid & 63, seg = tid >> 6;
     int sum = 0;
     if (e < E)
-      for (int b0 = seg; b0 < b; b0 += 32) {
-        int v[8];
+      for (int b0 = seg; b0 < b; b0 += 32 * S) {
+        int v[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int bb = b0 + 4 * u;
+        for (int u = 0; u < 32; ++u) {
+          const int bb = b0 + u * S;
           v[u] = bb < b ? __ldcg(blk_counts + size_t(bb) * E + e) : 0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) sum += v[u];
+        for (int u = 0; u < 32; ++u) sum += v[u];
       }
-    pre4[seg][e] = sum;
+    pre_seg[seg][e] = sum;
+  }
+  __syncthreads();
+  if (tid < 64) {
+    int t = 0;
+    for (int q = 0; q < int(blockDim.x / 64); ++q) t += pre_seg[q][tid];
+    pre_s[tid] = t;
   }
   __syncthreads();
   // receive layout of every GPU D: rows of expert e2 on D = sum over sources routing e2 to D;
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   if (tid < E) {
     const int e = tid, D = R[rank][e];
-    int base = pre4[0][e] + pre4[1][e] + pre4[2][e] + pre4[3][e] + Mpre[D][e];
+    int base = pre_s[e] + Mpre[D][e];
     for (int s = 0; s < rank; ++s)
       if (R[s][e] == D) base += C[s][e];
     base_s[e] = base;

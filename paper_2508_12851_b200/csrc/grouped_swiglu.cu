@@ -54,12 +54,31 @@ struct GemmSmemTail {
   int g_m[gg::kMaxGroups];
   int g_slot[gg::kMaxGroups];
   int g_orow[gg::kMaxGroups];
+  int g_expert[gg::kMaxGroups];  // mode 1: the group's expert id (per-source dispatch waits)
   int g_tmp[64];
 };
 
 struct TileCoord {
   int g, m_blk, n_blk;
 };
+
+// Source ranks whose dispatched rows fall in rows [r0, r1) of group g (mode 1: the receive
+// layout orders an expert's rows by source rank), as a bit mask; other modes: every rank.
+template <class Tail>
+MP_DEV uint32_t group_row_sources(const Tail& st, const GroupSpec& gs, int g, int r0, int r1) {
+  if (gs.mode != 1 || !gs.per_source) return 0xffu;
+  const int e = st.g_expert[g];
+  const int32_t* counts = gs.counts + (gs.parity ? size_t(*gs.parity) * gs.G * gs.E : 0);
+  uint32_t mask = 0;
+  int acc = 0;
+  for (int s = 0; s < gs.G && acc < r1; ++s) {
+    if (gs.route[s * gs.E + e] != gs.rank) continue;
+    const int c = __ldcg(counts + s * gs.E + e);
+    if (c > 0 && acc + c > r0) mask |= 1u << s;
+    acc += c;
+  }
+  return mask;
+}
 
 // Inclusive warp scan (Kogge-Stone over the 32 lanes).
 MP_DEV int warp_incl_scan(int v) {
@@ -112,6 +131,7 @@ MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
           st.g_m[idx[h]] = m[h];
           st.g_slot[idx[h]] = slot[h];
           st.g_orow[idx[h]] = row[h];
+          st.g_expert[idx[h]] = lane + 32 * h;
         }
       if (lane == 0) st.n_groups = __popc(b0) + __popc(b1);
     }
@@ -330,6 +350,7 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + gg::kStages * gg::kABytes;
+  static_assert(sizeof(GemmSmemTail) <= 4096, "GEMM smem tail exceeds its reservation");
   GemmSmemTail& st = *reinterpret_cast<GemmSmemTail*>(smem + gg::kStages * gg::kStageBytes);
 
   const int warp = warp_id();
@@ -377,13 +398,21 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
       // ================= TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      bool waited = !(peer_on(sync) && sync.wait);
+      // F2: a routed tile waits only for the ranks whose dispatched rows it reads (epoch B
+      // of each); this GPU's own rows are complete by stream order
+      const bool waits = peer_on(sync) && sync.wait;
+      const uint32_t epoch = waits ? sync.state[0] : 0u;
+      uint32_t ready = waits ? (1u << sync.rank) : 0xffu;
+      if (waits) fence_proxy_async_global();
       each_job([&](const TileJob& j) {
-        if (!waited && !j.aux) {
-          // rows from peers: every rank's dispatch (epoch B) before the first routed A load
-          peer_wait(sync, sync.state[0]);
-          fence_proxy_async_global();
-          waited = true;
+        if (waits && !j.aux) {
+          uint32_t need = group_row_sources(st, gs, j.g, j.m_row0, min(j.m_row0 + gg::BM, j.m_rows)) & ~ready;
+          if (need) {
+            for (int p = 0; p < sync.G; ++p)
+              if (need >> p & 1u) peer_wait_one(sync, p, epoch);
+            fence_proxy_async_global();
+            ready |= need;
+          }
         }
         for (int kb = 0; kb < j.k_blocks; ++kb) {
           mbar_wait(&st.empty[stage], phase ^ 1);
@@ -498,6 +527,7 @@ struct Gemm2SmemTail {
   int g_m[gg::kMaxGroups];
   int g_slot[gg::kMaxGroups];
   int g_orow[gg::kMaxGroups];
+  int g_expert[gg::kMaxGroups];  // mode 1: the group's expert id (per-source dispatch waits)
   int g_tmp[64];
 };
 
@@ -512,6 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smA = smem;
   uint8_t* smB = smem + g2::kStages * g2::kABytes;
+  static_assert(sizeof(Gemm2SmemTail) <= 4096, "GEMM smem tail exceeds its reservation");
   Gemm2SmemTail& st = *reinterpret_cast<Gemm2SmemTail*>(smem + g2::kStages * g2::kStageBytes);
 
   const int warp = warp_id();
@@ -562,14 +593,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
       // ================= TMA producer (both CTAs load their halves)
       int stage = 0;
       uint32_t phase = 0;
-      bool waited = !(peer_on(sync) && sync.wait);
+      // F2: a routed tile waits only for the ranks whose dispatched rows this CTA's half of
+      // it reads (epoch B of each); own rows are complete by stream order, and the
+      // shared-expert tiles scheduled first overlap the waits
+      const bool waits = peer_on(sync) && sync.wait;
+      const uint32_t epoch = waits ? sync.state[0] : 0u;
+      uint32_t ready = waits ? (1u << sync.rank) : 0xffu;
+      if (waits) fence_proxy_async_global();
       each_job([&](const TileJob& j) {
-        if (!waited && !j.aux) {
-          // first routed tile: rows from peers need every rank's dispatch (epoch B);
-          // the shared-expert tiles before it overlap the wait
-          peer_wait(sync, sync.state[0]);
-          fence_proxy_async_global();
-          waited = true;
+        if (waits && !j.aux) {
+          const int r0 = j.m_row0 + int(rank) * 128;
+          uint32_t need = r0 < j.m_rows ? group_row_sources(st, gs, j.g, r0, min(r0 + 128, j.m_rows)) & ~ready : 0u;
+          if (need) {
+            for (int p = 0; p < sync.G; ++p)
+              if (need >> p & 1u) peer_wait_one(sync, p, epoch);
+            fence_proxy_async_global();
+            ready |= need;
+          }
         }
         const int a_row = j.a_row + int(rank) * 128;
         const int b_row = j.b_row + int(rank) * 128;

@@ -117,6 +117,7 @@ struct GroupSpec {
   int single_m = 0;                   // mode 2: one group {0, single_m, slot 0, 0}
   int mode = 0;
   int m_lo = 0, m_hi = 1 << 30;       // mode 1: only groups with m_lo <= m < m_hi
+  int per_source = 1;                 // mode 1: a routed tile waits only for its rows' source ranks
 };
 // A second, dense problem fused into the same CTA-pair launch (the shared
 // expert): its tiles are scheduled first, round-robin over the clusters, and

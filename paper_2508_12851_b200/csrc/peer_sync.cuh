@@ -13,20 +13,23 @@ namespace mp {
 
 MP_DEV bool peer_on(const PeerSync& ps) { return ps.G > 1 && ps.flag_ptrs != nullptr; }
 
+// One thread: spin until rank p's flag in this rank's window reached `epoch`.
+MP_DEV void peer_wait_one(const PeerSync& ps, int p, uint32_t epoch) {
+  const uint32_t* mine = ps.flag_ptrs[ps.rank];
+  const uint64_t t0 = globaltimer_ns();
+  while (int32_t(ld_acquire_sys_u32(mine + p) - epoch) < 0) {
+    if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+      const uint32_t bits = atomicOr(ps.err, 1u << p) | (1u << p);
+      if (ps.err_host != nullptr) st_release_sys_u32(ps.err_host, bits);
+      break;
+    }
+    __nanosleep(64);
+  }
+}
+
 // One thread: spin until every rank's flag in this rank's window reached `epoch`.
 MP_DEV void peer_wait(const PeerSync& ps, uint32_t epoch) {
-  const uint32_t* mine = ps.flag_ptrs[ps.rank];
-  for (int p = 0; p < ps.G; ++p) {
-    const uint64_t t0 = globaltimer_ns();
-    while (int32_t(ld_acquire_sys_u32(mine + p) - epoch) < 0) {
-      if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
-        const uint32_t bits = atomicOr(ps.err, 1u << p) | (1u << p);
-        if (ps.err_host != nullptr) st_release_sys_u32(ps.err_host, bits);
-        break;
-      }
-      __nanosleep(64);
-    }
-  }
+  for (int p = 0; p < ps.G; ++p) peer_wait_one(ps, p, epoch);
 }
 
 // One thread: raise `epoch` in every rank's window (flags[rank]).
