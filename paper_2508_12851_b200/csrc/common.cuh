@@ -53,14 +53,17 @@ MP_DEV uint32_t mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return done;
 }
-// Wait for the phase with `parity` to complete.  A protocol bug must not hang
-// the GPU: after ~4e9 cycles (seconds) the kernel traps instead.
+MP_DEV uint64_t globaltimer_ns();
+// Wait for the phase with `parity` to complete.  A protocol bug must not hang the GPU:
+// after 40 s the kernel traps instead.  The bound is wall time and longer than the NVLink
+// peer waits' 30 s (kPeerTimeoutNs), so a warp parked behind a producer that legitimately
+// waits for a slow peer (e.g. a host-bound rank) is never the one that traps.
 MP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;
-  const long long t0 = clock64();
+  const uint64_t t0 = globaltimer_ns();
   while (!mbar_try_wait(addr, parity)) {
-    if (clock64() - t0 > (1ll << 32)) __trap();
+    if (globaltimer_ns() - t0 > 40ull * 1000ull * 1000ull * 1000ull) __trap();
   }
 }
 
