@@ -279,7 +279,11 @@ template <int N>
 struct Cfg {
   static constexpr int kBStage = 2 * N * kKB;                   // both Wg limbs: one [2N][128] tile
   static constexpr int kCols = 6 * N;                           // s32 accumulators (x limb i, Wg limb j)
-  static constexpr int kTmemCols = kCols <= 128 ? 128 : (kCols <= 256 ? 256 : 512);
+  // small N: the x limb tiles live in TMEM (columns 256.., 2 stages x 3 limbs x 32 columns), so
+  // the MMAs read no A operand from shared memory and the producers need no proxy fence
+  static constexpr bool kTmemA = kCols <= 256;
+  static constexpr int kTmemACol = 256;
+  static constexpr int kTmemCols = kTmemA ? 512 : (kCols <= 128 ? 128 : (kCols <= 256 ? 256 : 512));
   static constexpr size_t kOffB = size_t(kStages) * kAStage;
   // partial sums pushed by the other K ranges of the cluster: [split - 1][owned rows][N] int64
   static constexpr size_t kOffRecv = kOffB + size_t(kStages) * kBStage;
@@ -287,7 +291,7 @@ struct Cfg {
   static constexpr size_t kRecvBytes = size_t(kM) * kRow * 8 * (kMaxSplit - 1) / kMaxSplit;
   static constexpr size_t kOffMax = kOffRecv + kRecvBytes;             // [kMaxSplit][kM] row maxima
   static constexpr size_t kOffBar = kOffMax + size_t(kMaxSplit) * kM * 4;
-  static constexpr size_t kSmem = kOffBar + 128 + 1024;          // + alignment slack
+  static constexpr size_t kSmem = kOffBar + 256 + 1024;          // + alignment slack
   static_assert(size_t(kM) * kRow * 8 <= kOffB, "the fold staging must fit in the A ring");
 };
 }  // namespace ri
@@ -323,7 +327,8 @@ MP_DEV float exact_logit(long long s, int sh) {
 
 template <int N>
 __global__ void __launch_bounds__(ri::kBlock, 1)
-    router_i8_kernel(const __grid_constant__ CUtensorMap tmB, const __nv_bfloat16* __restrict__ x,
+    router_i8_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmX,
+                     const __nv_bfloat16* __restrict__ x,
                      const uint8_t* __restrict__ packed, const float* __restrict__ bias, int T, int d, int E,
                      int has_gate, int k, int score_mode, int renorm, int split, int32_t* __restrict__ idx,
                      float* __restrict__ wout, float* __restrict__ shared_gate, uint32_t* __restrict__ hist,
@@ -340,7 +345,8 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
   uint64_t* done = full + 4;                                      // every MMA done
   uint64_t* recv_bar = full + 5;                                  // the cluster's partials landed
   uint64_t* full_a = full + 6;                                    // [2] x limbs written (8 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 8);
+  uint64_t* xfull = full + 8;                                     // [3] x tiles landed (TMEM-A path)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(full + 12);
   long long* recv = reinterpret_cast<long long*>(sm + C::kOffRecv);
   __shared__ int ex_s[ri::kM];  // E(x_t) of the tile's rows
   __shared__ long long rw_s[N];  // Wg row sums and exponents
@@ -363,8 +369,10 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
     mbar_init(done, 1);
     mbar_init(recv_bar, 1);
     for (int s = 0; s < 2; ++s) mbar_init(&full_a[s], ri::kThreads / 32);
+    for (int s = 0; s < 3; ++s) mbar_init(&xfull[s], 1);
     fence_barrier_init();
     tma_prefetch_desc(&tmB);
+    if (C::kTmemA) tma_prefetch_desc(&tmX);
   }
   if (warp == 0) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
@@ -391,8 +399,21 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
     mbar_arrive_expect_tx(&full[s], uint32_t(C::kBStage));
     tma_load_2d(smB + size_t(s) * C::kBStage, &tmB, &full[s], (kb0 + i) * ri::kKB, 0);
   };
-  if (warp == ri::kMmaWarp && lane == 0)
+  // TMEM-A path: the k-block's x tile (128 rows x 128 k bf16, two 64-k SWIZZLE_128B boxes) by
+  // TMA into a 3-stage ring over the (unused) A region; rows past T arrive as zeros
+  auto issue_x = [&](int i) {
+    const int xs = i % 3;
+    mbar_arrive_expect_tx(&xfull[xs], uint32_t(ri::kM * ri::kKB * 2));
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      tma_load_2d(smA + size_t(xs) * (ri::kM * ri::kKB * 2) + size_t(h) * (ri::kM * 128), &tmX, &xfull[xs],
+                  (kb0 + i) * ri::kKB + 64 * h, row0);
+  };
+  if (warp == ri::kMmaWarp && lane == 0) {
     for (int i = 0; i < min(2, nk); ++i) issue_b(i);
+    if (C::kTmemA)
+      for (int i = 0; i < min(3, nk); ++i) issue_x(i);
+  }
 
   // ---- 1. per-row maxima of |x| over this CTA's K range, shared with the cluster.  A warp
   // takes 8 rows at a time with every lane's loads of all 8 in flight before any is used.
@@ -486,7 +507,50 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&full_a[s]);
   };
-  if (warp < ri::kMmaWarp) {
+  if (C::kTmemA && warp < ri::kMmaWarp) {
+    // TMEM-A producers: warp w owns TMEM lanes 32 (w & 3) .. +31 (= tile rows) and k-half w >> 2
+    // of every 128-k block: a lane reads its row's 128 bytes from the swizzled x tile (8 x 16 B,
+    // conflict-free), converts 64 elements -> 16 words per limb -> three tcgen05.st.  No proxy
+    // fence: the tiles come by TMA several blocks ahead.
+    const int q = warp & 3, hk = warp >> 2, r = q * 32 + lane;
+    const float sc = row_scale(ex_s[r], rt::kWinX);
+#pragma unroll 1
+    for (int i = 0; i < nk; ++i) {
+      const int s = i & 1, xs = i % 3;
+      if (i >= 2) {
+        if (lane == 0) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
+        __syncwarp();
+        tc_fence_after();
+      }
+      if (lane == 0) mbar_wait(&xfull[xs], (i / 3) & 1);
+      __syncwarp();
+      const uint8_t* xt = smA + size_t(xs) * (ri::kM * ri::kKB * 2) + size_t(hk) * (ri::kM * 128) + r * 128;
+      uint4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = *reinterpret_cast<const uint4*>(xt + ((j ^ (r & 7)) << 4));
+      uint32_t l0[16], l1[16], l2[16];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // 8 elements per uint4 -> two 4-element words per limb
+        const uint32_t w[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+        uint32_t y[8];
+#pragma unroll
+        for (int e2 = 0; e2 < 4; ++e2) {
+          y[2 * e2] = quant_bits(bf16_lo(w[e2]), sc);
+          y[2 * e2 + 1] = quant_bits(bf16_hi(w[e2]), sc);
+        }
+        limb_words(y[0], y[1], y[2], y[3], l0[2 * j], l1[2 * j], l2[2 * j]);
+        limb_words(y[4], y[5], y[6], y[7], l0[2 * j + 1], l1[2 * j + 1], l2[2 * j + 1]);
+      }
+      const uint32_t ta = tmem + (uint32_t(q * 32) << 16) + uint32_t(C::kTmemACol + s * 96 + hk * 16);
+      tmem_st_32x32b_x16(ta, l0);
+      tmem_st_32x32b_x16(ta + 32, l1);
+      tmem_st_32x32b_x16(ta + 64, l2);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_a[s]);  // also: this warp is done with x stage xs
+    }
+  } else if (warp < ri::kMmaWarp) {
     uint4 va[8], vb[8];  // block i's chunks / block i + 1's (landed by block i's fence)
     if (nk > 0) load_block(0, va);
     if (nk > 1) load_block(1, vb);
@@ -501,6 +565,7 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
         issue_b(i);
       }
       mbar_wait(&full_a[s], (i >> 1) & 1);
+      if (C::kTmemA && i + 3 < nk) issue_x(i + 3);  // every producer is past x stage i % 3
       mbar_wait(&full[s], (i >> 1) & 1);
       tc_fence_after();
       const uint8_t* a_st = smA + size_t(s) * ri::kAStage;
@@ -509,9 +574,15 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
       for (int ks = 0; ks < ri::kKB / 32; ++ks)
 #pragma unroll
         for (int ia = 0; ia < 3; ++ia) {
-          const uint64_t ad = make_sdesc_sw128(smem_u32(a_st + ia * ri::kABytes)) + uint64_t(2 * ks);
-          umma_i8(tmem + uint32_t(ia * 2 * N), ad, bd + uint64_t(2 * ks), make_idesc_i8(ri::kM, 2 * N, true),
-                  (i | ks) != 0 ? 1u : 0u);
+          if (C::kTmemA) {  // A tile: 8 TMEM columns (32 k) per step of limb ia's 32
+            const uint32_t at = tmem + uint32_t(C::kTmemACol + s * 96 + ia * 32 + ks * 8);
+            umma_i8_ts(tmem + uint32_t(ia * 2 * N), at, bd + uint64_t(2 * ks), make_idesc_i8(ri::kM, 2 * N, true),
+                       (i | ks) != 0 ? 1u : 0u);
+          } else {
+            const uint64_t ad = make_sdesc_sw128(smem_u32(a_st + ia * ri::kABytes)) + uint64_t(2 * ks);
+            umma_i8(tmem + uint32_t(ia * 2 * N), ad, bd + uint64_t(2 * ks), make_idesc_i8(ri::kM, 2 * N, true),
+                    (i | ks) != 0 ? 1u : 0u);
+          }
         }
       umma_commit(&empty[s]);
       if (i == nk - 1) umma_commit(done);
@@ -723,7 +794,7 @@ int router_split(int T, int d) {
 }
 
 template <int N>
-static cudaError_t launch_i8(const CUtensorMap& tmB, int split, int tiles, cudaStream_t stream, bool pdl,
+static cudaError_t launch_i8(const CUtensorMap& tmB, const CUtensorMap& tmX, int split, int tiles, cudaStream_t stream, bool pdl,
                              const __nv_bfloat16* x, const uint8_t* packed, const float* bias, int T, int d, int E,
                              int has_gate, int k, int score_mode, int renorm, int32_t* idx, float* w,
                              float* shared_gate, uint32_t* hist, int32_t* blk_counts, int32_t* batch_counts,
@@ -746,7 +817,7 @@ static cudaError_t launch_i8(const CUtensorMap& tmB, int split, int tiles, cudaS
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, router_i8_kernel<N>, tmB, x, packed, bias, T, d, E, has_gate, k, score_mode, renorm,
+  return cudaLaunchKernelEx(&cfg, router_i8_kernel<N>, tmB, tmX, x, packed, bias, T, d, E, has_gate, k, score_mode, renorm,
                             split, idx, w, shared_gate, hist, blk_counts, batch_counts, ticket, count_acc, ps);
 }
 
@@ -765,8 +836,9 @@ int launch_router(const __nv_bfloat16* x, const uint8_t* packed, const float* bi
     return set_error(MP_E_ARG, "router: the count exchange needs the batch counts");
   if (reinterpret_cast<uintptr_t>(x) % 16 != 0) return set_error(MP_E_ARG, "router: x not 16-byte aligned");
   const int E_tot = E + (has_gate ? 1 : 0), N = router_n_pad(E_tot);
-  CUtensorMap tmB;
+  CUtensorMap tmB, tmX;
   MP_TRY_R(encode_tmap_u8_2d(&tmB, packed, uint64_t(2) * N, uint64_t(d), uint32_t(2 * N)));
+  MP_TRY_R(encode_tmap_bf16_2d(&tmX, x, uint64_t(T), uint64_t(d), uint32_t(ri::kM)));  // TMEM-A path
   const int split = router_split(T, d), tiles = (T + ri::kM - 1) / ri::kM;
   const PeerSync ps = sync ? *sync : PeerSync();
   // programmatic dependent launch: scheduled while the previous kernel drains (the
@@ -777,7 +849,7 @@ int launch_router(const __nv_bfloat16* x, const uint8_t* packed, const float* bi
   }();
   cudaError_t e;
 #define MP_ROUTER_LAUNCH(NN)                                                                                       \
-  e = launch_i8<NN>(tmB, split, tiles, stream, pdl, x, packed, bias, T, d, E, has_gate, k, score_mode, renorm, idx, \
+  e = launch_i8<NN>(tmB, tmX, split, tiles, stream, pdl, x, packed, bias, T, d, E, has_gate, k, score_mode, renorm, idx, \
                     w, shared_gate, hist, blk_counts, batch_counts, ticket, count_acc, ps)
   switch (N) {
     case 16: MP_ROUTER_LAUNCH(16); break;
