@@ -32,12 +32,13 @@
 // CTA one contiguous K range of d:
 //   1. every CTA reads its x range once for the per-token maxima; the maxima go to
 //      every CTA of the cluster through DSMEM, so all CTAs share E(x_t);
-//   2. the CTA re-reads its x range (L2) and writes three limb tiles per 128-k block
-//      straight into shared memory in the UMMA SWIZZLE_128B K-major layout (limb
-//      j = byte j of the fp32 pattern of q + 1.5 * 2^23: an FFMA and byte permutes);
-//      both Wg limbs arrive by one TMA as a [2N][128] tile; one thread issues one MMA
-//      per (32-k step, x limb) with N' = 2N (each x limb tile is read once per step);
-//   3. the epilogue folds the six accumulators into int64 per (token, expert), the
+//   2. the x range comes again (L2) by TMA, one 128-k block at a time into a 3-stage
+//      shared-memory ring; each producer lane converts its row (limb j = byte j of the fp32
+//      pattern of q + 1.5 * 2^23: an FFMA and byte permutes) and writes the three limb tiles
+//      into TMEM (tcgen05.st); both Wg limbs arrive by one TMA as a [2N][128] tile; one thread
+//      issues one MMA per (32-k step, x limb) with A from TMEM and N' = 2N, into four s32
+//      accumulators, one per limb shift 8 (i + j);
+//   3. the epilogue folds the four accumulators into int64 per (token, expert), the
 //      cluster sums its K ranges through DSMEM (integer, exact), and each 32-token
 //      router block is selected by one CTA: one warp per token, top-k by two
 //      redux.sync rounds, gate weights, block histogram; the last CTA of the grid
@@ -278,12 +279,15 @@ constexpr int kMaxSplit = 4;             // CTAs per cluster (K ranges per tile)
 template <int N>
 struct Cfg {
   static constexpr int kBStage = 2 * N * kKB;                   // both Wg limbs: one [2N][128] tile
-  static constexpr int kCols = 6 * N;                           // s32 accumulators (x limb i, Wg limb j)
-  // small N: the x limb tiles live in TMEM (columns 256.., 2 stages x 3 limbs x 32 columns), so
-  // the MMAs read no A operand from shared memory and the producers need no proxy fence
-  static constexpr bool kTmemA = kCols <= 256;
-  static constexpr int kTmemACol = 256;
-  static constexpr int kTmemCols = kTmemA ? 512 : (kCols <= 128 ? 128 : (kCols <= 256 ? 256 : 512));
+  // s32 accumulators, one per limb shift s = i + j (x limb i, Wg limb j), at columns [s N, s N + N):
+  // x limb i's MMA (N' = 2N over both Wg limbs) lands at column i N, so shifts 1 and 2 collect
+  // two MMAs each -- the accumulators are zeroed first and every MMA accumulates
+  static constexpr int kCols = 4 * N;
+  // the x limb tiles live in TMEM (columns 320.., 2 stages x 3 limbs x 32 columns): the MMAs read
+  // no A operand from shared memory and the producers need no proxy fence
+  static constexpr int kTmemACol = 320;
+  static constexpr int kTmemCols = 512;
+  static_assert(kCols <= kTmemACol, "accumulators overlap the A stages");
   static constexpr size_t kOffB = size_t(kStages) * kAStage;
   // partial sums pushed by the other K ranges of the cluster: [split - 1][owned rows][N] int64
   static constexpr size_t kOffRecv = kOffB + size_t(kStages) * kBStage;
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
     for (int s = 0; s < 3; ++s) mbar_init(&xfull[s], 1);
     fence_barrier_init();
     tma_prefetch_desc(&tmB);
-    if (C::kTmemA) tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmX);
   }
   if (warp == 0) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
@@ -399,8 +403,8 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
     mbar_arrive_expect_tx(&full[s], uint32_t(C::kBStage));
     tma_load_2d(smB + size_t(s) * C::kBStage, &tmB, &full[s], (kb0 + i) * ri::kKB, 0);
   };
-  // TMEM-A path: the k-block's x tile (128 rows x 128 k bf16, two 64-k SWIZZLE_128B boxes) by
-  // TMA into a 3-stage ring over the (unused) A region; rows past T arrive as zeros
+  // the k-block's x tile (128 rows x 128 k bf16, two 64-k SWIZZLE_128B boxes) by TMA into a
+  // 3-stage ring at the head of shared memory; rows past T arrive as zeros
   auto issue_x = [&](int i) {
     const int xs = i % 3;
     mbar_arrive_expect_tx(&xfull[xs], uint32_t(ri::kM * ri::kKB * 2));
@@ -411,8 +415,7 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
   };
   if (warp == ri::kMmaWarp && lane == 0) {
     for (int i = 0; i < min(2, nk); ++i) issue_b(i);
-    if (C::kTmemA)
-      for (int i = 0; i < min(3, nk); ++i) issue_x(i);
+    for (int i = 0; i < min(3, nk); ++i) issue_x(i);
   }
 
   // ---- 1. per-row maxima of |x| over this CTA's K range, shared with the cluster.  A warp
@@ -458,62 +461,22 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
   __syncthreads();
 
   // ---- 2. limbs -> swizzled A tiles, Wg limbs by TMA, 9 MMAs per 32-k step
-  // x chunks of k-block i + 2 are loaded (into the buffer block i just released) right after
-  // block i's proxy fence -- a fence waits for every outstanding access of its thread, so loads
-  // issued before it would be waited for.  Unit = (row, 16-k chunk); 8 lanes cover a row's 256 B.
-  auto load_block = [&](int i, uint4 (&v)[8]) {
-    const int kbase = (kb0 + i) * ri::kKB;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int u = tid + j * ri::kThreads, r = u >> 3, c = u & 7;
-      const uint4* src = reinterpret_cast<const uint4*>(x + size_t(min(row0 + r, T - 1)) * d + kbase + c * 16);
-      v[2 * j] = ld_nc_v4(src);
-      v[2 * j + 1] = ld_nc_v4(src + 1);
-    }
-  };
-  auto produce = [&](int i, uint4 (&v)[8], uint4 (&vn)[8]) {
-    const int s = i & 1;
-    if (i >= 2) {  // the MMAs of block i - 2 released this stage (one lane polls per warp)
-      if (lane == 0) mbar_wait(&empty[s], ((i >> 1) - 1) & 1);
-      __syncwarp();
-    }
-    uint8_t* a_st = smA + size_t(s) * ri::kAStage;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int u = tid + j * ri::kThreads, r = u >> 3, c = u & 7;
-      const float sc = row_scale(ex_s[r], rt::kWinX);
-      const uint32_t w[8] = {v[2 * j].x, v[2 * j].y, v[2 * j].z, v[2 * j].w,
-                             v[2 * j + 1].x, v[2 * j + 1].y, v[2 * j + 1].z, v[2 * j + 1].w};
-      uint32_t y[16];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        y[2 * q] = quant_bits(bf16_lo(w[q]), sc);
-        y[2 * q + 1] = quant_bits(bf16_hi(w[q]), sc);
-      }
-      uint4 l0, l1, l2;
-      limb_words(y[0], y[1], y[2], y[3], l0.x, l1.x, l2.x);
-      limb_words(y[4], y[5], y[6], y[7], l0.y, l1.y, l2.y);
-      limb_words(y[8], y[9], y[10], y[11], l0.z, l1.z, l2.z);
-      limb_words(y[12], y[13], y[14], y[15], l0.w, l1.w, l2.w);
-      const int off = r * 128 + ((c ^ (r & 7)) << 4);  // SWIZZLE_128B, 8-row atoms of 1 KB
-      st_shared_v4(a_st + off, l0);
-      st_shared_v4(a_st + ri::kABytes + off, l1);
-      st_shared_v4(a_st + 2 * ri::kABytes + off, l2);
-    }
-    fence_proxy_async_shared();
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = vn[j];  // block i + 1 (its loads completed by the fence)
-    if (i + 2 < nk) load_block(i + 2, vn);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&full_a[s]);
-  };
-  if (C::kTmemA && warp < ri::kMmaWarp) {
+  if (warp < ri::kMmaWarp) {
     // TMEM-A producers: warp w owns TMEM lanes 32 (w & 3) .. +31 (= tile rows) and k-half w >> 2
     // of every 128-k block: a lane reads its row's 128 bytes from the swizzled x tile (8 x 16 B,
     // conflict-free), converts 64 elements -> 16 words per limb -> three tcgen05.st.  No proxy
     // fence: the tiles come by TMA several blocks ahead.
     const int q = warp & 3, hk = warp >> 2, r = q * 32 + lane;
     const float sc = row_scale(ex_s[r], rt::kWinX);
+    {  // zero this warp's half of the accumulator columns (ordered before the first MMA by the
+       // tcgen05.wait::st + full_a arrival of block 0)
+      uint32_t z[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) z[j] = 0u;
+#pragma unroll
+      for (int c = 0; c < 2 * N; c += 16)
+        tmem_st_32x32b_x16(tmem + (uint32_t(q * 32) << 16) + uint32_t(hk * 2 * N + c), z);
+    }
 #pragma unroll 1
     for (int i = 0; i < nk; ++i) {
       const int s = i & 1, xs = i % 3;
@@ -550,12 +513,6 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_a[s]);  // also: this warp is done with x stage xs
     }
-  } else if (warp < ri::kMmaWarp) {
-    uint4 va[8], vb[8];  // block i's chunks / block i + 1's (landed by block i's fence)
-    if (nk > 0) load_block(0, va);
-    if (nk > 1) load_block(1, vb);
-#pragma unroll 1
-    for (int i = 0; i < nk; ++i) produce(i, va, vb);
   } else if (lane == 0) {
     // MMA warp: one MMA per (32-k step, x limb), N' = 2N columns = (x limb ia) x (Wg limbs 0, 1)
     for (int i = 0; i < nk; ++i) {
@@ -565,24 +522,16 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
         issue_b(i);
       }
       mbar_wait(&full_a[s], (i >> 1) & 1);
-      if (C::kTmemA && i + 3 < nk) issue_x(i + 3);  // every producer is past x stage i % 3
+      if (i + 3 < nk) issue_x(i + 3);  // every producer is past x stage i % 3
       mbar_wait(&full[s], (i >> 1) & 1);
       tc_fence_after();
-      const uint8_t* a_st = smA + size_t(s) * ri::kAStage;
       const uint64_t bd = make_sdesc_sw128(smem_u32(smB + size_t(s) * C::kBStage));
 #pragma unroll
       for (int ks = 0; ks < ri::kKB / 32; ++ks)
 #pragma unroll
-        for (int ia = 0; ia < 3; ++ia) {
-          if (C::kTmemA) {  // A tile: 8 TMEM columns (32 k) per step of limb ia's 32
-            const uint32_t at = tmem + uint32_t(C::kTmemACol + s * 96 + ia * 32 + ks * 8);
-            umma_i8_ts(tmem + uint32_t(ia * 2 * N), at, bd + uint64_t(2 * ks), make_idesc_i8(ri::kM, 2 * N, true),
-                       (i | ks) != 0 ? 1u : 0u);
-          } else {
-            const uint64_t ad = make_sdesc_sw128(smem_u32(a_st + ia * ri::kABytes)) + uint64_t(2 * ks);
-            umma_i8(tmem + uint32_t(ia * 2 * N), ad, bd + uint64_t(2 * ks), make_idesc_i8(ri::kM, 2 * N, true),
-                    (i | ks) != 0 ? 1u : 0u);
-          }
+        for (int ia = 0; ia < 3; ++ia) {  // A tile: 8 TMEM columns (32 k) per step of limb ia's 32
+          const uint32_t at = tmem + uint32_t(C::kTmemACol + s * 96 + ia * 32 + ks * 8);
+          umma_i8_ts(tmem + uint32_t(ia * N), at, bd + uint64_t(2 * ks), make_idesc_i8(ri::kM, 2 * N, true), 1u);
         }
       umma_commit(&empty[s]);
       if (i == nk - 1) umma_commit(done);
@@ -592,7 +541,7 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
   if (tid == 0) mbar_wait(done, 0);
   __syncthreads();
   tc_fence_after();
-  // ---- 3. fold the six accumulators into int64 per (row, expert).  Rows of a router block
+  // ---- 3. fold the four accumulators into int64 per (row, expert).  Rows of a router block
   // another CTA selects are staged (over the A ring: every MMA is done) and sent there as one
   // bulk copy per block (completing on its recv_bar); rows selected here wait for those copies.
   long long* stage = reinterpret_cast<long long*>(smA);  // [kM][kRow] int64
@@ -606,13 +555,12 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
 #pragma unroll
     for (int j = 0; j < H; ++j) acc[j] = 0;
 #pragma unroll 1
-    for (int q = 0; q < 6; ++q) {  // accumulator (x limb ia, Wg limb jb), weight 2^(8 (ia + jb))
-      const int ia = q >> 1, jb = q & 1;
-      const long long wgt = 1ll << (8 * (ia + jb));
+    for (int sh = 0; sh < 4; ++sh) {  // accumulator of limb shift sh, weight 2^(8 sh)
+      const long long wgt = 1ll << (8 * sh);
 #pragma unroll
       for (int j0 = 0; j0 < H; j0 += 8) {
         uint32_t rv[8];
-        tmem_ld_32x32b_x8(tmem + lane_base + uint32_t(ia * 2 * N + jb * N + h0 + j0), rv);
+        tmem_ld_32x32b_x8(tmem + lane_base + uint32_t(sh * N + h0 + j0), rv);
         tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[j0 + j] += (long long)int32_t(rv[j]) * wgt;
