@@ -172,8 +172,15 @@ MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
 template <class Tail>
 MP_DEV TileCoord decode_any(const Tail& s, int tile, int n_blocks, int bm) {
   TileCoord c;
-  int g = 0;
-  while (s.tile_prefix[g + 1] <= tile) ++g;
+  // the group holding `tile`: the last g with tile_prefix[g] <= tile (binary search: every warp
+  // role decodes every tile, so a linear scan over up to 128 groups sat on the producer's path)
+  int lo = 0, hi = s.n_groups - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s.tile_prefix[mid] <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  const int g = lo;  // (an empty group shares its prefix with the next: the last such g is the owner)
   const int local = tile - s.tile_prefix[g];
   const int m_blocks = (s.g_m[g] + bm - 1) / bm;
   c.g = g;
