@@ -211,3 +211,29 @@ def test_router_logits_in_selection(E, k, mode, renorm):
     assert np.array_equal(idx.cpu().numpy(), idx_ref)
     assert np.array_equal(hist.cpu().numpy(), orc.histogram(idx_ref, E))
     np.testing.assert_allclose(w.cpu().numpy(), w_ref, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("E,k,d", [(8, 2, 512), (64, 6, 2048)])
+def test_router_extreme_rows_bit_exact(E, k, d):
+    """Rows at the edges of the grid rule on the GPU: all-zero tokens, tokens below the E = -100
+    clamp, huge tokens, single-element tokens, constant tokens, a tiny and a duplicated expert --
+    indices, histogram and weights against the oracle."""
+    rng = np.random.default_rng(E + d)
+    T = 160
+    x = orc.synthetic_tokens(0, T, d, seed=21)
+    x[0::8] = 0.0
+    x[1::8] = orc.bf16_round(x[1::8] * np.float32(2.0 ** -120))
+    x[2::8] = orc.bf16_round(x[2::8] * np.float32(2.0 ** 60))
+    x[3::8] = 0.0
+    x[3::8, 5] = np.float32(-2.5)
+    x[4::8] = np.float32(0.25)
+    wg = orc.synthetic_router(E, d, seed=21)
+    wg[1] = orc.bf16_round(wg[1] * np.float32(2.0 ** -110))
+    wg[E - 1] = wg[0]
+    bias = orc.origin_bias(0, E, seed=21)
+    lg = orc.router_logits(x, wg, bias)
+    idx_ref, w_ref = orc.topk_route(lg, E, k, 0)
+    idx, w, hist, _ = _run_router(x, wg, bias, E, k, 0, 0)
+    assert np.array_equal(idx, idx_ref)
+    assert np.array_equal(hist, orc.histogram(idx_ref, E))
+    np.testing.assert_allclose(w, w_ref, rtol=1e-5, atol=1e-6)

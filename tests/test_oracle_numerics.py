@@ -113,3 +113,38 @@ def test_layer_linear_in_gate_weights_and_empty_batch():
     x = orc.synthetic_tokens(0, 0, 256)
     r = orc.moe_layer_forward(shape, [x], wg, [None], np.zeros((1, 4), np.int32), experts)
     assert r.out[0].shape == (0, 256) and r.counts.sum() == 0
+
+
+def test_router_contract_extreme_rows():
+    """Rows at the edges of the grid rule -- all zero, subnormal-range bf16 values (E(a) clamped
+    at -100), huge magnitudes, a single non-zero element, ties -- against the Python-integer
+    restatement, and the logits are finite."""
+    rng = np.random.default_rng(11)
+    d = 256
+    x = orc.bf16_round(rng.standard_normal((6, d)).astype(np.float32))
+    w = orc.bf16_round(rng.standard_normal((4, d)).astype(np.float32) / np.float32(16.0))
+    x[0] = 0.0
+    x[1] = orc.bf16_round(x[1] * np.float32(2.0 ** -120))      # below the clamp: E = -100
+    x[2] = orc.bf16_round(x[2] * np.float32(2.0 ** 60))        # huge
+    x[3] = 0.0
+    x[3, 17] = np.float32(-3.0)                                 # one element
+    x[4] = orc.bf16_round(np.full(d, 0.5, np.float32))          # constant row
+    w[1] = orc.bf16_round(w[1] * np.float32(2.0 ** -110))
+    w[2] = w[0]                                                 # duplicated expert
+    got = orc.router_logits(x, w)
+    assert np.isfinite(got).all()
+
+    def grid(row, win):
+        m = max(abs(float(v)) for v in row)
+        ef = 0 if m == 0 else int(np.frexp(np.float32(m))[1]) + 126
+        e = max(ef - 126, -100)
+        return [int(np.rint(float(v) * 2.0 ** (win - e))) for v in row], e
+
+    for t in range(x.shape[0]):
+        qx, ex = grid(x[t], 21)
+        for e in range(w.shape[0]):
+            qw, ew = grid(w[e], 14)
+            s = sum(a * b for a, b in zip(qx, qw))
+            assert got[t, e] == np.float32(_rne_f32(s) * 2.0 ** (ex + ew - 35)), (t, e)
+    assert (got[:, 0] == got[:, 2]).all()
+    assert (got[0] == 0).all() and (got[3, :] == got[3, :]).all()
