@@ -76,15 +76,6 @@ MP_DEV uint32_t cluster_ctarank() {
 MP_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// Store a float at the same smem offset in CTA `cta` of the cluster (DSMEM).
-MP_DEV void st_cluster_f32(const void* local_equiv, uint32_t cta, float v) {
-  asm volatile(
-      "{\n\t.reg .b32 ra;\n\t"
-      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "st.shared::cluster.f32 [ra], %2;\n\t}" ::"r"(smem_u32(local_equiv)),
-      "r"(cta), "f"(v)
-      : "memory");
-}
 // Arrive on the mbarrier at the same smem offset in CTA `cta` of the cluster.
 MP_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
   asm volatile(
@@ -98,15 +89,6 @@ MP_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
 // ---------------------------------------------------------------- TMA
 MP_DEV void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-// 1-D bulk copy global -> shared (async proxy), completion on `bar` (tx bytes).
-// bytes % 16 == 0, both addresses 16-byte aligned.
-MP_DEV void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
 }
 // Prefetch a contiguous global range into L2 (bytes % 16 == 0).
 MP_DEV void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
@@ -122,15 +104,6 @@ MP_DEV void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
-// Same, with an L2 cache-policy hint (createpolicy result).
-MP_DEV void tma_load_2d_hint(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                             uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
-      "%3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
 // 2-SM variant: data lands in this CTA's smem, completion is signalled on the
 // LEADER CTA's mbarrier (same offset, peer bit cleared).
 MP_DEV void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -139,16 +112,6 @@ MP_DEV void tma_load_2d_2sm(void* smem_dst, const CUtensorMap* map, uint64_t* ba
       "%3}], [%4];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
       : "memory");
-}
-MP_DEV uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-MP_DEV uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
 }
 
 // ---------------------------------------------------------------- tcgen05
@@ -250,15 +213,6 @@ MP_DEV void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&r)[8]) {
                : "r"(taddr));
 }
 
-// D[tmem] (+)= A[smem] * B[smem]^T, 8-bit integer inputs, s32 accumulator (exact), one thread.
-MP_DEV void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 // Same with A read from TMEM (K-major: one lane per row, 4 k per 32-bit column).
 MP_DEV void umma_i8_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -290,38 +244,13 @@ __host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N, bool b_signed
 // Order this thread's generic-proxy shared-memory writes before later async-proxy
 // (tcgen05.mma / TMA) reads of them.
 MP_DEV void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-MP_DEV void st_shared_v4(void* p, uint4 v) {
-  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
-// DSMEM: 32-bit store / 64-bit load at the same smem offset in CTA `cta` of the cluster.
+// DSMEM: 32-bit store at the same smem offset in CTA `cta` of the cluster.
 MP_DEV void st_cluster_u32(const void* local_equiv, uint32_t cta, uint32_t v) {
   asm volatile(
       "{\n\t.reg .b32 ra;\n\t"
       "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
       "st.shared::cluster.u32 [ra], %2;\n\t}" ::"r"(smem_u32(local_equiv)),
       "r"(cta), "r"(v)
-      : "memory");
-}
-// Generic pointer to the same shared-memory object in CTA `cta` of the cluster (plain loads
-// through it are ordinary memory operations the compiler can batch).
-template <typename T>
-MP_DEV const T* cluster_map(const T* local, uint32_t cta) {
-  uint64_t r;
-  asm("mapa.u64 %0, %1, %2;" : "=l"(r) : "l"(reinterpret_cast<uint64_t>(local)), "r"(cta));
-  return reinterpret_cast<const T*>(r);
-}
-// Remote 16-byte store into CTA `cta`'s shared memory (same offsets as the local
-// `dst_equiv` / `bar_equiv`) that completes `bytes` = 16 of tx on that CTA's mbarrier.
-MP_DEV void st_async_v2_b64(const void* dst_equiv, const uint64_t* bar_equiv, uint32_t cta, long long a,
-                            long long b) {
-  asm volatile(
-      "{\n\t.reg .b32 rd, rb;\n\t"
-      "mapa.shared::cluster.u32 rd, %0, %2;\n\t"
-      "mapa.shared::cluster.u32 rb, %1, %2;\n\t"
-      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [rd], {%3, %4}, [rb];\n\t}" ::"r"(
-          smem_u32(dst_equiv)),
-      "r"(smem_u32(bar_equiv)), "r"(cta), "l"(a), "l"(b)
       : "memory");
 }
 // Bulk copy of `bytes` (multiple of 16) from this CTA's shared memory to the same offsets as
@@ -339,17 +268,6 @@ MP_DEV void bulk_s2s_cluster(const void* dst_equiv, const void* src, uint32_t by
 }
 MP_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 MP_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-MP_DEV long long ld_cluster_s64(const void* local_equiv, uint32_t cta) {
-  long long v;
-  asm volatile(
-      "{\n\t.reg .b32 ra;\n\t"
-      "mapa.shared::cluster.u32 ra, %1, %2;\n\t"
-      "ld.shared::cluster.s64 %0, [ra];\n\t}"
-      : "=l"(v)
-      : "r"(smem_u32(local_equiv)), "r"(cta)
-      : "memory");
-  return v;
-}
 
 // ---------------------------------------------------------------- system scope (NVLink peers)
 MP_DEV void st_release_sys_u32(uint32_t* p, uint32_t v) {
@@ -391,11 +309,6 @@ MP_DEV uint4 ld_nc_v4(const void* p) {
 MP_DEV uint4 ld_cg_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-  return r;
-}
-MP_DEV uint4 ld_v4(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
 MP_DEV void st_v4(void* p, uint4 v) {
