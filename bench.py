@@ -92,6 +92,19 @@ def init_dist_quiet(dev):
 
 
 # ----------------------------------------------------------------------------- clocks
+def agree_max(v, world: int, dev) -> int:
+    """max of an int (or bool) over the ranks: loop counts that decide how many layer
+    forwards a rank runs must agree, since each forward is a lock-step of every rank."""
+    v = int(v)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([v], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        v = int(t.item())
+    return v
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
 
@@ -111,6 +124,8 @@ class ClockSampler:
         self.window = (now, None) if which == "start" else (self.window[0] if self.window else now, now)
 
     def start(self):
+        if os.environ.get("MP_BENCH_NO_CLOCKS") == "1":  # diagnostics: no nvidia-smi sampler
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
@@ -416,13 +431,17 @@ def main_b200(args):
     # settle: the sampler's start and the event setup left the GPU idle; keep it busy for
     # ~150 ms (untimed, extra warm-up) so the timed steps start from the loaded power / clock
     # state instead of ramping out of idle inside a short timed region
+    # (in chunks of 8 whose continuation every rank agrees on: at G > 1 each forward is a
+    # lock-step of all ranks, so every rank must run the same number of them)
     t_settle = time.time()
     i_settle = 0
-    while time.time() - t_settle < 0.15 or i_settle < 3:
-        layer.forward(xs[i_settle % N_ROTATE], out)
-        i_settle += 1
-        if i_settle % 8 == 0:
-            torch.cuda.synchronize()
+    while True:
+        for _ in range(8):
+            layer.forward(xs[i_settle % N_ROTATE], out)
+            i_settle += 1
+        torch.cuda.synchronize()
+        if not agree_max(time.time() - t_settle < 0.15, world, dev):
+            break
     barrier()
     torch.cuda.synchronize()
     sampler.mark("start")
@@ -489,6 +508,7 @@ def main_b200(args):
     # (>= 150 ms of them, like the device-timed region's settle phase, so the timed batches run
     # in the loaded power state)
     n_pre = max(2, min(args.warmup, 4), min(64, int(np.ceil(150.0 / max(t_ms / K, 1e-3)))))
+    n_pre = agree_max(n_pre, world, dev)  # the same number of forwards on every rank
     for i in range(n_pre):
         pipe.submit(xh[i % N_ROTATE], oh[i % N_ROTATE])
     e0 = torch.cuda.Event(enable_timing=True)

@@ -231,6 +231,13 @@ int mp_layer_read_counts(mp_layer* layer, int32_t* host_counts, void* stream);
 /* Barrier/peer error word (0 = ok); synchronises the stream. */
 int mp_layer_check(mp_layer* layer, void* stream);
 
+/* Diagnostic: the NVLink flag protocol's device state at a quiescent point (synchronises
+ * `stream` and the layer's side stream).  out[16]: [0] epoch, [1] forwards seen, [2] count
+ * parity, [3] router / [4] permute / [5] GEMM2 arrival tickets, [6] timeout bits, [7] nonzero
+ * router count accumulators, [8 + p] flags[p] of this rank's window (p < G).  Between
+ * forwards every rank holds the same epoch, every flag equals it and [3..7] are 0. */
+int mp_layer_sync_state(mp_layer* layer, uint32_t* out, void* stream);
+
 /* K6 -- executes the slot diff of migration_cost (cost.py:186-187) adopted by
  * should_migrate (cost.py:217-248): copy expert slots into local slots, from a
  * peer GPU's pool over NVLink (src_rank != rank) or locally, on `stream`

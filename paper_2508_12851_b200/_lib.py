@@ -45,7 +45,7 @@ EXPORTED_SYMBOLS = (
     "mp_layer_open_peers", "mp_layer_set_routes", "mp_layer_prepare_router", "mp_layer_forward",
     "mp_layer_forward_timed", "mp_layer_route", "mp_layer_permute", "mp_layer_experts", "mp_layer_combine_gather",
     "mp_layer_last_launches", "mp_layer_config", "mp_layer_read_counts", "mp_layer_check", "mp_layer_migrate",
-    "mp_layer_peer_probe",
+    "mp_layer_peer_probe", "mp_layer_sync_state",
 )
 
 
@@ -115,6 +115,7 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
         "mp_layer_last_launches": ([V], I),
         "mp_layer_config": ([V, I], I),
         "mp_layer_read_counts": ([V, V, V], I),
+        "mp_layer_sync_state": ([V, V, V], I),
         "mp_layer_check": ([V, V], I),
         "mp_layer_migrate": ([V, POINTER(CopyOp), I, V, V], I),
         "mp_layer_peer_probe": ([V, I, I64, I, V, POINTER(ctypes.c_float)], I),

@@ -948,6 +948,25 @@ int mp_layer_check(mp_layer* L, void* stream) {
   return MP_OK;
 }
 
+int mp_layer_sync_state(mp_layer* L, uint32_t* out, void* stream) {
+  if (!L || !out) return set_error(MP_E_ARG, "mp_layer_sync_state: null pointer");
+  DeviceGuard dg(L->desc.device);
+  MP_CUDA(dg.status);
+  MP_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  if (L->side) MP_CUDA(cudaStreamSynchronize(L->side));
+  for (int i = 0; i < 16; ++i) out[i] = 0;
+  MP_CUDA(cudaMemcpy(out, L->sync_state, 3 * 4, cudaMemcpyDeviceToHost));
+  MP_CUDA(cudaMemcpy(out + 3, L->ticket, 4, cudaMemcpyDeviceToHost));
+  MP_CUDA(cudaMemcpy(out + 4, L->perm_ticket, 4, cudaMemcpyDeviceToHost));
+  MP_CUDA(cudaMemcpy(out + 5, L->ret_ticket, 4, cudaMemcpyDeviceToHost));
+  MP_CUDA(cudaMemcpy(out + 6, L->err, 4, cudaMemcpyDeviceToHost));
+  int32_t acc[64];
+  MP_CUDA(cudaMemcpy(acc, L->count_acc, sizeof(acc), cudaMemcpyDeviceToHost));
+  for (int e = 0; e < 64; ++e) out[7] += acc[e] != 0;
+  if (L->G > 1) MP_CUDA(cudaMemcpy(out + 8, L->flags, size_t(L->G) * 4, cudaMemcpyDeviceToHost));
+  return MP_OK;
+}
+
 int mp_layer_peer_probe(mp_layer* L, int peer, int64_t bytes, int reps, void* stream, float* ms_per_copy) {
   if (!L || !ms_per_copy) return set_error(MP_E_ARG, "mp_layer_peer_probe: null pointer");
   if (peer < 0 || peer >= L->G || peer == L->rank) return set_error(MP_E_ARG, "mp_layer_peer_probe: peer %d", peer);

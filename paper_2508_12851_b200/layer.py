@@ -255,6 +255,13 @@ class B200MoELayer:
     def check(self) -> None:
         _lib.check(self.lib.mp_layer_check(self._h, self._stream()), "mp_layer_check")
 
+    def sync_state(self) -> np.ndarray:
+        """Flag-protocol state at a quiescent point (synchronises): see mp_layer_sync_state."""
+        out = np.zeros(16, dtype=np.uint32)
+        _lib.check(self.lib.mp_layer_sync_state(self._h, out.ctypes.data_as(ctypes.c_void_p), self._stream()),
+                   "mp_layer_sync_state")
+        return out
+
     # ------------------------------------------------------------------ statistics / accounting
     def activation_counts(self) -> np.ndarray:
         """Cumulative per-expert token counts of this origin (fused router histogram)."""

@@ -101,3 +101,32 @@ def test_multi_rank_host_logic_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert sorted(res) == [(r, "ok") for r in range(world)], res
+
+
+def _agree_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import bench
+
+        # loop counts a rank derives from its own clock (settle length, e2e pre-batches) differ
+        # across ranks; bench.agree_max makes every rank run the same number of forwards
+        n = bench.agree_max(3 + 4 * rank, world, torch.device("cpu"))
+        go = bench.agree_max(rank == world - 1, world, torch.device("cpu"))
+        q.put((rank, n, go))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_loop_counts_agree_gloo():
+    world, port = 2, _port()
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_agree_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+        assert p.exitcode == 0
+    got = sorted(q.get() for _ in range(world))
+    assert got == [(0, 7, 1), (1, 7, 1)]
