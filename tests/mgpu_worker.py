@@ -30,6 +30,20 @@ from paper_2508_12851_b200.shapes import LayerShape
 NCCL_GROUP = None
 
 
+def assert_protocol_quiescent(layer, G, tag):
+    """Between forwards the NVLink flag protocol is at rest on every rank: one epoch
+    everywhere, every flag of every window equal to it, arrival tickets / router count
+    accumulator / timeout bits zero (mp_layer_sync_state)."""
+    st = [int(v) for v in layer.sync_state()]
+    allst = [None] * G
+    dist.all_gather_object(allst, st)
+    ep = allst[0][0]
+    for r, s in enumerate(allst):
+        assert s[0] == ep, f"{tag}: rank {r} epoch {s[0]} != {ep}"
+        assert s[8:8 + G] == [ep] * G, f"{tag}: rank {r} flags {s[8:8 + G]} != {ep}"
+        assert s[3:8] == [0] * 5, f"{tag}: rank {r} tickets / accumulator / err {s[3:8]}"
+
+
 def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None, expect_rounds=0, staging=1):
     """expect: K3 plan keys (B200MoELayer.exec_plan) the first forward must have run, so the
     production plans -- CTA-pair tiles with the NVLink-scatter GEMM2 epilogue; the split plan
@@ -90,6 +104,7 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None, 
     layer.check()
     dist.barrier()
     assert torch.equal(gout, out_a), "graph replay differs from eager forward"
+    assert_protocol_quiescent(layer, G, "after graph replay")
     # the NCCL all-to-all-v transport (the K4 A/B arm) runs the same kernels as stages with NCCL
     # moving the rows: bit-identical outputs and routing
     from paper_2508_12851_b200.nccl_path import NcclForward
@@ -120,6 +135,7 @@ def run_case(shape, G, rank, sets, sets2, T_list, seed, caps=None, expect=None, 
         assert np.array_equal(w2.float().cpu().numpy(), experts[e][2]), f"migrated W2 of expert {e}"
     layer.check()
     check(route2, "placement B (after migration)")
+    assert_protocol_quiescent(layer, G, "end of case")
     layer.close()
 
 

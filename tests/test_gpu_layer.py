@@ -100,6 +100,10 @@ def test_layer_repeated_forwards_accumulate_histogram():
     idx = orc.topk_route(orc.router_logits(x, wg, bias), shape.E, shape.k, 0)[0]
     assert np.array_equal(layer.activation_counts(), 2 * orc.histogram(idx, shape.E))
     assert layer.last_launches() >= 5
+    # the router's last-CTA ticket and batch-count accumulator are back at zero between
+    # forwards (mp_layer_sync_state [3], [7]); no peer protocol at G = 1
+    st = layer.sync_state()
+    assert st[3] == 0 and st[7] == 0 and st[6] == 0, st
     layer.close()
 
 
