@@ -143,6 +143,7 @@ struct mp_layer {
   int last_small_grid = 0;
   // small-group split: groups below split_m rows run on a side stream over small_grid SMs
   int split_m = 0, small_grid = 20;
+  int tail_max = 0;  // split plans: pair-tile tails of up to tail_max rows go to the side chain
   bool small_grid_fixed = false;  // MP_GEMM_SMALL_GRID pins it; else chosen per forward
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -420,6 +421,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   // the shared expert rides in the routed launches (either kernel) as the aux problem
   L->fuse_shared = (D.shared_f > 0 && D.n_slots > 0) ? 1 : 0;
   if (const char* env = getenv("MP_STREAM_ROWS")) L->stream_rows = atoi(env);
+  if (const char* env = getenv("MP_GEMM_TAILS")) L->tail_max = atoi(env);
   if (const char* env = getenv("MP_FUSE_SHARED")) L->fuse_shared = L->fuse_shared && atoi(env) != 0;
   if (D.shared_f > 0) {
     if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
@@ -682,6 +684,12 @@ int stage_experts(mp_layer* L, int T, const int32_t* counts_all, const uint32_t*
       GroupSpec gsmall = gs;
       gsmall.m_hi = L->split_m;
       gs.m_lo = L->split_m;
+      if (pr && L->tail_max > 0) {  // big groups' short pair-tile tails -> the 1-CTA side chain
+        gs.tail_role = 1;
+        gsmall.tail_role = 2;
+        gs.tail_max = gsmall.tail_max = L->tail_max;
+        gs.tail_block = gsmall.tail_block = 256;
+      }
       MP_CUDA(cudaEventRecord(L->ev_fork, st));
       MP_CUDA(cudaStreamWaitEvent(L->side, L->ev_fork, 0));
       MP_TRY(mk.mark_on(11, L->side));

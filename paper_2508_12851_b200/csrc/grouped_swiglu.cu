@@ -67,7 +67,9 @@ struct TileCoord {
 template <class Tail>
 MP_DEV uint32_t group_row_sources(const Tail& st, const GroupSpec& gs, int g, int r0, int r1) {
   if (gs.mode != 1 || !gs.per_source) return 0xffu;
-  const int e = st.g_expert[g];
+  const int e = st.g_expert[g] & 0xff, roff = st.g_expert[g] >> 8;  // a tail group starts at roff
+  r0 += roff;
+  r1 += roff;
   const int32_t* counts = gs.counts + (gs.parity ? size_t(*gs.parity) * gs.G * gs.E : 0);
   uint32_t mask = 0;
   int acc = 0;
@@ -118,20 +120,38 @@ MP_DEV void load_groups(Tail& st, const GroupSpec& gs, int bm, int n_blocks) {
       const int tot0 = __shfl_sync(0xffffffffu, p0, 31);
       const int p1 = warp_incl_scan(m[1]);
       const int row[2] = {p0 - m[0], tot0 + p1 - m[1]};
-      const bool sel0 = m[0] > 0 && m[0] >= gs.m_lo && m[0] < gs.m_hi;
-      const bool sel1 = m[1] > 0 && m[1] >= gs.m_lo && m[1] < gs.m_hi;
-      const unsigned b0 = __ballot_sync(0xffffffffu, sel0), b1 = __ballot_sync(0xffffffffu, sel1);
+      bool sel[2];
+      int gm[2], roff[2] = {0, 0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int mh = m[h];
+        sel[h] = mh > 0 && mh >= gs.m_lo && mh < gs.m_hi;
+        gm[h] = mh;
+        if (gs.tail_role != 0) {  // big group: m >= the split threshold
+          const bool big = mh >= (gs.tail_role == 1 ? gs.m_lo : gs.m_hi);
+          const int tail = big ? mh % gs.tail_block : 0;
+          if (tail > 0 && tail <= gs.tail_max) {
+            if (gs.tail_role == 1) {
+              gm[h] = mh - tail;  // body
+            } else {
+              sel[h] = true;      // tail
+              gm[h] = tail;
+              roff[h] = mh - tail;
+            }
+          }
+        }
+      }
+      const unsigned b0 = __ballot_sync(0xffffffffu, sel[0]), b1 = __ballot_sync(0xffffffffu, sel[1]);
       const unsigned lt = (1u << lane) - 1u;
       const int idx[2] = {__popc(b0 & lt), __popc(b0) + __popc(b1 & lt)};
-      const bool sel[2] = {sel0, sel1};
 #pragma unroll
       for (int h = 0; h < 2; ++h)
         if (sel[h]) {
-          st.g_arow[idx[h]] = row[h];
-          st.g_m[idx[h]] = m[h];
+          st.g_arow[idx[h]] = row[h] + roff[h];
+          st.g_m[idx[h]] = gm[h];
           st.g_slot[idx[h]] = slot[h];
-          st.g_orow[idx[h]] = row[h];
-          st.g_expert[idx[h]] = lane + 32 * h;
+          st.g_orow[idx[h]] = row[h] + roff[h];
+          st.g_expert[idx[h]] = (lane + 32 * h) | (roff[h] << 8);
         }
       if (lane == 0) st.n_groups = __popc(b0) + __popc(b1);
     }

@@ -117,6 +117,11 @@ struct GroupSpec {
   int single_m = 0;                   // mode 2: one group {0, single_m, slot 0, 0}
   int mode = 0;
   int m_lo = 0, m_hi = 1 << 30;       // mode 1: only groups with m_lo <= m < m_hi
+  // mode 1, split plans: a big group's last partial CTA-pair tile (tail = m % tail_block rows,
+  // 0 < tail <= tail_max) runs on the 1-CTA side chain as its own group, so the pair tile does
+  // not pad it to tail_block rows.  tail_role 1: this launch takes the big groups less their
+  // tails (m_lo = the threshold); 2: the small groups plus the tails (m_hi = the threshold)
+  int tail_role = 0, tail_block = 256, tail_max = 0;
   int per_source = 1;                 // mode 1: a routed tile waits only for its rows' source ranks
 };
 // A second, dense problem fused into the same CTA-pair launch (the shared
