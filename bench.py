@@ -942,6 +942,32 @@ def main_shift(args):
         tps_b_mig, _ = run(args.steps)
         acc_b_mig = dispatch_accounting(all_counts(), layer.route, shape.d)
 
+    # ---- parity of the forward on the final placement (after the migration when adopted): 32
+    # tokens per rank against the fp32 restatement of the layer math (tests/torch_ref.py) under
+    # the stated tolerance (tests/tolerance.py), routing taken from the layer's own router
+    chk = torch.empty_like(out)
+    layer.forward(xs[0], chk)
+    torch.cuda.synchronize()
+    sys.path.insert(0, str(REPO / "tests"))
+    from tolerance import check_layer_close
+    from torch_ref import layer_reference
+    n_chk = min(32, T)
+    shared_w = wl.shared_weights(shape.d, shape.shared_f, dev, seed) if shape.shared_f else None
+    gate = layer.shared_gate[:n_chk] if shape.shared_gate else None
+    ref, mag, mag2 = layer_reference(xs[0][:n_chk], layer.idx[:n_chk], layer.gate_w[:n_chk], expert_src, shared_w, gate)
+    try:
+        st = check_layer_close(chk[:n_chk].float().cpu().numpy(), ref.cpu().numpy(), mag.cpu().numpy(),
+                               mag2.cpu().numpy(), "post-migration forward")
+        used, ok = st["max_err_over_bound"], 1.0
+    except AssertionError:
+        used, ok = float("inf"), 0.0
+    pv = torch.tensor([used if used != float("inf") else 1e30, -ok], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(pv, op=dist.ReduceOp.MAX)
+    parity = {"tokens_per_rank": n_chk, "placement": "migrated" if tps_b_mig is not None else "static",
+              "max_err_over_bound": pv[0].item(), "ok": pv[1].item() == -1.0,
+              "reference": "fp32 restatement (tests/torch_ref.py), bound of tests/tolerance.py"}
+
     if rank == 0:
         keep = ("remote_invocations", "remote_bytes", "local_ratio")
         line = {"scenario": "workload-shift (BASELINE config 5)", "metric": METRIC, "unit": UNIT, "n_gpus": G,
@@ -951,7 +977,8 @@ def main_shift(args):
                 "phase_b_static": {"value": tps_b_static, **{k: acc_b_static[k] for k in keep}},
                 "migration": mig,
                 "phase_b_migrated": None if tps_b_mig is None else
-                {"value": tps_b_mig, **{k: acc_b_mig[k] for k in keep}}}
+                {"value": tps_b_mig, **{k: acc_b_mig[k] for k in keep}},
+                "parity": parity}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
