@@ -284,7 +284,13 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int j = 0; j < K; ++j) wj[j] = w[size_t(t) * K + j];
   const float g = shared_gate ? shared_gate[t] : 1.0f;
-  const int nvec = d / 8;
+  // blockIdx.y: this CTA's column slice of the token rows (more, smaller CTAs even out the
+  // per-SM work of a one-wave grid)
+  const int nvec = d / 8 / int(gridDim.y), c_base = int(blockIdx.y) * nvec;
+#pragma unroll
+  for (int j = 0; j < K; ++j) rows[j] += size_t(8) * c_base;
+  if (shared_y) shared_y += size_t(8) * c_base;
+  out += size_t(8) * c_base;
   // U column vectors per lane per batch: all their loads are issued before any
   // of their stores (the asm loads / stores keep program order, so an unbatched
   // loop would serialise one load round trip per vector)
@@ -341,12 +347,16 @@ int launch_combine(const __nv_bfloat16* ret, const float* w, int T, int d, int k
   if (k < 1 || k > 8) return set_error(MP_E_SHAPE, "combine: top_k=%d outside [1, 8]", k);
   if (T <= 0) return MP_OK;
   const int grid = (T + 7) / 8;
+  // column slices: 1 unless MP_COMBINE_SLICES asks (each slice keeps >= 32 vectors per row)
+  int ny = 1;
+  if (const char* env = getenv("MP_COMBINE_SLICES")) ny = std::max(1, atoi(env));
+  while (ny > 1 && ((d / 8) % ny != 0 || (d / 8) / ny < 32)) ny /= 2;
   const PeerSync ps = sync ? *sync : PeerSync();
   cudaError_t e = cudaSuccess;
   switch (k) {
 #define MP_COMBINE_CASE(N) \
   case N:                                                                                                  \
-    e = launch_pdl(combine_kernel<N>, dim3(grid), dim3(256), 0, stream, ret, w, T, d, shared_y, shared_gate, out, ps, \
+    e = launch_pdl(combine_kernel<N>, dim3(grid, ny), dim3(256), 0, stream, ret, w, T, d, shared_y, shared_gate, out, ps, \
                    bases, pos_dst, pos_row);                                                                \
     break;
     MP_COMBINE_CASE(1) MP_COMBINE_CASE(2) MP_COMBINE_CASE(3) MP_COMBINE_CASE(4)
