@@ -36,3 +36,20 @@ def test_multi_gpu_layer_matches_oracle(G):
     sys.stderr.write(res.stderr[-8000:])
     assert res.returncode == 0
     assert f"mgpu ok: G={G}" in res.stdout
+
+
+@pytest.mark.parametrize("G,config,steps", [(2, "toy", 4000), (4, "deepseek", 2000)])
+def test_flag_protocol_soak(G, config, steps):
+    """Thousands of back-to-back forwards at G > 1 (tools/soak.py): between chunks every rank's
+    protocol state (mp_layer_sync_state) must show one epoch, all flags equal to it, arrival
+    tickets and the router accumulator at zero and no timeout bits."""
+    if torch.cuda.device_count() < G:
+        pytest.skip(f"needs {G} GPUs, have {torch.cuda.device_count()}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(REPO / "tools" / "soak.py"),
+           "--gpus", str(G), "--config", config, "--steps", str(steps), "--warmup", "3", "--chunk=500"]
+    res = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=600)
+    sys.stdout.write(res.stdout[-2000:])
+    sys.stderr.write(res.stderr[-4000:])
+    assert res.returncode == 0
+    assert '"ok": true' in res.stdout
