@@ -53,3 +53,20 @@ def test_flag_protocol_soak(G, config, steps):
     sys.stderr.write(res.stderr[-4000:])
     assert res.returncode == 0
     assert '"ok": true' in res.stdout
+
+
+def test_multi_gpu_tail_split_plan_matches_oracle():
+    """The opt-in tail split (MP_GEMM_TAILS: big groups' short CTA-pair tails on the side chain)
+    through the same G = 2 cases, production split plans included."""
+    G = 2
+    if torch.cuda.device_count() < G:
+        pytest.skip(f"needs {G} GPUs, have {torch.cuda.device_count()}")
+    import os
+    env = dict(os.environ, MP_GEMM_TAILS="128")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(REPO / "tests" / "mgpu_worker.py")]
+    res = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=900, env=env)
+    sys.stdout.write(res.stdout[-4000:])
+    sys.stderr.write(res.stderr[-8000:])
+    assert res.returncode == 0
+    assert f"mgpu ok: G={G}" in res.stdout
