@@ -76,6 +76,10 @@ MP_DEV uint32_t cluster_ctarank() {
 MP_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Split cluster barrier: arrive early (no ordering), wait later -- e.g. "every CTA of the
+// cluster has started" before the first distributed-shared-memory store.
+MP_DEV void cluster_arrive_relaxed() { asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory"); }
+MP_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 // Arrive on the mbarrier at the same smem offset in CTA `cta` of the cluster.
 MP_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
   asm volatile(

@@ -382,6 +382,7 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  cluster_arrive_relaxed();  // this CTA has started (waited on before the first DSMEM store)
   const uint32_t tmem = *tmem_slot;
   // rows of the tile this CTA selects: router blocks b (32 tokens) with b % split == rank
   const int own_blocks = (4 - int(rank) + split - 1) / split;
@@ -420,6 +421,7 @@ __global__ void __launch_bounds__(ri::kBlock, 1)
 
   // ---- 1. per-row maxima of |x| over this CTA's K range, shared with the cluster.  A warp
   // takes 8 rows at a time with every lane's loads of all 8 in flight before any is used.
+  cluster_wait();  // every CTA of the cluster has started: its shared memory takes remote stores
   {
     const int kc = nk * ri::kKB / 8;  // 16-byte chunks of one row's range (a multiple of 16)
     const int per = kc / 16;          // chunks per half-warp and row: lanes 0-15 / 16-31 split a row
