@@ -770,6 +770,14 @@ static int layer_forward(mp_layer* L, const void* x, void* out, int T, void* str
     ps0.err = L->err;
     ps0.err_host = L->err_host_d;
     ps0.G = G;
+    // one bounded peer wait: 30 s, or MP_PEER_TIMEOUT_MS (tests), capped below the 40 s
+    // mbarrier bound of the warps that wait behind a waiting producer
+    static const uint64_t timeout_ns = [] {
+      const char* env = getenv("MP_PEER_TIMEOUT_MS");
+      const long long ms = env ? atoll(env) : 30000;
+      return uint64_t(std::min(std::max(ms, 1ll), 30000ll)) * 1000000ull;
+    }();
+    ps0.timeout_ns = timeout_ns;
     ps0.rank = rank;
   }
   PeerSync ps_wait = ps0, ps_perm = ps0, ps_ret = ps0;

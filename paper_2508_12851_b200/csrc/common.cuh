@@ -56,7 +56,7 @@ MP_DEV uint32_t mbar_try_wait(uint32_t addr, uint32_t parity) {
 MP_DEV uint64_t globaltimer_ns();
 // Wait for the phase with `parity` to complete.  A protocol bug must not hang the GPU:
 // after 40 s the kernel traps instead.  The bound is wall time and longer than the NVLink
-// peer waits' 30 s (kPeerTimeoutNs), so a warp parked behind a producer that legitimately
+// peer waits' 30 s (PeerSync::timeout_ns, one bound per multi-rank wait), so a warp parked behind a producer that legitimately
 // waits for a slow peer (e.g. a host-bound rank) is never the one that traps.
 MP_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
@@ -292,7 +292,6 @@ MP_DEV uint64_t globaltimer_ns() {
 // async-proxy (TMA) global reads.
 MP_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-constexpr uint64_t kPeerTimeoutNs = 30ull * 1000ull * 1000ull * 1000ull;
 
 // 16-byte streaming load / store.
 // 16-byte asynchronous global -> shared copy (L2 only), grouped per thread.

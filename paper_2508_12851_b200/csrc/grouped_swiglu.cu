@@ -435,8 +435,9 @@ __global__ void __launch_bounds__(gg::kThreads, 1)
         if (waits && !j.aux) {
           uint32_t need = group_row_sources(st, gs, j.g, j.m_row0, min(j.m_row0 + gg::BM, j.m_rows)) & ~ready;
           if (need) {
+            const uint64_t t0 = globaltimer_ns();
             for (int p = 0; p < sync.G; ++p)
-              if (need >> p & 1u) peer_wait_one(sync, p, epoch);
+              if (need >> p & 1u) peer_wait_one(sync, p, epoch, t0);
             fence_proxy_async_global();
             ready |= need;
           }
@@ -632,8 +633,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gg::kThreads, 1)
           const int r0 = j.m_row0 + int(rank) * 128;
           uint32_t need = r0 < j.m_rows ? group_row_sources(st, gs, j.g, r0, min(r0 + 128, j.m_rows)) & ~ready : 0u;
           if (need) {
+            const uint64_t t0 = globaltimer_ns();
             for (int p = 0; p < sync.G; ++p)
-              if (need >> p & 1u) peer_wait_one(sync, p, epoch);
+              if (need >> p & 1u) peer_wait_one(sync, p, epoch, t0);
             fence_proxy_async_global();
             ready |= need;
           }

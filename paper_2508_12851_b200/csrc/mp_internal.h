@@ -59,6 +59,7 @@ struct PeerSync {
   int G = 1, rank = 0;
   int wait = 0;    // this launch waits for state[0] before touching peer-written rows
   int total = 0;   // this launch raises once `total` CTAs (across launches sharing ticket) arrived
+  uint64_t timeout_ns = 30ull * 1000ull * 1000ull * 1000ull;  // bound of one wait (MP_PEER_TIMEOUT_MS)
 };
 
 // Error state (thread-local, read through mp_last_error).

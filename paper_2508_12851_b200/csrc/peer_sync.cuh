@@ -1,5 +1,5 @@
 // Device side of PeerSync (mp_internal.h): the NVLink flag protocol folded into
-// the layer kernels.  All waits are bounded (kPeerTimeoutNs): on timeout the
+// the layer kernels.  All waits are bounded (PeerSync::timeout_ns, 30 s): on timeout the
 // missing ranks' bits are set in the error word -- in device memory for
 // mp_layer_check and in mapped host memory, which the next mp_layer_forward
 // reads before launching anything and turns into MP_E_PEER -- and the kernel
@@ -13,12 +13,15 @@ namespace mp {
 
 MP_DEV bool peer_on(const PeerSync& ps) { return ps.G > 1 && ps.flag_ptrs != nullptr; }
 
-// One thread: spin until rank p's flag in this rank's window reached `epoch`.
-MP_DEV void peer_wait_one(const PeerSync& ps, int p, uint32_t epoch) {
+// One thread: spin until rank p's flag in this rank's window reached `epoch`, at most until
+// t0 + ps.timeout_ns -- t0 is the start of the caller's whole wait, so a wait on several
+// ranks is bounded once (below the 40 s mbarrier bound of the warps waiting behind it).  A
+// rank this layer already marked lost is not waited for again.
+MP_DEV void peer_wait_one(const PeerSync& ps, int p, uint32_t epoch, uint64_t t0) {
   const uint32_t* mine = ps.flag_ptrs[ps.rank];
-  const uint64_t t0 = globaltimer_ns();
   while (int32_t(ld_acquire_sys_u32(mine + p) - epoch) < 0) {
-    if (globaltimer_ns() - t0 > kPeerTimeoutNs) {
+    if ((*reinterpret_cast<volatile uint32_t*>(ps.err) >> p) & 1u) break;
+    if (globaltimer_ns() - t0 > ps.timeout_ns) {
       const uint32_t bits = atomicOr(ps.err, 1u << p) | (1u << p);
       if (ps.err_host != nullptr) st_release_sys_u32(ps.err_host, bits);
       break;
@@ -29,7 +32,8 @@ MP_DEV void peer_wait_one(const PeerSync& ps, int p, uint32_t epoch) {
 
 // One thread: spin until every rank's flag in this rank's window reached `epoch`.
 MP_DEV void peer_wait(const PeerSync& ps, uint32_t epoch) {
-  for (int p = 0; p < ps.G; ++p) peer_wait_one(ps, p, epoch);
+  const uint64_t t0 = globaltimer_ns();
+  for (int p = 0; p < ps.G; ++p) peer_wait_one(ps, p, epoch, t0);
 }
 
 // One thread: raise `epoch` in every rank's window (flags[rank]).

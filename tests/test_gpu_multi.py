@@ -70,3 +70,20 @@ def test_multi_gpu_tail_split_plan_matches_oracle():
     sys.stderr.write(res.stderr[-8000:])
     assert res.returncode == 0
     assert f"mgpu ok: G={G}" in res.stdout
+
+
+def test_lost_peer_fails_loudly_without_trap():
+    """A rank that stops calling forward: its peer's waits time out (bounded once per wait, no
+    kernel trap), check() names the lost rank and the next forward refuses to launch."""
+    G = 2
+    if torch.cuda.device_count() < G:
+        pytest.skip(f"needs {G} GPUs, have {torch.cuda.device_count()}")
+    import os
+    env = dict(os.environ, MP_PEER_TIMEOUT_MS="2000")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={G}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(REPO / "tests" / "mgpu_lost_peer.py")]
+    res = subprocess.run(cmd, cwd=REPO, capture_output=True, text=True, timeout=300, env=env)
+    sys.stdout.write(res.stdout[-2000:])
+    sys.stderr.write(res.stderr[-4000:])
+    assert res.returncode == 0
+    assert "lost-peer ok" in res.stdout
