@@ -152,10 +152,13 @@ def main():
     NCCL_GROUP = dist.new_group(backend="nccl")
     only = os.environ.get("MGPU_CASES")  # optional subset, e.g. "prod" (production plans only)
 
-    if only != "prod":
-        small_cases(G, rank)
-        tight_cap_case(G, rank)
-    production_cases(G, rank)
+    if only == "rand":  # randomised cases only, seeds from MGPU_RAND_SEEDS (a fuzz run)
+        random_cases(G, rank, [int(v) for v in os.environ.get("MGPU_RAND_SEEDS", "11,12").split(",")])
+    else:
+        if only != "prod":
+            small_cases(G, rank)
+            tight_cap_case(G, rank)
+        production_cases(G, rank)
 
     dist.barrier()
     if rank == 0:
@@ -250,9 +253,13 @@ def small_cases(G, rank):
     caps = [max(len(x) for x in sets)] * (G - 1) + [0]
     run_case(shape, G, rank, sets, sets, [100 + 20 * s for s in range(G)], seed=5, caps=caps, staging=0)
 
+    random_cases(G, rank, (11, 12))
+
+
+def random_cases(G, rank, seeds):
     # case 6: randomised shapes and placements (every rank draws the same ones): replicated
     # experts, ragged T including empty origins, migration between two random placements
-    for seed in (11, 12):
+    for seed in seeds:
         r = np.random.default_rng(seed * 100 + G)
         E = int(r.choice([8, 16, 60, 64]))
         k = int(r.integers(1, min(6, E) + 1))
@@ -268,7 +275,8 @@ def small_cases(G, rank):
                     held[int(g)].add(e)
             return [sorted(h) for h in held]
         sets, sets2 = random_sets(), random_sets()
-        T_list = [int(t) for t in r.integers(0, 300, size=G)]
+        # seeds >= 100 draw batches up to 3000 tokens, so the CTA-pair / split plans run too
+        T_list = [int(t) for t in r.integers(0, 3000 if seed >= 100 else 300, size=G)]
         T_list[int(r.integers(0, G))] = max(1, T_list[0])
         run_case(shape, G, rank, sets, sets2, T_list, seed=seed)
 
