@@ -9,6 +9,8 @@ The shapes cover every K3 plan (1-CTA only, CTA pairs, small-group side chain,
 fused shared expert) and every router variant.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -37,7 +39,11 @@ def _draw(seed):
     return shape, T, alpha
 
 
-@pytest.mark.parametrize("seed", range(40))
+# MP_FUZZ_SEEDS=a:b widens the sweep for a dedicated fuzz run (the suite default: 40 seeds)
+_SEEDS = range(*map(int, os.environ.get("MP_FUZZ_SEEDS", "0:40").split(":")))
+
+
+@pytest.mark.parametrize("seed", _SEEDS)
 def test_random_layer_matches_oracle(seed):
     from paper_2508_12851_b200.layer import B200MoELayer
     shape, T, alpha = _draw(seed)
