@@ -144,6 +144,7 @@ struct mp_layer {
   // small-group split: groups below split_m rows run on a side stream over small_grid SMs
   int split_m = 0, small_grid = 20;
   int tail_max = 0;  // split plans: pair-tile tails of up to tail_max rows go to the side chain
+  int side_shared_rows = 0;  // split plans: the fused shared expert's last rows run on the side chain
   bool small_grid_fixed = false;  // MP_GEMM_SMALL_GRID pins it; else chosen per forward
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -422,6 +423,7 @@ int mp_layer_create(const mp_layer_desc* desc, mp_layer** out) {
   L->fuse_shared = (D.shared_f > 0 && D.n_slots > 0) ? 1 : 0;
   if (const char* env = getenv("MP_STREAM_ROWS")) L->stream_rows = atoi(env);
   if (const char* env = getenv("MP_GEMM_TAILS")) L->tail_max = atoi(env);
+  if (const char* env = getenv("MP_SIDE_SHARED_ROWS")) L->side_shared_rows = atoi(env);
   if (const char* env = getenv("MP_FUSE_SHARED")) L->fuse_shared = L->fuse_shared && atoi(env) != 0;
   if (D.shared_f > 0) {
     if ((r = encode_tmap_bf16_2d(&L->tm_w13s, L->w13s, uint64_t(2) * D.shared_f, uint64_t(D.d), 256)) != MP_OK)
@@ -678,6 +680,28 @@ int stage_experts(mp_layer* L, int T, const int32_t* counts_all, const uint32_t*
     if (ps_ret) ps_ret->total = grouped_gemm_ctas(big_grid, pr) + (split ? grouped_gemm_ctas(small_grid, 0) : 0);
     const int32_t* scatter_src = ret_ptrs ? L->recv_src : nullptr;
     __nv_bfloat16* out2 = ret_ptrs ? L->ret : L->recv;
+    // the fused shared expert's last ms rows (a multiple of 256, so neither chain pads a tile)
+    // can ride on the side chain, whose weight-bound small groups leave it slack
+    const int ms = (split && fused) ? std::min(L->side_shared_rows / 256 * 256, T / 256 * 256) : 0;
+    AuxProblem saux1, saux2;
+    if (ms > 0) {
+      const size_t r0 = size_t(T - ms);
+      MP_TRY(encode_tmap_bf16_2d(&saux1.tmA, static_cast<const __nv_bfloat16*>(L->tm_x_ptr) + r0 * D.d,
+                                 uint64_t(ms), uint64_t(D.d), 128));
+      saux1.tmB = L->tm_w13s;
+      saux1.out = L->hs + r0 * D.shared_f;
+      saux1.out_ld = D.shared_f;
+      saux1.m = ms;
+      saux1.N = 2 * D.shared_f;
+      saux1.K = D.d;
+      MP_TRY(encode_tmap_bf16_2d(&saux2.tmA, L->hs + r0 * D.shared_f, uint64_t(ms), uint64_t(D.shared_f), 128));
+      saux2.tmB = L->tm_w2s;
+      saux2.out = L->ys + r0 * D.d;
+      saux2.out_ld = D.d;
+      saux2.m = ms;
+      saux2.N = D.d;
+      saux2.K = D.shared_f;
+    }
     if (split) {
       // fork: small groups (weight-bound) on the side stream over small_grid SMs, large
       // groups (compute-bound) on the main stream over the rest, then join
@@ -695,9 +719,10 @@ int stage_experts(mp_layer* L, int T, const int32_t* counts_all, const uint32_t*
       MP_TRY(mk.mark_on(11, L->side));
       // (no PDL on the split chains: early-scheduled CTAs would contend for the other chain's SMs)
       MP_TRY(launch_grouped_gemm(L->tm_recv, L->tm_w13, gsmall, 2 * D.f, D.d, 3 * D.f, 0, L->h, D.f, 1,
-                                 small_grid, L->side, 0, nullptr, nullptr, false, nullptr, sw));
+                                 small_grid, L->side, 0, nullptr, nullptr, false, ms > 0 ? &saux1 : nullptr, sw));
       MP_TRY(launch_grouped_gemm(L->tm_h, L->tm_w2, gsmall, D.d, D.f, 3 * D.d, 2 * D.d, out2, D.d, 0,
-                                 small_grid, L->side, 0, scatter_src, ret_ptrs, false, nullptr, ps_ret));
+                                 small_grid, L->side, 0, scatter_src, ret_ptrs, false, ms > 0 ? &saux2 : nullptr,
+                                 ps_ret));
       MP_TRY(mk.mark_on(12, L->side));
       MP_CUDA(cudaEventRecord(L->ev_join, L->side));
       launches += 2;
@@ -710,14 +735,14 @@ int stage_experts(mp_layer* L, int T, const int32_t* counts_all, const uint32_t*
       aux1.tmB = pr ? L->tm_w13s_p : L->tm_w13s;
       aux1.out = L->hs;
       aux1.out_ld = D.shared_f;
-      aux1.m = T;
+      aux1.m = T - ms;
       aux1.N = 2 * D.shared_f;
       aux1.K = D.d;
       aux2.tmA = L->tm_hs;
       aux2.tmB = pr ? L->tm_w2s_p : L->tm_w2s;
       aux2.out = L->ys;
       aux2.out_ld = D.d;
-      aux2.m = T;
+      aux2.m = T - ms;
       aux2.N = D.d;
       aux2.K = D.shared_f;
     }
